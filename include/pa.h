@@ -1,0 +1,170 @@
+/*
+ * pa.h — C ABI of libpa: the PA-SFM differentiable acoustic radiation operator
+ * (arXiv 2604.09643) on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n (the paper's LaTeX source), S:n = SPEC.md line n,
+ * R<k> = a reading of the paper listed in DESIGN.md §3.
+ *
+ * The operator (Eq. gpu_forward_model; Eq. 1):
+ *
+ *   traces[f][e][j] = sum_k p0[k] * D/(2r) * exp(-D^2 / (2 sigma^2)) * [|D| <= kappa*sigma]
+ *   r = |x_fe - y_k|,  D = r - c (t0 + j dt),  x_fe = R_f tmpl[e] + t_f  (Stage 4)
+ *   y_k = origin + pitch * (i, j, l),  k = i + nx*(j + ny*l)    (x fastest, R7)
+ *
+ * Units: mm, µs, mm/µs.  Arithmetic: fp32 with fp64 per-tile anchors.
+ *
+ * Conventions for every entry point
+ *   - Array arguments are caller-owned DEVICE pointers (cudaMalloc / torch), fp32,
+ *     C-contiguous, 4-byte aligned, unless stated "host".  Outputs are overwritten.
+ *     The library keeps no pointer after a call returns.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).  Kernels are
+ *     enqueued asynchronously on it.  Validation (arguments, supported window class,
+ *     degenerate geometry) runs before any output is written; the degenerate-geometry
+ *     check enqueues a tiny kernel and synchronises `stream` to read its verdict.
+ *   - F == 0 is a no-op returning PA_OK.
+ *   - Results are bitwise deterministic run-to-run for a fixed GPU, shapes and inputs
+ *     (no floating-point atomics; all reductions in fixed order).
+ *   - Errors: the status code; pa_last_error() returns a thread-local message.
+ *   - A pa_ctx owns only internal workspace (pose-gradient partials, scratch); use one
+ *     context per stream.  Calls on different contexts may run concurrently.
+ */
+#ifndef PA_H
+#define PA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PA_OK = 0,
+    PA_EINVAL = 1,        /* non-positive dims/pitch/c/dt/nt/sigma, kappa < 4, bad cfg       */
+    PA_ESHAPE = 2,        /* E < 1, F < 0, null or misaligned pointer                         */
+    PA_EDEGENERATE = 3,   /* an element lies within 1e-6 mm of a voxel centre (R10) */
+    PA_ECUDA = 4,         /* a CUDA call or launch failed                                     */
+    PA_ENOMEM = 5,        /* workspace allocation failed                                      */
+    PA_EUNSUPPORTED = 6   /* window/pitch ratio outside the compiled kernel classes           */
+} pa_status;
+
+/* Voxel grid.  Voxel (i,j,l) centre = origin + pitch*(i,j,l); p0[l][j][i]. */
+typedef struct {
+    int32_t nx, ny, nz;
+    float origin[3];
+    float pitch;
+} pa_grid;
+
+/* Acquisition + kernel.  Sample j at t0 + j*dt (R5); speed of sound c;
+ * Gaussian width sigma; window |D| <= kappa*sigma, kappa >= 4 (R4). */
+typedef struct {
+    float c, t0, dt;
+    int32_t nt;
+    float sigma, kappa;
+} pa_acq;
+
+typedef struct pa_ctx pa_ctx;
+
+/* Create a context bound to `device` (cudaSetDevice is NOT changed for the caller's thread
+ * beyond the duration of the call).  *ctx = NULL on failure. */
+pa_status pa_create(pa_ctx **ctx, int device);
+void pa_destroy(pa_ctx *ctx);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char *pa_last_error(void);
+
+/* Library version string. */
+const char *pa_version(void);
+
+/*
+ * a2 — forward radiation (Eq. gpu_forward_model).
+ *   tmpl   [E][3]      array template x^_e
+ *   poses  [F][12]     R_f row-major 3x3 then t_f (x_fe = R_f x^_e + t_f)
+ *   p0     [nz][ny][nx] initial-pressure amplitudes P_c
+ *   traces [F][E][nt]  output (overwritten)
+ */
+pa_status pa_forward(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                     const float *poses, int32_t F, const float *p0, float *traces, void *stream);
+
+/*
+ * a4 — adjoint back-projection, the exact transpose of pa_forward:
+ *   grad_p0[k] = sum_f sum_e sum_j cot[f][e][j] * D/(2r) exp(-D^2/2sigma^2) [|D| <= kappa sigma]
+ *   cot [F][E][nt] cotangent dL/dtraces;  grad_p0 [nz][ny][nx] output (overwritten).
+ */
+pa_status pa_adjoint(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                     const float *poses, int32_t F, const float *cot, float *grad_p0, void *stream);
+
+/*
+ * a5+a6 — pose gradient ("sensor spatial coordinates"; Stage 4 P:109-115):
+ *   grad_elem[f][e] = sum_k p0[k] sum_j cot[f][e][j] d/dr[D/(2r) e^{-D^2/2s^2}] (x_fe - y_k)/r
+ *                     (window indicator held constant, R11)
+ *   grad_pose[f] = [ dL/dR_f (row-major 3x3) = sum_e grad_elem[f][e] tmpl[e]^T , dL/dt_f = sum_e grad_elem[f][e] ]
+ *   grad_pose [F][12] output; grad_elem [F][E][3] output or NULL.
+ */
+pa_status pa_pose_grad(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                       const float *poses, int32_t F, const float *p0, const float *cot, float *grad_pose,
+                       float *grad_elem, void *stream);
+
+/* Fused a4+a5+a6 in one pass over (voxel, element, sample): both outputs of pa_adjoint and
+ * pa_pose_grad (identical values).  grad_elem may be NULL. */
+pa_status pa_adjoint_pose(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                          const float *poses, int32_t F, const float *p0, const float *cot, float *grad_p0,
+                          float *grad_pose, float *grad_elem, void *stream);
+
+/*
+ * Unit of work: exact number of (voxel, element, sample) terms with
+ * |D| <= kappa sigma and 0 <= j < nt, evaluated in fp64 with the literal predicate.
+ *   total (host, int64) ; per_frame (host [F] int64, nullable).  Synchronises `stream`.
+ */
+pa_status pa_count(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                   const float *poses, int32_t F, int64_t *total, int64_t *per_frame, void *stream);
+
+/*
+ * a3 — loss and cotangent from traces (Eq. 2 data term P:85 / Eq. 3 NC P:91-93, Eq. 4 mask P:112-114):
+ *   kind 0 (MSE): L = sum (y - S)^2, cot = 2 (y - S)
+ *   kind 1 (NC):  per row (f,e): L_fe = -cov(y,S)/(sd_y sd_S) (population), cot = dL/dy
+ *   y, S, cot [F][E][nt]; row_mask [F][E] uint8 or NULL (masked rows: zero loss and cotangent);
+ *   cot may alias y.  loss (device, 1 float) = sum of row losses in fixed order.
+ */
+pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, const uint8_t *row_mask, int32_t F,
+                  int32_t E, int32_t nt, float *cot, float *loss, void *stream);
+
+/* All-reduce callback (sum, in place, on `stream`) — lets the caller's NCCL process group
+ * combine dL/dp0 across frame shards (Stage 5).  Return 0 on success.  NULL = one rank. */
+typedef int (*pa_allreduce_fn)(float *buf, size_t n, void *stream, void *user);
+
+typedef struct {
+    float lr_p0, lr_rot, lr_trans;  /* Adam learning rates: p0, Euler angles, translation        */
+    float beta1, beta2, eps;        /* Adam                                     */
+    int32_t step;                   /* Adam step t >= 1 (bias correction)                         */
+    int32_t loss_kind;              /* 0 MSE (Eq. 2), 1 NC (Eq. 3/4)                              */
+    int32_t update_p0, update_pose; /* apply the p0 / pose updates                                */
+} pa_step_cfg;
+
+/*
+ * One SfM iteration over this rank's F frames (Alg. 1 Stages 1/4/5 objective):
+ *   poses <- Euler ZYX(euler_t) (R8), y = forward(p0), (L, cot) = loss(y, meas),
+ *   grad_p0 = adjoint(cot) [all-reduced across ranks by `ar`], grad_pose, dL/dEuler,
+ *   Adam on p0 with clamp p0 >= 0, Adam on euler_t (angles lr_rot, translation lr_trans).
+ *   meas      [F][E][nt]   measured traces S
+ *   row_mask  [F][E] uint8 or NULL
+ *   p0        [nz][ny][nx] in/out;   euler_t [F][6] (a, b, c, tx, ty, tz) in/out
+ *   adam_p0   [2][nz*ny*nx] (m, v) in/out;   adam_pose [2][F][6] in/out
+ *   grad_p0   [nz*ny*nx]   out (after the all-reduce), caller-owned so `ar` can name it
+ *   loss      [2]          out: local loss, global loss (after `ar` on a copy)
+ *   grad_euler [F][6]      out or NULL
+ */
+pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E, int32_t F,
+                  const float *meas, const uint8_t *row_mask, float *p0, float *euler_t, float *adam_p0,
+                  float *adam_pose, const pa_step_cfg *cfg, pa_allreduce_fn ar, void *user, float *grad_p0,
+                  float *loss, float *grad_euler, void *stream);
+
+/* Kernel-level timing of the last pa_step / pa_forward / pa_adjoint_pose call on this context
+ * (CUDA events recorded on `stream`): ms of the forward kernel and of the adjoint+pose kernel.
+ * Synchronises the events.  Either pointer may be NULL. */
+pa_status pa_last_kernel_ms(pa_ctx *ctx, float *forward_ms, float *adjoint_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PA_H */

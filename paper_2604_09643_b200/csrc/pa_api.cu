@@ -1,0 +1,844 @@
+// pa_api.cu — C ABI of libpa (see include/pa.h) + the small kernels (checks, count, K3 pose
+// reduction, Euler chain, Adam, loss sums).  Citations as in pa_kernels.cuh.
+#include "pa.h"
+#include "pa_kernels.cuh"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace pa;
+
+namespace {
+
+thread_local std::string g_err;
+
+pa_status fail(pa_status s, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CUDA_TRY(x)                                                                          \
+    do {                                                                                     \
+        cudaError_t _e = (x);                                                                \
+        if (_e != cudaSuccess) return fail(PA_ECUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
+    } while (0)
+
+inline bool aligned4(const void *p) { return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+
+// ------------------------------------------------------------------------ kernel classes
+struct Klass {
+    int lmin, omax, span, seg;
+};
+// Compiled window classes: sigma/(c dt) in {5.33, 2.67, 10.67} at kappa = 5
+// for the BASELINE configs; any geometry whose L_min, cluster spread, tile span and
+// segment need fit a class is supported.
+constexpr Klass kClasses[] = {{53, 11, 64, 128}, {26, 6, 32, 64}, {106, 21, 128, 256}};
+
+struct Plan {
+    Geo g;
+    BPow bp;
+    int klass;
+};
+
+pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &pl)
+{
+    if (!grid || !acq) return fail(PA_EINVAL, "null grid/acq");
+    if (grid->nx <= 0 || grid->ny <= 0 || grid->nz <= 0) return fail(PA_EINVAL, "grid dims must be positive");
+    if (!(grid->pitch > 0.f) || !std::isfinite(grid->pitch)) return fail(PA_EINVAL, "pitch must be > 0");
+    for (int i = 0; i < 3; ++i)
+        if (!std::isfinite(grid->origin[i])) return fail(PA_EINVAL, "origin must be finite");
+    if (!(acq->c > 0.f) || !(acq->dt > 0.f) || acq->nt <= 0 || !(acq->sigma > 0.f))
+        return fail(PA_EINVAL, "c, dt, nt, sigma must be positive");
+    if (!std::isfinite(acq->t0)) return fail(PA_EINVAL, "t0 must be finite");
+    if (!(acq->kappa >= 4.f)) return fail(PA_EINVAL, "kappa must be >= 4 (got %g)", (double)acq->kappa);
+    if (E < 1) return fail(PA_ESHAPE, "E must be >= 1");
+    if (F < 0) return fail(PA_ESHAPE, "F must be >= 0");
+    Geo &g = pl.g;
+    g.nx = grid->nx;
+    g.ny = grid->ny;
+    g.nz = grid->nz;
+    g.nt = acq->nt;
+    g.ntx = (g.nx + TX - 1) / TX;
+    g.nty = (g.ny + TY - 1) / TY;
+    g.ntz = (g.nz + TZ - 1) / TZ;
+    long long nt_ = (long long)g.ntx * g.nty * g.ntz;
+    if (nt_ > (1ll << 30)) return fail(PA_EINVAL, "grid too large");
+    g.ntiles = (int)nt_;
+    g.E = E;
+    g.F = F;
+    g.ox = grid->origin[0];
+    g.oy = grid->origin[1];
+    g.oz = grid->origin[2];
+    g.h = grid->pitch;
+    g.c = acq->c;
+    g.t0 = acq->t0;
+    const double a = (double)acq->c * (double)acq->dt;
+    const double sig = acq->sigma;
+    g.a_d = a;
+    g.ksig_d = (double)acq->kappa * sig;
+    g.rt_d = 0.5 * g.h * std::sqrt((double)((TX - 1) * (TX - 1) + (TY - 1) * (TY - 1) + (TZ - 1) * (TZ - 1)));
+    g.hf = grid->pitch;
+    g.af = (float)a;
+    g.inv_a = (float)(1.0 / a);
+    g.ksig = (float)g.ksig_d;
+    const double k2 = 1.4426950408889634 / (2.0 * sig * sig);
+    g.k2 = (float)k2;
+    g.two_a_k2 = (float)(2.0 * a * k2);
+    g.a2_k2 = (float)(a * a * k2);
+    g.s2 = (float)(sig * sig);
+    g.inv_s2 = (float)(1.0 / (sig * sig));
+    g.rt = (float)g.rt_d;
+    for (int i = 0; i < 128; ++i) pl.bp.B[i] = (float)std::exp(-(double)i * a * a / (sig * sig));
+
+    const double K2 = 2.0 * g.ksig_d / a;
+    const int wmin = (int)std::floor(K2);
+    const int o_need = (int)std::floor(std::sqrt(3.0) * g.h / a) + 2;
+    const int span_need = (int)std::ceil(2.0 * g.rt_d / a) + 3;
+    const int seg_need = (int)std::ceil(2.0 * g.rt_d / a) + 5 + (wmin + 1);
+    pl.klass = -1;
+    for (int k = 0; k < (int)(sizeof kClasses / sizeof kClasses[0]); ++k) {
+        const Klass &c = kClasses[k];
+        if (c.lmin == wmin && o_need <= c.omax && span_need <= c.span && seg_need <= c.seg) {
+            pl.klass = k;
+            break;
+        }
+    }
+    if (pl.klass < 0)
+        return fail(PA_EUNSUPPORTED,
+                    "window class not compiled: L_min=%d (2 kappa sigma/(c dt)=%.4f), cluster spread %d, tile span %d, "
+                    "segment %d; compiled classes L_min in {53, 26, 106}",
+                    wmin, K2, o_need, span_need, seg_need);
+    return PA_OK;
+}
+
+// ------------------------------------------------------------------------ small kernels
+struct DegenOut {
+    int fe;
+    int i, j, k;
+    double d;
+};
+
+// Degenerate geometry check (R10): nearest lattice point of every element.
+__global__ void k_check(Geo g, const float *__restrict__ poses, const float *__restrict__ tmpl,
+                        unsigned long long *__restrict__ best)
+{
+    const int fe = blockIdx.x * blockDim.x + threadIdx.x;
+    if (fe >= g.F * g.E) return;
+    const int f = fe / g.E, e = fe - f * g.E;
+    double x[3];
+    elem_pos(poses, tmpl, f, e, x);
+    const double o[3] = {g.ox, g.oy, g.oz};
+    const int n[3] = {g.nx, g.ny, g.nz};
+    double d2 = 0.0;
+    int idx[3];
+    for (int a = 0; a < 3; ++a) {
+        double q = rint((x[a] - o[a]) / g.h);
+        q = q < 0 ? 0 : (q > n[a] - 1 ? n[a] - 1 : q);
+        idx[a] = (int)q;
+        const double dd = x[a] - (o[a] + g.h * q);
+        d2 += dd * dd;
+    }
+    if (d2 < 1e-12) {
+        // pack (fe, voxel) — deterministic minimum fe wins
+        const unsigned long long key = ((unsigned long long)(unsigned)fe << 32) |
+                                       (unsigned long long)((idx[0] & 0x3ff) | ((idx[1] & 0x3ff) << 10) |
+                                                            ((idx[2] & 0x3ff) << 20));
+        atomicMin(best, key);
+    }
+}
+
+// Exact unit-of-work count: fp64, no contraction, literal predicate.
+__device__ __forceinline__ bool in_win(double r, int j, double c, double t0, double dt, double w)
+{
+    const double D = __dsub_rn(r, __dmul_rn(c, __dadd_rn(t0, __dmul_rn((double)j, dt))));
+    return fabs(D) <= w;
+}
+
+__global__ void k_count(Geo g, double c, double t0, double dt, double kappa, double sigma,
+                        const float *__restrict__ poses, const float *__restrict__ tmpl,
+                        long long *__restrict__ counts)
+{
+    const int fe = blockIdx.x;
+    const int f = fe / g.E, e = fe - f * g.E;
+    const float *P = poses + 12 * f;
+    const float *xh = tmpl + 3 * e;
+    double x[3];
+    for (int a = 0; a < 3; ++a) {
+        double s = __dmul_rn((double)P[3 * a], (double)xh[0]);
+        s = __dadd_rn(s, __dmul_rn((double)P[3 * a + 1], (double)xh[1]));
+        s = __dadd_rn(s, __dmul_rn((double)P[3 * a + 2], (double)xh[2]));
+        x[a] = __dadd_rn(s, (double)P[9 + a]);
+    }
+    const double w = __dmul_rn(kappa, sigma), cdt = __dmul_rn(c, dt);
+    const long long nvox = (long long)g.nx * g.ny * g.nz;
+    long long n = 0;
+    for (long long k = threadIdx.x; k < nvox; k += blockDim.x) {
+        const long long i = k % g.nx, j = (k / g.nx) % g.ny, l = k / ((long long)g.nx * g.ny);
+        const double y0 = __dadd_rn(g.ox, __dmul_rn(g.h, (double)i));
+        const double y1 = __dadd_rn(g.oy, __dmul_rn(g.h, (double)j));
+        const double y2 = __dadd_rn(g.oz, __dmul_rn(g.h, (double)l));
+        const double dx = __dsub_rn(x[0], y0), dy = __dsub_rn(x[1], y1), dz = __dsub_rn(x[2], y2);
+        const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        const double lo = ceil(__ddiv_rn(__dsub_rn(__dsub_rn(r, w), __dmul_rn(c, t0)), cdt));
+        const double hi = floor(__ddiv_rn(__dsub_rn(__dadd_rn(r, w), __dmul_rn(c, t0)), cdt));
+        if (hi < 0.0 || lo > (double)(g.nt - 1)) continue;
+        int jlo = lo < 0.0 ? 0 : (int)lo;
+        int jhi = hi > (double)(g.nt - 1) ? g.nt - 1 : (int)hi;
+        while (jlo > 0 && in_win(r, jlo - 1, c, t0, dt, w)) --jlo;
+        while (jlo <= jhi && !in_win(r, jlo, c, t0, dt, w)) ++jlo;
+        while (jhi < g.nt - 1 && in_win(r, jhi + 1, c, t0, dt, w)) ++jhi;
+        while (jhi >= jlo && !in_win(r, jhi, c, t0, dt, w)) --jhi;
+        if (jhi >= jlo) n += jhi - jlo + 1;
+    }
+    __shared__ long long red[256];
+    red[threadIdx.x] = n;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) counts[fe] = red[0];
+}
+
+// K3 — fixed-order reduction of the per-CTA partials and the pose chain rule (a6).
+__global__ void k_pose_reduce(const float *__restrict__ partial, int P, int F, int E, const float *__restrict__ tmpl,
+                              float *__restrict__ grad_elem, float *__restrict__ grad_pose)
+{
+    const int f = blockIdx.x;
+    float acc[12];
+    for (int i = 0; i < 12; ++i) acc[i] = 0.f;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        float G[3];
+        for (int c = 0; c < 3; ++c) {
+            float s = 0.f;
+            for (int p = 0; p < P; ++p) s += partial[(((size_t)p * F + f) * E + e) * 3 + c];
+            G[c] = s;
+            grad_elem[((size_t)f * E + e) * 3 + c] = s;
+        }
+        const float *xh = tmpl + 3 * e;
+        for (int r = 0; r < 3; ++r) {
+            for (int c = 0; c < 3; ++c) acc[3 * r + c] += G[r] * xh[c];
+            acc[9 + r] += G[r];
+        }
+    }
+    __shared__ float red[12][128];
+    for (int i = 0; i < 12; ++i) red[i][threadIdx.x] = acc[i];
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            for (int i = 0; i < 12; ++i) red[i][threadIdx.x] += red[i][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x < 12) grad_pose[12 * f + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// Euler ZYX intrinsic (R8): R = Rz(a) Ry(b) Rx(c) and dR/d(a,b,c), in fp64.
+__device__ void mat3mul(const double *A, const double *B, double *C)
+{
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
+}
+
+__global__ void k_euler_pose(const float *__restrict__ euler_t, int F, float *__restrict__ poses,
+                             float *__restrict__ dR)
+{
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= F) return;
+    const double a = euler_t[6 * f], b = euler_t[6 * f + 1], c = euler_t[6 * f + 2];
+    const double ca = cos(a), sa = sin(a), cb = cos(b), sb = sin(b), cc = cos(c), sc = sin(c);
+    const double Rz[9] = {ca, -sa, 0, sa, ca, 0, 0, 0, 1};
+    const double Ry[9] = {cb, 0, sb, 0, 1, 0, -sb, 0, cb};
+    const double Rx[9] = {1, 0, 0, 0, cc, -sc, 0, sc, cc};
+    const double dRz[9] = {-sa, -ca, 0, ca, -sa, 0, 0, 0, 0};
+    const double dRy[9] = {-sb, 0, cb, 0, 0, 0, -cb, 0, -sb};
+    const double dRx[9] = {0, 0, 0, 0, -sc, -cc, 0, cc, -sc};
+    double T[9], R[9], D[9];
+    mat3mul(Rz, Ry, T);
+    mat3mul(T, Rx, R);
+    for (int i = 0; i < 9; ++i) poses[12 * f + i] = (float)R[i];
+    for (int i = 0; i < 3; ++i) poses[12 * f + 9 + i] = euler_t[6 * f + 3 + i];
+    mat3mul(dRz, Ry, T);
+    mat3mul(T, Rx, D);
+    for (int i = 0; i < 9; ++i) dR[27 * f + i] = (float)D[i];
+    mat3mul(Rz, dRy, T);
+    mat3mul(T, Rx, D);
+    for (int i = 0; i < 9; ++i) dR[27 * f + 9 + i] = (float)D[i];
+    mat3mul(Rz, Ry, T);
+    mat3mul(T, dRx, D);
+    for (int i = 0; i < 9; ++i) dR[27 * f + 18 + i] = (float)D[i];
+}
+
+// dL/dEuler_q = <dL/dR, dR/dq>_F ; dL/dt passes through.
+__global__ void k_euler_grad(const float *__restrict__ grad_pose, const float *__restrict__ dR, int F,
+                             float *__restrict__ geul)
+{
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= F) return;
+    for (int q = 0; q < 3; ++q) {
+        float s = 0.f;
+        for (int i = 0; i < 9; ++i) s += grad_pose[12 * f + i] * dR[27 * f + 9 * q + i];
+        geul[6 * f + q] = s;
+        geul[6 * f + 3 + q] = grad_pose[12 * f + 9 + q];
+    }
+}
+
+// a8 — Adam with optional clamp x >= 0.
+__global__ void k_adam(float *__restrict__ x, float *__restrict__ m, float *__restrict__ v,
+                       const float *__restrict__ g, long long n, float lr, float b1, float b2, float eps, float bc1,
+                       float bc2, int clamp)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float gi = g[i];
+        const float mi = b1 * m[i] + (1.f - b1) * gi;
+        const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        float xi = x[i] - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+        if (clamp && xi < 0.f) xi = 0.f;
+        x[i] = xi;
+    }
+}
+
+__global__ void k_adam_pose(float *__restrict__ x, float *__restrict__ m, float *__restrict__ v,
+                            const float *__restrict__ g, int F, float lr_rot, float lr_t, float b1, float b2, float eps,
+                            float bc1, float bc2)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 6 * F) return;
+    const float lr = (i % 6) < 3 ? lr_rot : lr_t;
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    x[i] = x[i] - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+}
+
+// Fixed-order sum of the per-row losses -> loss[0] (local) and loss[1] (pre-all-reduce copy).
+__global__ void k_rowloss_sum(const double *__restrict__ rl, long long n, float *__restrict__ loss)
+{
+    __shared__ double red[256];
+    double s = 0.0;
+    const long long chunk = (n + blockDim.x - 1) / blockDim.x;
+    const long long b = threadIdx.x * chunk, e = min(n, b + chunk);
+    for (long long i = b; i < e; ++i) s += rl[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        loss[0] = (float)red[0];
+        loss[1] = (float)red[0];
+    }
+}
+
+// Standalone a3 (pa_loss): one CTA per row.
+__global__ void k_loss_rows(int kind, const float *__restrict__ y, const float *__restrict__ S,
+                            const uint8_t *__restrict__ mask, int nt, float *__restrict__ cot,
+                            double *__restrict__ rowloss)
+{
+    __shared__ double red[128];
+    const size_t off = (size_t)blockIdx.x * nt;
+    const bool masked = mask != nullptr && mask[blockIdx.x] == 0;
+    if (kind == 0) {
+        double part = 0.0;
+        for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+            const float d = y[off + j] - S[off + j];
+            part += (double)d * (double)d;
+            cot[off + j] = masked ? 0.f : 2.f * d;
+        }
+        const double tot = block_sum(part, red);
+        if (threadIdx.x == 0) rowloss[blockIdx.x] = masked ? 0.0 : tot;
+        return;
+    }
+    double sy = 0.0, ss = 0.0;
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        sy += y[off + j];
+        ss += S[off + j];
+    }
+    const double my = block_sum(sy, red) / nt, ms = block_sum(ss, red) / nt;
+    double cv = 0.0, vy = 0.0, vs = 0.0;
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        const double a = y[off + j] - my, b = (double)S[off + j] - ms;
+        cv += a * b;
+        vy += a * a;
+        vs += b * b;
+    }
+    const double COV = block_sum(cv, red) / nt, VY = block_sum(vy, red) / nt, VS = block_sum(vs, red) / nt;
+    const double sdy = sqrt(VY), sds = sqrt(VS);
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        const double gj = -(((double)S[off + j] - ms) / (sdy * sds) - COV * (y[off + j] - my) / (sdy * sdy * sdy * sds)) / nt;
+        cot[off + j] = masked ? 0.f : (float)gj;
+    }
+    if (threadIdx.x == 0) rowloss[blockIdx.x] = masked ? 0.0 : -COV / (sdy * sds);
+}
+
+}  // namespace
+
+// ============================================================================ context
+struct pa_ctx {
+    int device = 0;
+    int nsm = 148;
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    unsigned long long *dflag = nullptr;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    bool ev_fwd = false, ev_adj = false;
+};
+
+namespace {
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int d)
+    {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DevGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+pa_status ws_reserve(pa_ctx *ctx, size_t bytes)
+{
+    if (bytes <= ctx->ws_bytes) return PA_OK;
+    if (ctx->ws) cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+    size_t b = bytes + (bytes >> 3) + 4096;
+    if (cudaMalloc(&ctx->ws, b) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PA_ENOMEM, "workspace allocation of %zu bytes failed", b);
+    }
+    ctx->ws_bytes = b;
+    return PA_OK;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+pa_status check_degenerate(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, cudaStream_t st)
+{
+    const unsigned long long init = ~0ull;
+    CUDA_TRY(cudaMemcpyAsync(ctx->dflag, &init, sizeof init, cudaMemcpyHostToDevice, st));
+    const int n = pl.g.F * pl.g.E;
+    k_check<<<(n + 127) / 128, 128, 0, st>>>(pl.g, poses, tmpl, ctx->dflag);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long best = 0;
+    CUDA_TRY(cudaMemcpyAsync(&best, ctx->dflag, sizeof best, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (best != ~0ull) {
+        const int fe = (int)(best >> 32);
+        const unsigned v = (unsigned)(best & 0xffffffffu);
+        return fail(PA_EDEGENERATE, "degenerate geometry: frame %d element %d lies within 1e-6 mm of voxel (%u,%u,%u)",
+                    fe / pl.g.E, fe % pl.g.E, v & 0x3ff, (v >> 10) & 0x3ff, (v >> 20) & 0x3ff);
+    }
+    return PA_OK;
+}
+
+// ---------------------------------------------------------------- launchers per class
+template <int LMIN, int OMAX, int SPAN>
+pa_status launch_forward_t(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
+                           const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
+{
+    using C = FwdCfg<LMIN, OMAX, SPAN>;
+    const size_t smem = (size_t)FWD_WARPS * C::warp_floats(pl.g.nt) * sizeof(float);
+    if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "nt=%d too long for the forward kernel's shared memory", pl.g.nt);
+    auto kern = k_forward<LMIN, OMAX, SPAN>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<pl.g.F * pl.g.E, FWD_WARPS * 32, smem, st>>>(pl.g, pl.bp, poses, tmpl, p0, out, mode, meas, mask, rowloss);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+pa_status launch_forward(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
+                         const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
+{
+    switch (pl.klass) {
+    case 0: return launch_forward_t<53, 11, 64>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    case 1: return launch_forward_t<26, 6, 32>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    default: return launch_forward_t<106, 21, 128>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    }
+}
+
+struct AdjLaunch {
+    int P = 0, Fc = 0;
+    size_t smem = 0;
+};
+
+template <int LMIN, int SEG, bool POSE, bool ADJ>
+pa_status launch_adjoint_t(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
+                           const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
+{
+    auto kern = k_adjoint<LMIN, SEG, POSE, ADJ>;
+    const int E = pl.g.E, F = pl.g.F;
+    int Fc = POSE ? 64 : F;
+    size_t smem = AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float);
+    // prefer 2 CTAs/SM with a frame chunk >= 8, else the largest chunk that fits one CTA/SM
+    const size_t two = 113 * 1024, one = 227 * 1024;
+    if (POSE) {
+        Fc = 64;
+        while (Fc > 8 && AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float) > two) Fc -= 4;
+        if (AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float) > two) {
+            Fc = 64;
+            while (Fc > 1 && AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float) > one) Fc -= 1;
+        }
+        Fc = Fc < F ? Fc : (F > 0 ? F : 1);
+        smem = AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float);
+    }
+    if (smem > one) return fail(PA_EUNSUPPORTED, "E=%d too large for the adjoint kernel's shared memory", E);
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
+    if (occ < 1) occ = 1;
+    int P = occ * ctx->nsm;
+    if (P > pl.g.ntiles) P = pl.g.ntiles;
+    L.P = P;
+    L.Fc = Fc;
+    L.smem = smem;
+    if (dry) return PA_OK;
+    kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.bp, poses, tmpl, p0, cot, grad_p0, partial, Fc);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+template <bool POSE, bool ADJ>
+pa_status launch_adjoint(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
+                         const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
+{
+    switch (pl.klass) {
+    case 0: return launch_adjoint_t<53, 128, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    case 1: return launch_adjoint_t<26, 64, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    default: return launch_adjoint_t<106, 256, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    }
+}
+
+pa_status check_ptrs(std::initializer_list<const void *> ps)
+{
+    for (const void *p : ps)
+        if (!aligned4(p)) return fail(PA_ESHAPE, "null or misaligned pointer");
+    return PA_OK;
+}
+
+// Fused adjoint+pose core used by pa_pose_grad / pa_adjoint_pose / pa_step.
+pa_status adjoint_pose_core(pa_ctx *ctx, const Plan &pl, const float *tmpl, const float *poses, const float *p0,
+                            const float *cot, float *grad_p0, float *grad_pose, float *grad_elem, bool want_adj,
+                            cudaStream_t st, char *ws_base, size_t ws_off)
+{
+    AdjLaunch L;
+    pa_status s = want_adj ? launch_adjoint<true, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, nullptr, L, true, st)
+                           : launch_adjoint<true, false>(ctx, pl, poses, tmpl, p0, cot, grad_p0, nullptr, L, true, st);
+    if (s) return s;
+    (void)ws_base;
+    const size_t part_b = align256((size_t)L.P * pl.g.F * pl.g.E * 3 * sizeof(float));
+    const size_t ge_b = grad_elem ? 0 : align256((size_t)pl.g.F * pl.g.E * 3 * sizeof(float));
+    if ((s = ws_reserve(ctx, ws_off + part_b + ge_b))) return s;
+    char *base = static_cast<char *>(ctx->ws) + ws_off;
+    float *partial = reinterpret_cast<float *>(base);
+    float *ge = grad_elem ? grad_elem : reinterpret_cast<float *>(base + part_b);
+    if (ctx->ev_adj || true) CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+    s = want_adj ? launch_adjoint<true, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, false, st)
+                 : launch_adjoint<true, false>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, false, st);
+    if (s) return s;
+    CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
+    ctx->ev_adj = true;
+    k_pose_reduce<<<pl.g.F, 128, 0, st>>>(partial, L.P, pl.g.F, pl.g.E, tmpl, ge, grad_pose);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+const char *pa_last_error(void) { return g_err.c_str(); }
+
+const char *pa_version(void) { return "libpa 0.1 (sm_100a, fp32 + fp64 anchors)"; }
+
+pa_status pa_create(pa_ctx **out, int device)
+{
+    if (!out) return fail(PA_EINVAL, "null ctx pointer");
+    *out = nullptr;
+    int n = 0;
+    CUDA_TRY(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(PA_EINVAL, "device %d out of range (%d devices)", device, n);
+    DevGuard dg(device);
+    pa_ctx *c = new pa_ctx;
+    c->device = device;
+    cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMalloc(&c->dflag, 64) != cudaSuccess) {
+        delete c;
+        return fail(PA_ENOMEM, "flag allocation failed");
+    }
+    for (int i = 0; i < 3; ++i) cudaEventCreate(&c->ev[i]);
+    *out = c;
+    g_err.clear();
+    return PA_OK;
+}
+
+void pa_destroy(pa_ctx *c)
+{
+    if (!c) return;
+    DevGuard dg(c->device);
+    if (c->ws) cudaFree(c->ws);
+    if (c->dflag) cudaFree(c->dflag);
+    for (int i = 0; i < 3; ++i)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    delete c;
+}
+
+pa_status pa_forward(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                     const float *poses, int32_t F, const float *p0, float *traces, void *stream)
+{
+    if (!ctx) return fail(PA_EINVAL, "null ctx");
+    Plan pl;
+    pa_status s = make_plan(grid, acq, E, F, pl);
+    if (s) return s;
+    if (F == 0) return PA_OK;
+    if ((s = check_ptrs({tmpl, poses, p0, traces}))) return s;
+    DevGuard dg(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
+    CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
+    if ((s = launch_forward(pl, poses, tmpl, p0, traces, FWD_TRACE, nullptr, nullptr, nullptr, st))) return s;
+    CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+    ctx->ev_fwd = true;
+    return PA_OK;
+}
+
+pa_status pa_adjoint(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                     const float *poses, int32_t F, const float *cot, float *grad_p0, void *stream)
+{
+    if (!ctx) return fail(PA_EINVAL, "null ctx");
+    Plan pl;
+    pa_status s = make_plan(grid, acq, E, F, pl);
+    if (s) return s;
+    if ((s = check_ptrs({tmpl, poses, cot, grad_p0}))) return s;
+    DevGuard dg(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (F == 0) {
+        CUDA_TRY(cudaMemsetAsync(grad_p0, 0, sizeof(float) * (size_t)grid->nx * grid->ny * grid->nz, st));
+        return PA_OK;
+    }
+    if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
+    AdjLaunch L;
+    CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+    if ((s = launch_adjoint<false, true>(ctx, pl, poses, tmpl, nullptr, cot, grad_p0, nullptr, L, false, st))) return s;
+    CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
+    ctx->ev_adj = true;
+    return PA_OK;
+}
+
+pa_status pa_adjoint_pose(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                          const float *poses, int32_t F, const float *p0, const float *cot, float *grad_p0,
+                          float *grad_pose, float *grad_elem, void *stream)
+{
+    if (!ctx) return fail(PA_EINVAL, "null ctx");
+    Plan pl;
+    pa_status s = make_plan(grid, acq, E, F, pl);
+    if (s) return s;
+    if ((s = check_ptrs({tmpl, poses, p0, cot, grad_p0}))) return s;
+    if (F > 0 && (s = check_ptrs({grad_pose}))) return s;
+    if (grad_elem && !aligned4(grad_elem)) return fail(PA_ESHAPE, "misaligned grad_elem");
+    DevGuard dg(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (F == 0) {
+        CUDA_TRY(cudaMemsetAsync(grad_p0, 0, sizeof(float) * (size_t)grid->nx * grid->ny * grid->nz, st));
+        return PA_OK;
+    }
+    if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
+    return adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, grad_pose, grad_elem, true, st, nullptr, 0);
+}
+
+pa_status pa_pose_grad(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                       const float *poses, int32_t F, const float *p0, const float *cot, float *grad_pose,
+                       float *grad_elem, void *stream)
+{
+    if (!ctx) return fail(PA_EINVAL, "null ctx");
+    Plan pl;
+    pa_status s = make_plan(grid, acq, E, F, pl);
+    if (s) return s;
+    if (F == 0) return PA_OK;
+    if ((s = check_ptrs({tmpl, poses, p0, cot, grad_pose}))) return s;
+    if (grad_elem && !aligned4(grad_elem)) return fail(PA_ESHAPE, "misaligned grad_elem");
+    DevGuard dg(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
+    return adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, nullptr, grad_pose, grad_elem, false, st, nullptr, 0);
+}
+
+pa_status pa_count(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
+                   const float *poses, int32_t F, int64_t *total, int64_t *per_frame, void *stream)
+{
+    if (!ctx || !total) return fail(PA_EINVAL, "null ctx/total");
+    Plan pl;
+    pa_status s = make_plan(grid, acq, E, F, pl);
+    if (s && s != PA_EUNSUPPORTED) return s;  // the count is defined for every valid geometry
+    *total = 0;
+    if (F == 0) return PA_OK;
+    if ((s = check_ptrs({tmpl, poses}))) return s;
+    DevGuard dg(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((s = ws_reserve(ctx, sizeof(long long) * (size_t)F * E))) return s;
+    long long *d = static_cast<long long *>(ctx->ws);
+    k_count<<<F * E, 256, 0, st>>>(pl.g, (double)acq->c, (double)acq->t0, (double)acq->dt, (double)acq->kappa,
+                                   (double)acq->sigma, poses, tmpl, d);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<long long> h((size_t)F * E);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), d, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    long long tot = 0;
+    for (int f = 0; f < F; ++f) {
+        long long sf = 0;
+        for (int e = 0; e < E; ++e) sf += h[(size_t)f * E + e];
+        if (per_frame) per_frame[f] = sf;
+        tot += sf;
+    }
+    *total = tot;
+    return PA_OK;
+}
+
+pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, const uint8_t *row_mask, int32_t F,
+                  int32_t E, int32_t nt, float *cot, float *loss, void *stream)
+{
+    if (!ctx) return fail(PA_EINVAL, "null ctx");
+    if (kind != 0 && kind != 1) return fail(PA_EINVAL, "loss kind must be 0 (MSE) or 1 (NC)");
+    if (F < 0 || E < 1 || nt < 1) return fail(PA_ESHAPE, "bad shape");
+    pa_status s;
+    if ((s = check_ptrs({y, S, cot, loss}))) return s;
+    DevGuard dg(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long rows = (long long)F * E;
+    if ((s = ws_reserve(ctx, sizeof(double) * (size_t)(rows + 1)))) return s;
+    double *rl = static_cast<double *>(ctx->ws);
+    if (rows > 0) {
+        k_loss_rows<<<(unsigned)rows, 128, 0, st>>>(kind, y, S, row_mask, nt, cot, rl);
+        CUDA_TRY(cudaGetLastError());
+    }
+    k_rowloss_sum<<<1, 256, 0, st>>>(rl, rows, loss);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E, int32_t F,
+                  const float *meas, const uint8_t *row_mask, float *p0, float *euler_t, float *adam_p0,
+                  float *adam_pose, const pa_step_cfg *cfg, pa_allreduce_fn ar, void *user, float *grad_p0,
+                  float *loss, float *grad_euler, void *stream)
+{
+    if (!ctx || !cfg) return fail(PA_EINVAL, "null ctx/cfg");
+    Plan pl;
+    pa_status s = make_plan(grid, acq, E, F, pl);
+    if (s) return s;
+    if (cfg->step < 1) return fail(PA_EINVAL, "cfg.step must be >= 1");
+    if (cfg->loss_kind != 0 && cfg->loss_kind != 1) return fail(PA_EINVAL, "cfg.loss_kind must be 0 or 1");
+    if (!(cfg->beta1 >= 0.f && cfg->beta1 < 1.f && cfg->beta2 >= 0.f && cfg->beta2 < 1.f && cfg->eps > 0.f))
+        return fail(PA_EINVAL, "bad Adam hyper-parameters");
+    if ((s = check_ptrs({tmpl, p0, adam_p0, grad_p0, loss}))) return s;
+    if (F > 0 && (s = check_ptrs({meas, euler_t, adam_pose}))) return s;
+    if (grad_euler && !aligned4(grad_euler)) return fail(PA_ESHAPE, "misaligned grad_euler");
+    DevGuard dg(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
+    const size_t ntr = (size_t)F * E * acq->nt;
+
+    // workspace: poses | dR | cot | rowloss | grad_pose | geul | (partials, grad_elem from core)
+    size_t off = 0;
+    const size_t o_poses = off; off += align256(sizeof(float) * 12 * (size_t)(F > 0 ? F : 1));
+    const size_t o_dR = off; off += align256(sizeof(float) * 27 * (size_t)(F > 0 ? F : 1));
+    const size_t o_cot = off; off += align256(sizeof(float) * (ntr > 0 ? ntr : 1));
+    const size_t o_rl = off; off += align256(sizeof(double) * (size_t)(F > 0 ? F * E : 1));
+    const size_t o_gp = off; off += align256(sizeof(float) * 12 * (size_t)(F > 0 ? F : 1));
+    const size_t o_ge = off; off += align256(sizeof(float) * 6 * (size_t)(F > 0 ? F : 1));
+    // reserve enough for the core as well (partials + grad_elem)
+    AdjLaunch L;
+    if (F > 0 && (s = launch_adjoint<true, true>(ctx, pl, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, true, st)))
+        return s;
+    const size_t core_b = align256((size_t)L.P * (F > 0 ? F : 1) * E * 3 * sizeof(float)) +
+                          align256((size_t)(F > 0 ? F : 1) * E * 3 * sizeof(float));
+    if ((s = ws_reserve(ctx, off + core_b))) return s;
+    char *ws = static_cast<char *>(ctx->ws);
+    float *poses = reinterpret_cast<float *>(ws + o_poses);
+    float *dR = reinterpret_cast<float *>(ws + o_dR);
+    float *cot = reinterpret_cast<float *>(ws + o_cot);
+    double *rl = reinterpret_cast<double *>(ws + o_rl);
+    float *gpose = reinterpret_cast<float *>(ws + o_gp);
+    float *geul = grad_euler ? grad_euler : reinterpret_cast<float *>(ws + o_ge);
+
+    if (F > 0) {
+        k_euler_pose<<<(F + 127) / 128, 128, 0, st>>>(euler_t, F, poses, dR);
+        CUDA_TRY(cudaGetLastError());
+        if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
+        // a2 + a3: forward with fused loss/cotangent epilogue
+        CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
+        if ((s = launch_forward(pl, poses, tmpl, p0, cot, cfg->loss_kind == 0 ? FWD_MSE : FWD_NC, meas, row_mask, rl,
+                                st)))
+            return s;
+        ctx->ev_fwd = true;
+        k_rowloss_sum<<<1, 256, 0, st>>>(rl, (long long)F * E, loss);
+        CUDA_TRY(cudaGetLastError());
+        // a4 + a5 + a6 (records ev[1], ev[2])
+        if ((s = adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, gpose, nullptr, true, st, ws, off))) return s;
+        k_euler_grad<<<(F + 127) / 128, 128, 0, st>>>(gpose, dR, F, geul);
+        CUDA_TRY(cudaGetLastError());
+    } else {
+        CUDA_TRY(cudaMemsetAsync(grad_p0, 0, sizeof(float) * nvox, st));
+        CUDA_TRY(cudaMemsetAsync(loss, 0, 2 * sizeof(float), st));
+    }
+    // a7: cross-rank sum of dL/dp0 and of the loss (Stage 5)
+    if (ar) {
+        if (ar(grad_p0, (size_t)nvox, stream, user) != 0) return fail(PA_ECUDA, "all-reduce callback failed (grad_p0)");
+        if (ar(loss + 1, 1, stream, user) != 0) return fail(PA_ECUDA, "all-reduce callback failed (loss)");
+    }
+    // a8: Adam
+    const double bc1 = 1.0 - std::pow((double)cfg->beta1, cfg->step), bc2 = 1.0 - std::pow((double)cfg->beta2, cfg->step);
+    if (cfg->update_p0) {
+        int blocks = ctx->nsm * 8;
+        k_adam<<<blocks, 256, 0, st>>>(p0, adam_p0, adam_p0 + nvox, grad_p0, nvox, cfg->lr_p0, cfg->beta1, cfg->beta2,
+                                      cfg->eps, (float)bc1, (float)bc2, 1);
+        CUDA_TRY(cudaGetLastError());
+    }
+    if (cfg->update_pose && F > 0) {
+        k_adam_pose<<<(6 * F + 127) / 128, 128, 0, st>>>(euler_t, adam_pose, adam_pose + 6 * F, geul, F, cfg->lr_rot,
+                                                         cfg->lr_trans, cfg->beta1, cfg->beta2, cfg->eps, (float)bc1,
+                                                         (float)bc2);
+        CUDA_TRY(cudaGetLastError());
+    }
+    return PA_OK;
+}
+
+pa_status pa_last_kernel_ms(pa_ctx *ctx, float *forward_ms, float *adjoint_ms)
+{
+    if (!ctx) return fail(PA_EINVAL, "null ctx");
+    DevGuard dg(ctx->device);
+    if (forward_ms) {
+        *forward_ms = 0.f;
+        if (ctx->ev_fwd) {
+            CUDA_TRY(cudaEventSynchronize(ctx->ev[1]));
+            CUDA_TRY(cudaEventElapsedTime(forward_ms, ctx->ev[0], ctx->ev[1]));
+        }
+    }
+    if (adjoint_ms) {
+        *adjoint_ms = 0.f;
+        if (ctx->ev_adj) {
+            CUDA_TRY(cudaEventSynchronize(ctx->ev[2]));
+            CUDA_TRY(cudaEventElapsedTime(adjoint_ms, ctx->ev[1], ctx->ev[2]));
+        }
+    }
+    return PA_OK;
+}
+
+}  // extern "C"

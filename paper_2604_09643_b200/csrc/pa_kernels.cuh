@@ -1,0 +1,539 @@
+// pa_kernels.cuh — device code of libpa (PA-SFM acoustic radiation operator, sm_100a).
+//
+// Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, R<k> = DESIGN.md §3 reading,
+// K<k> = kernel id of DESIGN.md §6.  This file shares no code with oracle/.
+//
+// Geometry of the arithmetic (DESIGN.md §6 "precision"):
+//   * voxels are processed in 8x8x4 tiles; per (tile, element) an fp64 anchor
+//     rho = |y_c - x| (tile centre y_c) and D_A = rho - c t0 = J_A a + C_A (|C_A| <= a/2)
+//     are formed once; per voxel, r - rho = (2 d.delta + |delta|^2)/(r + rho) is evaluated in
+//     fp32 on small numbers, so D = r - c t_j = (r - rho) + C_A - (j - J_A) a keeps ~1e-7 mm.
+//   * exp(-D^2/2s^2) along a window is a two-term recurrence E_{i+1} = E_i * q0 * B^i with
+//     B^i = exp(-i a^2/s^2) precomputed in fp64 on the host (kernel parameter), so errors do
+//     not compound in q.
+//   * the window [jlo, jlo+L) of every (voxel, element) pair is produced by ONE function
+//     (pair()) used by both the forward and the adjoint, so the GPU forward and adjoint are
+//     exact transposes of each other up to fp32 rounding (R17).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pa {
+
+constexpr int TX = 8, TY = 8, TZ = 4;  // voxel tile (anchor unit) — 256 voxels
+constexpr int FWD_WARPS = 4;           // warps per forward CTA
+constexpr int ADJ_THREADS = 256;       // one thread per tile voxel
+
+struct Geo {
+    int nx, ny, nz, nt;
+    int ntx, nty, ntz, ntiles;
+    int E, F;
+    double ox, oy, oz, h;       // grid (fp64 copies of the fp32 inputs)
+    double c, t0, a_d, ksig_d;  // a_d = c*dt in fp64
+    double rt_d;                // tile half-diagonal (mm)
+    float hf, af, inv_a, ksig;  // fp32 working constants
+    float k2, two_a_k2, a2_k2;  // log2(e)/(2 s^2), 2a*k2, a^2*k2
+    float s2, inv_s2, rt;
+};
+
+struct BPow {
+    float B[128];  // B^i = exp(-i a^2 / s^2)
+};
+
+struct Anc {
+    float dx2, dy2, dz2;  // 2 * (y_c - x)  (fp32)
+    float dx, dy, dz;     // y_c - x
+    float rho, rho2, CA;
+    int JA;
+    int cull;
+};
+
+__device__ __forceinline__ float ex2(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void elem_pos(const float *__restrict__ poses, const float *__restrict__ tmpl, int f, int e,
+                                         double x[3])
+{
+    const float *P = poses + 12 * f;
+    const float *xh = tmpl + 3 * e;
+    double x0 = xh[0], x1 = xh[1], x2 = xh[2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        x[a] = (double)P[3 * a] * x0 + (double)P[3 * a + 1] * x1 + (double)P[3 * a + 2] * x2 + (double)P[9 + a];
+}
+
+// Per (tile, element) fp64 anchor (K1/K2 prologue).
+__device__ __forceinline__ Anc make_anchor(const Geo &g, const double x[3], int tx, int ty, int tz)
+{
+    double cx = g.ox + g.h * (TX * tx + 0.5 * (TX - 1));
+    double cy = g.oy + g.h * (TY * ty + 0.5 * (TY - 1));
+    double cz = g.oz + g.h * (TZ * tz + 0.5 * (TZ - 1));
+    double dx = cx - x[0], dy = cy - x[1], dz = cz - x[2];
+    double rho = sqrt(dx * dx + dy * dy + dz * dz);
+    double D = rho - g.c * g.t0;
+    double JA = rint(D / g.a_d);
+    double CA = D - JA * g.a_d;
+    Anc A;
+    A.dx = (float)dx;
+    A.dy = (float)dy;
+    A.dz = (float)dz;
+    A.dx2 = 2.0f * A.dx;
+    A.dy2 = 2.0f * A.dy;
+    A.dz2 = 2.0f * A.dz;
+    A.rho = (float)rho;
+    A.rho2 = (float)(rho * rho);
+    A.CA = (float)CA;
+    A.JA = (int)JA;
+    double m = g.rt_d + g.ksig_d + 3.0 * g.a_d;
+    A.cull = (D - m > (double)(g.nt - 1) * g.a_d) || (D + m < 0.0);
+    return A;
+}
+
+struct Pair {
+    float drel;   // r - rho
+    float inv_r;  // 1/r
+    int jlo;      // first in-window sample (unclipped)
+    int L;        // window length, clamped to [LMIN, LMIN+1]
+};
+
+// The single definition of a (voxel, element) pair's window used by every kernel (R17).
+template <int LMIN>
+__device__ __forceinline__ Pair pair(const Geo &g, const Anc &A, float ex, float ey, float ez, float e2)
+{
+    float num = __fmaf_rn(A.dx2, ex, __fmaf_rn(A.dy2, ey, __fmaf_rn(A.dz2, ez, e2)));
+    float r2 = __fadd_rn(A.rho2, num);
+    float inv_r = rsqrtf(r2);
+    float r = __fmul_rn(r2, inv_r);
+    float drel = __fdividef(num, __fadd_rn(r, A.rho));
+    float base = __fadd_rn(drel, A.CA);
+    float xlo = __fmul_rn(__fsub_rn(base, g.ksig), g.inv_a);
+    float xhi = __fmul_rn(__fadd_rn(base, g.ksig), g.inv_a);
+    int clo = (int)ceilf(xlo);
+    int L = (int)floorf(xhi) - clo + 1;
+    L = L < LMIN ? LMIN : (L > LMIN + 1 ? LMIN + 1 : L);
+    Pair p;
+    p.drel = drel;
+    p.inv_r = inv_r;
+    p.jlo = A.JA + clo;
+    p.L = L;
+    return p;
+}
+
+__device__ __forceinline__ float warp_sum(float v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ int warp_min(int v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+// Fixed-order block reduction (blockDim a power of two); red has blockDim entries.
+__device__ __forceinline__ double block_sum(double v, double *red)
+{
+    __syncthreads();
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+__device__ __forceinline__ int warp_max(int v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ============================================================================================
+// K1 — forward radiation (a2, Eq. gpu_forward_model), element-stationary.
+//
+// CTA = one (frame f, element e) row of the output; 4 warps stride over the 8x8x4 voxel
+// tiles.  In a tile, lane l owns a 2x2x2 voxel cluster and a register window acc[0..R) of
+// samples [J_l, J_l+R), R = LMIN+OMAX, J_l = min jlo over the cluster (jlo spread < OMAX by
+// geometry).  Each voxel adds its L in-window terms by the exp recurrence with static
+// register indices (only the first OMAX-1 and last OMAX steps are predicated).  The 32
+// windows are then summed through shared memory into a warp-private trace (no atomics),
+// and the 4 warp traces are summed in fixed order at the end.  Epilogue optionally fuses
+// the MSE / NC cotangent (a3) so the trace is never written.
+// ============================================================================================
+template <int LMIN, int OMAX, int SPAN>
+struct FwdCfg {
+    static constexpr int R = LMIN + OMAX;
+    static constexpr int SROW = R + SPAN + 1;  // +1: bank skew
+    static constexpr int PADL = LMIN + 2;
+    static __host__ __device__ int trace_len(int nt) { return PADL + nt + R + SPAN + 1; }
+    static __host__ __device__ int warp_floats(int nt) { return trace_len(nt) + 32 * SROW; }
+};
+
+enum { FWD_TRACE = 0, FWD_MSE = 1, FWD_NC = 2 };
+
+template <int LMIN, int OMAX, int SPAN>
+__global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, BPow bp, const float *__restrict__ poses,
+                                                            const float *__restrict__ tmpl,
+                                                            const float *__restrict__ p0, float *__restrict__ out,
+                                                            int mode, const float *__restrict__ meas,
+                                                            const uint8_t *__restrict__ row_mask,
+                                                            double *__restrict__ rowloss)
+{
+    using C = FwdCfg<LMIN, OMAX, SPAN>;
+    constexpr int R = C::R;
+    extern __shared__ float sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int TL = C::trace_len(g.nt);
+    float *trw = sm + warp * C::warp_floats(g.nt);
+    float *rows = trw + TL;
+    for (int i = lane; i < TL; i += 32) trw[i] = 0.0f;
+
+    const int fe = blockIdx.x;
+    const int f = fe / g.E, e = fe - f * g.E;
+    double x[3];
+    elem_pos(poses, tmpl, f, e, x);
+
+    const int cx = lane & 3, cy = (lane >> 2) & 3, cz = lane >> 4;
+    __syncwarp();
+
+    for (int tile = warp; tile < g.ntiles; tile += FWD_WARPS) {
+        const int tx = tile % g.ntx, ty = (tile / g.ntx) % g.nty, tz = tile / (g.ntx * g.nty);
+        const Anc A = make_anchor(g, x, tx, ty, tz);
+        if (A.cull) continue;  // warp-uniform
+
+        float drel[8], coef[8];
+        int jlo[8], Lw[8];
+        int J = 0x7fffffff;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+            const int lx = 2 * cx + (v & 1), ly = 2 * cy + ((v >> 1) & 1), lz = 2 * cz + (v >> 2);
+            const int ix = TX * tx + lx, iy = TY * ty + ly, iz = TZ * tz + lz;
+            const bool inside = ix < g.nx && iy < g.ny && iz < g.nz;
+            const float ex = ((float)lx - 0.5f * (TX - 1)) * g.hf;
+            const float ey = ((float)ly - 0.5f * (TY - 1)) * g.hf;
+            const float ez = ((float)lz - 0.5f * (TZ - 1)) * g.hf;
+            const float e2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+            const Pair p = pair<LMIN>(g, A, ex, ey, ez, e2);
+            const float P = inside ? __ldg(p0 + ((size_t)iz * g.ny + iy) * g.nx + ix) : 0.0f;
+            const bool valid = inside && p.jlo <= g.nt - 1 && p.jlo + p.L - 1 >= 0;
+            drel[v] = p.drel;
+            jlo[v] = p.jlo;
+            Lw[v] = p.L;
+            coef[v] = valid ? P * 0.5f * p.inv_r : 0.0f;
+            if (valid) J = min(J, p.jlo);
+        }
+        const bool any = J != 0x7fffffff;
+        const unsigned anym = __ballot_sync(0xffffffffu, any);
+        if (anym == 0u) continue;
+        const int Jmin = warp_min(any ? J : 0x7fffffff);
+        if (!any) J = Jmin;
+
+        float acc[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) acc[i] = 0.0f;
+        unsigned ovf = 0u;  // voxels whose jlo spread exceeds OMAX (never for supported geometry)
+#pragma unroll 1
+        for (int v = 0; v < 8; ++v) {
+            int o = jlo[v] - J;
+            float cv = coef[v];
+            if (cv != 0.0f && (o < 0 || o >= OMAX)) {
+                ovf |= 1u << v;
+                cv = 0.0f;
+            }
+            if (cv == 0.0f) o = 0;
+            const int oL = o + Lw[v];
+            const float DJ = __fmaf_rn(-(float)(J - A.JA), g.af, __fadd_rn(drel[v], A.CA));
+            float Ev = cv * ex2(-DJ * DJ * g.k2);
+            const float q0 = ex2(__fmaf_rn(DJ, g.two_a_k2, -g.a2_k2));
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const float D = __fmaf_rn(-(float)i, g.af, DJ);
+                if (i < OMAX - 1) {
+                    if (i >= o) acc[i] = __fmaf_rn(Ev, D, acc[i]);
+                } else if (i < LMIN) {
+                    acc[i] = __fmaf_rn(Ev, D, acc[i]);
+                } else {
+                    if (i < oL) acc[i] = __fmaf_rn(Ev, D, acc[i]);
+                }
+                Ev = Ev * (q0 * bp.B[i]);
+            }
+        }
+
+        // ---- flush the 32 register windows into the warp trace (fixed order, no atomics)
+        const int Jmax = warp_max(J);
+        if (Jmax - Jmin <= SPAN) {
+            float *row = rows + lane * C::SROW;
+            const int off = J - Jmin;
+            for (int c = 0; c < off; ++c) row[c] = 0.0f;
+#pragma unroll
+            for (int i = 0; i < R; ++i) row[off + i] = acc[i];
+            for (int c = off + R; c < C::SROW - 1; ++c) row[c] = 0.0f;
+            __syncwarp();
+            const int ncol = Jmax - Jmin + R;
+            for (int c = lane; c < ncol; c += 32) {
+                float s = 0.0f;
+#pragma unroll 8
+                for (int l = 0; l < 32; ++l) s += rows[l * C::SROW + c];
+                trw[C::PADL + Jmin + c] += s;
+            }
+            __syncwarp();
+        } else {
+            // serialized fallback (not reached for supported geometry)
+            for (int l = 0; l < 32; ++l) {
+                if (lane == l) {
+#pragma unroll
+                    for (int i = 0; i < R; ++i) trw[C::PADL + J + i] += acc[i];
+                }
+                __syncwarp();
+            }
+        }
+        // ---- exact slow path for any overflow voxel (lane-serialised, direct exp)
+        const unsigned ovm = __ballot_sync(0xffffffffu, ovf != 0u);
+        if (ovm) {
+            for (int l = 0; l < 32; ++l) {
+                if (!((ovm >> l) & 1u)) continue;
+                if (lane == l) {
+                    for (int v = 0; v < 8; ++v) {
+                        if (!((ovf >> v) & 1u)) continue;
+                        for (int i = 0; i < Lw[v]; ++i) {
+                            const int j = jlo[v] + i;
+                            const float D = __fmaf_rn(-(float)(j - A.JA), g.af, __fadd_rn(drel[v], A.CA));
+                            trw[C::PADL + j] += coef[v] * D * ex2(-D * D * g.k2);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- sum warp traces in fixed order; epilogue
+    const int nt = g.nt;
+    const size_t rowoff = (size_t)fe * nt;
+    const int wf = C::warp_floats(nt);
+    const bool masked = row_mask != nullptr && row_mask[fe] == 0;
+    __shared__ double red[FWD_WARPS * 32];
+    if (mode == FWD_TRACE) {
+        for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+            float s = 0.0f;
+#pragma unroll
+            for (int w = 0; w < FWD_WARPS; ++w) s += sm[w * wf + C::PADL + j];
+            out[rowoff + j] = s;
+        }
+        return;
+    }
+    // y -> warp-0 trace slot (each j owned by one thread; read all warps before writing)
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        float s = 0.0f;
+#pragma unroll
+        for (int w = 0; w < FWD_WARPS; ++w) s += sm[w * wf + C::PADL + j];
+        sm[C::PADL + j] = s;
+    }
+    __syncthreads();
+    const float *y = sm + C::PADL;
+    const float *S = meas + rowoff;
+    if (mode == FWD_MSE) {
+        double part = 0.0;
+        for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+            const float d = y[j] - __ldg(S + j);
+            part += (double)d * (double)d;
+            out[rowoff + j] = masked ? 0.0f : 2.0f * d;
+        }
+        const double tot = block_sum(part, red);
+        if (threadIdx.x == 0) rowloss[fe] = masked ? 0.0 : tot;
+        return;
+    }
+    // NC (Eq. 3, population normalisation)
+    double sy = 0.0, ss = 0.0;
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        sy += y[j];
+        ss += __ldg(S + j);
+    }
+    const double my = block_sum(sy, red) / nt, ms = block_sum(ss, red) / nt;
+    double cv = 0.0, vy = 0.0, vs = 0.0;
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        const double a = y[j] - my, b = (double)__ldg(S + j) - ms;
+        cv += a * b;
+        vy += a * a;
+        vs += b * b;
+    }
+    const double COV = block_sum(cv, red) / nt, VY = block_sum(vy, red) / nt, VS = block_sum(vs, red) / nt;
+    const double sdy = sqrt(VY), sds = sqrt(VS);
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        const double gj = -(((double)__ldg(S + j) - ms) / (sdy * sds) - COV * (y[j] - my) / (sdy * sdy * sdy * sds)) / nt;
+        out[rowoff + j] = masked ? 0.0f : (float)gj;
+    }
+    if (threadIdx.x == 0) rowloss[fe] = masked ? 0.0 : -COV / (sdy * sds);
+}
+
+// ============================================================================================
+// K2 (+K3 partials) — adjoint back-projection (a4) fused with the element/pose gradient (a5).
+//
+// Persistent CTAs (grid = 2 x #SM), one thread per voxel of an 8x8x4 tile; static tile
+// ownership.  Loop order: frame chunk (Fc frames) > tile > frame > element.  Per (tile,
+// frame) all E cotangent segments the tile can touch are staged in shared memory (zero
+// padded outside [0, nt)) and all E fp64 anchors are formed once.  Each thread walks its
+// voxel's L-sample window with the exp recurrence:
+//   A1 = sum g D E   (adjoint: z += A1/(2r))
+//   Bq = sum g E (D^2 - s^2)  => sum g h'(D) = -Bq/s^2
+//   dL/dr = P/(2r) (-Bq/s^2 - A1/r);  G_fe += dL/dr (x_fe - y_k)/r       (R11)
+// G is reduced over the 32 voxels of a warp by shuffles, over the 8 warps in smem (fixed
+// order), accumulated over the CTA's tiles for the frame chunk, and written as a per-CTA
+// partial [P][F][E][3] reduced by K3 in fixed order.  z stays in a register across the
+// frames of a chunk and is read-modified-written once per chunk by its owner thread.
+// ============================================================================================
+struct AdjCfg {
+    static __host__ __device__ size_t smem_floats(int E, int SEG, int Fc, bool pose)
+    {
+        size_t f = (size_t)E * SEG + (size_t)E * 12 /*anchors*/ + (size_t)E /*jseg*/;
+        if (pose) f += (size_t)(ADJ_THREADS / 32) * E * 3 + (size_t)Fc * E * 3;
+        return f;
+    }
+};
+
+struct AncS {  // anchor as stored in shared memory (12 words)
+    float dx2, dy2, dz2, dx, dy, dz, rho, rho2, CA;
+    int JA, cull, jseg;
+};
+
+template <int LMIN, int SEG, bool POSE, bool ADJ>
+__global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, BPow bp, const float *__restrict__ poses,
+                                                           const float *__restrict__ tmpl,
+                                                           const float *__restrict__ p0,
+                                                           const float *__restrict__ cot, float *__restrict__ grad_p0,
+                                                           float *__restrict__ partial, int Fc)
+{
+    constexpr int LMAX = LMIN + 1;
+    extern __shared__ float sm[];
+    const int E = g.E, F = g.F;
+    float *seg = sm;
+    AncS *anc = reinterpret_cast<AncS *>(seg + (size_t)E * SEG);
+    float *wred = reinterpret_cast<float *>(anc + E);  // [8][E][3]
+    float *gacc = wred + (ADJ_THREADS / 32) * E * 3;  // [Fc][E][3]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+    const float ex = ((float)lx - 0.5f * (TX - 1)) * g.hf;
+    const float ey = ((float)ly - 0.5f * (TY - 1)) * g.hf;
+    const float ez = ((float)lz - 0.5f * (TZ - 1)) * g.hf;
+    const float e2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+
+    for (int f0 = 0; f0 < F; f0 += Fc) {
+        const int fn = min(Fc, F - f0);
+        if (POSE) {
+            for (int q = tid; q < Fc * E * 3; q += ADJ_THREADS) gacc[q] = 0.0f;
+        }
+        for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+            const int tx = tile % g.ntx, ty = (tile / g.ntx) % g.nty, tz = tile / (g.ntx * g.nty);
+            const int ix = TX * tx + lx, iy = TY * ty + ly, iz = TZ * tz + lz;
+            const bool inside = ix < g.nx && iy < g.ny && iz < g.nz;
+            const size_t kidx = ((size_t)iz * g.ny + iy) * g.nx + ix;
+            const float P = (POSE && inside) ? __ldg(p0 + kidx) : 0.0f;
+            float z = 0.0f;
+            for (int fl = 0; fl < fn; ++fl) {
+                const int f = f0 + fl;
+                __syncthreads();  // previous frame's segments / wred fully consumed
+                for (int e = tid; e < E; e += ADJ_THREADS) {
+                    double x[3];
+                    elem_pos(poses, tmpl, f, e, x);
+                    const Anc A = make_anchor(g, x, tx, ty, tz);
+                    AncS s;
+                    s.dx2 = A.dx2; s.dy2 = A.dy2; s.dz2 = A.dz2;
+                    s.dx = A.dx; s.dy = A.dy; s.dz = A.dz;
+                    s.rho = A.rho; s.rho2 = A.rho2; s.CA = A.CA;
+                    s.JA = A.JA; s.cull = A.cull;
+                    s.jseg = A.JA + (int)floorf((A.CA - g.rt - g.ksig) * g.inv_a) - 2;
+                    anc[e] = s;
+                }
+                __syncthreads();
+                const float *cf = cot + (size_t)f * E * g.nt;
+                for (int q = tid; q < E * SEG; q += ADJ_THREADS) {
+                    const int e = q / SEG, i = q - e * SEG;
+                    const int j = anc[e].jseg + i;
+                    seg[q] = (!anc[e].cull && j >= 0 && j < g.nt) ? __ldg(cf + (size_t)e * g.nt + j) : 0.0f;
+                }
+                __syncthreads();
+#pragma unroll 1
+                for (int e = 0; e < E; ++e) {
+                    const AncS s = anc[e];
+                    if (s.cull) {
+                        if (POSE && lane == 0) {
+                            wred[(warp * E + e) * 3 + 0] = 0.0f;
+                            wred[(warp * E + e) * 3 + 1] = 0.0f;
+                            wred[(warp * E + e) * 3 + 2] = 0.0f;
+                        }
+                        continue;
+                    }
+                    Anc A;
+                    A.dx2 = s.dx2; A.dy2 = s.dy2; A.dz2 = s.dz2;
+                    A.dx = s.dx; A.dy = s.dy; A.dz = s.dz;
+                    A.rho = s.rho; A.rho2 = s.rho2; A.CA = s.CA; A.JA = s.JA; A.cull = 0;
+                    const Pair p = pair<LMIN>(g, A, ex, ey, ez, e2);
+                    const bool valid = inside && p.jlo <= g.nt - 1 && p.jlo + p.L - 1 >= 0;
+                    int off = p.jlo - s.jseg;
+                    off = valid ? min(max(off, 0), SEG - LMAX) : 0;
+                    const float *gs = seg + e * SEG + off;
+                    const float D0 = __fmaf_rn(-(float)(p.jlo - s.JA), g.af, __fadd_rn(p.drel, s.CA));
+                    float Ev = ex2(-D0 * D0 * g.k2);
+                    const float q0 = ex2(__fmaf_rn(D0, g.two_a_k2, -g.a2_k2));
+                    float A1 = 0.0f, Bq = 0.0f;
+#pragma unroll
+                    for (int i = 0; i < LMAX; ++i) {
+                        const float gv = gs[i];
+                        const float D = __fmaf_rn(-(float)i, g.af, D0);
+                        const float t = gv * Ev;
+                        if (i < LMIN || i < p.L) {
+                            A1 = __fmaf_rn(t, D, A1);
+                            if (POSE) Bq = __fmaf_rn(t, __fmaf_rn(D, D, -g.s2), Bq);
+                        }
+                        Ev = Ev * (q0 * bp.B[i]);
+                    }
+                    if (!valid) {
+                        A1 = 0.0f;
+                        Bq = 0.0f;
+                    }
+                    if (ADJ) z = __fmaf_rn(A1, 0.5f * p.inv_r, z);
+                    if (POSE) {
+                        const float dLdr = P * 0.5f * p.inv_r * (-Bq * g.inv_s2 - A1 * p.inv_r);
+                        const float sc = -dLdr * p.inv_r;  // x - y_k = -(d + delta)
+                        float gx = sc * (s.dx + ex), gy = sc * (s.dy + ey), gz = sc * (s.dz + ez);
+                        gx = warp_sum(gx);
+                        gy = warp_sum(gy);
+                        gz = warp_sum(gz);
+                        if (lane == 0) {
+                            wred[(warp * E + e) * 3 + 0] = gx;
+                            wred[(warp * E + e) * 3 + 1] = gy;
+                            wred[(warp * E + e) * 3 + 2] = gz;
+                        }
+                    }
+                }
+                if (POSE) {
+                    __syncthreads();
+                    for (int q = tid; q < E * 3; q += ADJ_THREADS) {
+                        float s = 0.0f;
+#pragma unroll
+                        for (int w = 0; w < ADJ_THREADS / 32; ++w) s += wred[w * E * 3 + q];
+                        gacc[fl * E * 3 + q] += s;
+                    }
+                }
+            }
+            if (ADJ && inside) grad_p0[kidx] = (f0 == 0 ? 0.0f : grad_p0[kidx]) + z;
+        }
+        if (POSE) {
+            __syncthreads();
+            for (int q = tid; q < fn * E * 3; q += ADJ_THREADS)
+                partial[((size_t)blockIdx.x * F + f0) * E * 3 + q] = gacc[q];
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace pa
