@@ -549,7 +549,7 @@ pa_status adjoint_pose_core(pa_ctx *ctx, const Plan &pl, const float *tmpl, cons
     char *base = static_cast<char *>(ctx->ws) + ws_off;
     float *partial = reinterpret_cast<float *>(base);
     float *ge = grad_elem ? grad_elem : reinterpret_cast<float *>(base + part_b);
-    if (ctx->ev_adj || true) CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+    CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
     s = want_adj ? launch_adjoint<true, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, false, st)
                  : launch_adjoint<true, false>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, false, st);
     if (s) return s;
@@ -627,7 +627,8 @@ pa_status pa_adjoint(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
     Plan pl;
     pa_status s = make_plan(grid, acq, E, F, pl);
     if (s) return s;
-    if ((s = check_ptrs({tmpl, poses, cot, grad_p0}))) return s;
+    if ((s = check_ptrs({tmpl, grad_p0}))) return s;
+    if (F > 0 && (s = check_ptrs({poses, cot}))) return s;
     DevGuard dg(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
     if (F == 0) {
@@ -651,8 +652,8 @@ pa_status pa_adjoint_pose(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, c
     Plan pl;
     pa_status s = make_plan(grid, acq, E, F, pl);
     if (s) return s;
-    if ((s = check_ptrs({tmpl, poses, p0, cot, grad_p0}))) return s;
-    if (F > 0 && (s = check_ptrs({grad_pose}))) return s;
+    if ((s = check_ptrs({tmpl, p0, grad_p0}))) return s;
+    if (F > 0 && (s = check_ptrs({poses, cot, grad_pose}))) return s;
     if (grad_elem && !aligned4(grad_elem)) return fail(PA_ESHAPE, "misaligned grad_elem");
     DevGuard dg(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
