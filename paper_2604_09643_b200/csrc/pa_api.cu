@@ -85,6 +85,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     const double a = (double)acq->c * (double)acq->dt;
     const double sig = acq->sigma;
     g.a_d = a;
+    g.inv_a_d = 1.0 / a;
     g.ksig_d = (double)acq->kappa * sig;
     g.rt_d = 0.5 * g.h * std::sqrt((double)((TX - 1) * (TX - 1) + (TY - 1) * (TY - 1) + (TZ - 1) * (TZ - 1)));
     g.hf = grid->pitch;

@@ -29,7 +29,7 @@ struct Geo {
     int ntx, nty, ntz, ntiles;
     int E, F;
     double ox, oy, oz, h;       // grid (fp64 copies of the fp32 inputs)
-    double c, t0, a_d, ksig_d;  // a_d = c*dt in fp64
+    double c, t0, a_d, inv_a_d, ksig_d;  // a_d = c*dt in fp64
     double rt_d;                // tile half-diagonal (mm)
     float hf, af, inv_a, ksig;  // fp32 working constants
     float k2, two_a_k2, a2_k2;  // log2(e)/(2 s^2), 2a*k2, a^2*k2
@@ -75,7 +75,7 @@ __device__ __forceinline__ Anc make_anchor(const Geo &g, const double x[3], int 
     double dx = cx - x[0], dy = cy - x[1], dz = cz - x[2];
     double rho = sqrt(dx * dx + dy * dy + dz * dz);
     double D = rho - g.c * g.t0;
-    double JA = rint(D / g.a_d);
+    double JA = rint(D * g.inv_a_d);
     double CA = D - JA * g.a_d;
     Anc A;
     A.dx = (float)dx;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, BPow bp, cons
     const int TL = C::trace_len(g.nt);
     float *trw = sm + warp * C::warp_floats(g.nt);
     float *rows = trw + TL;
-    for (int i = lane; i < TL; i += 32) trw[i] = 0.0f;
+    for (int i = lane; i < C::warp_floats(g.nt); i += 32) trw[i] = 0.0f;  // trace + rows
 
     const int fe = blockIdx.x;
     const int f = fe / g.E, e = fe - f * g.E;
@@ -240,42 +240,57 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, BPow bp, cons
 #pragma unroll
         for (int i = 0; i < R; ++i) acc[i] = 0.0f;
         unsigned ovf = 0u;  // voxels whose jlo spread exceeds OMAX (never for supported geometry)
+        // two voxels per pass: two independent exp-recurrence chains per lane (ILP 2)
 #pragma unroll 1
-        for (int v = 0; v < 8; ++v) {
-            int o = jlo[v] - J;
-            float cv = coef[v];
-            if (cv != 0.0f && (o < 0 || o >= OMAX)) {
+        for (int v = 0; v < 8; v += 2) {
+            int oa = jlo[v] - J, ob = jlo[v + 1] - J;
+            float ca = coef[v], cb = coef[v + 1];
+            if (ca != 0.0f && (oa < 0 || oa >= OMAX)) {
                 ovf |= 1u << v;
-                cv = 0.0f;
+                ca = 0.0f;
             }
-            if (cv == 0.0f) o = 0;
-            const int oL = o + Lw[v];
-            const float DJ = __fmaf_rn(-(float)(J - A.JA), g.af, __fadd_rn(drel[v], A.CA));
-            float Ev = cv * ex2(-DJ * DJ * g.k2);
-            const float q0 = ex2(__fmaf_rn(DJ, g.two_a_k2, -g.a2_k2));
+            if (cb != 0.0f && (ob < 0 || ob >= OMAX)) {
+                ovf |= 2u << v;
+                cb = 0.0f;
+            }
+            if (ca == 0.0f) oa = 0;
+            if (cb == 0.0f) ob = 0;
+            const int oLa = oa + Lw[v], oLb = ob + Lw[v + 1];
+            const float jj = -(float)(J - A.JA);
+            const float DJa = __fmaf_rn(jj, g.af, __fadd_rn(drel[v], A.CA));
+            const float DJb = __fmaf_rn(jj, g.af, __fadd_rn(drel[v + 1], A.CA));
+            float Ea = ca * ex2(-DJa * DJa * g.k2);
+            float Eb = cb * ex2(-DJb * DJb * g.k2);
+            const float qa = ex2(__fmaf_rn(DJa, g.two_a_k2, -g.a2_k2));
+            const float qb = ex2(__fmaf_rn(DJb, g.two_a_k2, -g.a2_k2));
 #pragma unroll
             for (int i = 0; i < R; ++i) {
-                const float D = __fmaf_rn(-(float)i, g.af, DJ);
+                const float Da = __fmaf_rn(-(float)i, g.af, DJa);
+                const float Db = __fmaf_rn(-(float)i, g.af, DJb);
                 if (i < OMAX - 1) {
-                    if (i >= o) acc[i] = __fmaf_rn(Ev, D, acc[i]);
+                    if (i >= oa) acc[i] = __fmaf_rn(Ea, Da, acc[i]);
+                    if (i >= ob) acc[i] = __fmaf_rn(Eb, Db, acc[i]);
                 } else if (i < LMIN) {
-                    acc[i] = __fmaf_rn(Ev, D, acc[i]);
+                    acc[i] = __fmaf_rn(Ea, Da, acc[i]);
+                    acc[i] = __fmaf_rn(Eb, Db, acc[i]);
                 } else {
-                    if (i < oL) acc[i] = __fmaf_rn(Ev, D, acc[i]);
+                    if (i < oLa) acc[i] = __fmaf_rn(Ea, Da, acc[i]);
+                    if (i < oLb) acc[i] = __fmaf_rn(Eb, Db, acc[i]);
                 }
-                Ev = Ev * (q0 * bp.B[i]);
+                const float Bi = bp.B[i];
+                Ea = Ea * (qa * Bi);
+                Eb = Eb * (qb * Bi);
             }
         }
 
-        // ---- flush the 32 register windows into the warp trace (fixed order, no atomics)
+        // ---- flush the 32 register windows into the warp trace (fixed order, no atomics).
+        // rows[] is all-zero between flushes: each lane writes its window at column J-Jmin,
+        // the warp sums columns, then each lane clears what it wrote.
         const int Jmax = warp_max(J);
         if (Jmax - Jmin <= SPAN) {
-            float *row = rows + lane * C::SROW;
-            const int off = J - Jmin;
-            for (int c = 0; c < off; ++c) row[c] = 0.0f;
+            float *row = rows + lane * C::SROW + (J - Jmin);
 #pragma unroll
-            for (int i = 0; i < R; ++i) row[off + i] = acc[i];
-            for (int c = off + R; c < C::SROW - 1; ++c) row[c] = 0.0f;
+            for (int i = 0; i < R; ++i) row[i] = acc[i];
             __syncwarp();
             const int ncol = Jmax - Jmin + R;
             for (int c = lane; c < ncol; c += 32) {
@@ -284,6 +299,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, BPow bp, cons
                 for (int l = 0; l < 32; ++l) s += rows[l * C::SROW + c];
                 trw[C::PADL + Jmin + c] += s;
             }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < R; ++i) row[i] = 0.0f;
             __syncwarp();
         } else {
             // serialized fallback (not reached for supported geometry)
