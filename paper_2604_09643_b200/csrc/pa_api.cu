@@ -46,7 +46,8 @@ constexpr Klass kClasses[] = {{53, 11, 64, 128}, {26, 6, 32, 64}, {106, 21, 128,
 
 struct Plan {
     Geo g;
-    BPow bp;
+    FwdConst fc;
+    AdjConst ac;
     int klass;
 };
 
@@ -99,7 +100,6 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     g.s2 = (float)(sig * sig);
     g.inv_s2 = (float)(1.0 / (sig * sig));
     g.rt = (float)g.rt_d;
-    for (int i = 0; i < 128; ++i) pl.bp.B[i] = (float)std::exp(-(double)i * a * a / (sig * sig));
 
     const double K2 = 2.0 * g.ksig_d / a;
     const int wmin = (int)std::floor(K2);
@@ -112,6 +112,21 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
         if (c.lmin == wmin && o_need <= c.omax && span_need <= c.span && seg_need <= c.seg) {
             pl.klass = k;
             break;
+        }
+    }
+    if (pl.klass >= 0) {
+        const Klass &c = kClasses[pl.klass];
+        const double kc = g.ksig_d / a;  // window half-width in samples
+        g.mF = (int)std::lround(kc + 0.5 * (c.omax - 1));
+        g.mA = (int)std::lround(kc);
+        const double be = a * a / (2.0 * sig * sig);
+        for (int i = 0; i < 128; ++i) {
+            const double kf = i - g.mF, ka = i - g.mA;
+            pl.fc.C[i] = (float)std::exp(-kf * kf * be);
+            const double ca = std::exp(-ka * ka * be);
+            pl.ac.C0[i] = (float)ca;
+            pl.ac.C1[i] = (float)(ca * ka);
+            pl.ac.C2[i] = (float)(ca * ka * ka);
         }
     }
     if (pl.klass < 0)
@@ -460,7 +475,7 @@ pa_status launch_forward_t(const Plan &pl, const float *poses, const float *tmpl
     if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "nt=%d too long for the forward kernel's shared memory", pl.g.nt);
     auto kern = k_forward<LMIN, OMAX, SPAN>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<pl.g.F * pl.g.E, FWD_WARPS * 32, smem, st>>>(pl.g, pl.bp, poses, tmpl, p0, out, mode, meas, mask, rowloss);
+    kern<<<pl.g.F * pl.g.E, FWD_WARPS * 32, smem, st>>>(pl.g, pl.fc, poses, tmpl, p0, out, mode, meas, mask, rowloss);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
@@ -511,7 +526,7 @@ pa_status launch_adjoint_t(pa_ctx *ctx, const Plan &pl, const float *poses, cons
     L.Fc = Fc;
     L.smem = smem;
     if (dry) return PA_OK;
-    kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.bp, poses, tmpl, p0, cot, grad_p0, partial, Fc);
+    kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.ac, poses, tmpl, p0, cot, grad_p0, partial, Fc);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }

@@ -34,10 +34,19 @@ struct Geo {
     float hf, af, inv_a, ksig;  // fp32 working constants
     float k2, two_a_k2, a2_k2;  // log2(e)/(2 s^2), 2a*k2, a^2*k2
     float s2, inv_s2, rt;
+    int mF, mA;                 // recurrence centres (forward cluster window / adjoint pair window)
 };
 
-struct BPow {
-    float B[128];  // B^i = exp(-i a^2 / s^2)
+// Step-index constants of the factored Gaussian (DESIGN.md §6 "recurrence"):
+//   exp(-D_i^2/2s^2) = u_i * C_i,  D_i = D_m - (i - m) a,  C_i = exp(-(i-m)^2 a^2 / 2s^2),
+//   u_i = u_0 p^i,  p = exp(a D_m / s^2),  u_0 = exp(-(D_m^2 + 2 m a D_m) / 2s^2).
+struct FwdConst {
+    float C[128];  // C_i about the cluster-window centre mF
+};
+struct AdjConst {
+    float C0[128];  // C_i about the pair-window centre mA
+    float C1[128];  // C_i (i - mA)
+    float C2[128];  // C_i (i - mA)^2
 };
 
 struct Anc {
@@ -53,6 +62,20 @@ __device__ __forceinline__ float ex2(float x)
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// exp(x) for |x| <= 0.5 to ~1 ulp (degree-8 Taylor): the per-voxel ratio p of the recurrence,
+// whose rounding would otherwise compound over the window.
+__device__ __forceinline__ float exp_small(float x)
+{
+    float r = __fmaf_rn(x, 1.0f / 8.0f, 1.0f);
+    r = __fmaf_rn(x * (1.0f / 7.0f), r, 1.0f);
+    r = __fmaf_rn(x * (1.0f / 6.0f), r, 1.0f);
+    r = __fmaf_rn(x * (1.0f / 5.0f), r, 1.0f);
+    r = __fmaf_rn(x * (1.0f / 4.0f), r, 1.0f);
+    r = __fmaf_rn(x * (1.0f / 3.0f), r, 1.0f);
+    r = __fmaf_rn(x * 0.5f, r, 1.0f);
+    return __fmaf_rn(x, r, 1.0f);
 }
 
 __device__ __forceinline__ void elem_pos(const float *__restrict__ poses, const float *__restrict__ tmpl, int f, int e,
@@ -180,7 +203,7 @@ struct FwdCfg {
 enum { FWD_TRACE = 0, FWD_MSE = 1, FWD_NC = 2 };
 
 template <int LMIN, int OMAX, int SPAN>
-__global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, BPow bp, const float *__restrict__ poses,
+__global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
                                                             const float *__restrict__ tmpl,
                                                             const float *__restrict__ p0, float *__restrict__ out,
                                                             int mode, const float *__restrict__ meas,
@@ -259,29 +282,33 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, BPow bp, cons
             const float jj = -(float)(J - A.JA);
             const float DJa = __fmaf_rn(jj, g.af, __fadd_rn(drel[v], A.CA));
             const float DJb = __fmaf_rn(jj, g.af, __fadd_rn(drel[v + 1], A.CA));
-            float Ea = ca * ex2(-DJa * DJa * g.k2);
-            float Eb = cb * ex2(-DJb * DJb * g.k2);
-            const float qa = ex2(__fmaf_rn(DJa, g.two_a_k2, -g.a2_k2));
-            const float qb = ex2(__fmaf_rn(DJb, g.two_a_k2, -g.a2_k2));
+            const float mfa = (float)g.mF * g.af;
+            const float Dma = DJa - mfa, Dmb = DJb - mfa;
+            // u_0 = coef * exp(-(Dm^2 + 2 m a Dm)/2s^2), p = exp(a Dm / s^2)
+            float ua = ca * ex2(-g.k2 * Dma * (Dma + 2.0f * mfa));
+            float ub = cb * ex2(-g.k2 * Dmb * (Dmb + 2.0f * mfa));
+            const float pa = exp_small(g.af * g.inv_s2 * Dma);
+            const float pb = exp_small(g.af * g.inv_s2 * Dmb);
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 const float Da = __fmaf_rn(-(float)i, g.af, DJa);
                 const float Db = __fmaf_rn(-(float)i, g.af, DJb);
                 if (i < OMAX - 1) {
-                    if (i >= oa) acc[i] = __fmaf_rn(Ea, Da, acc[i]);
-                    if (i >= ob) acc[i] = __fmaf_rn(Eb, Db, acc[i]);
+                    if (i >= oa) acc[i] = __fmaf_rn(ua, Da, acc[i]);
+                    if (i >= ob) acc[i] = __fmaf_rn(ub, Db, acc[i]);
                 } else if (i < LMIN) {
-                    acc[i] = __fmaf_rn(Ea, Da, acc[i]);
-                    acc[i] = __fmaf_rn(Eb, Db, acc[i]);
+                    acc[i] = __fmaf_rn(ua, Da, acc[i]);
+                    acc[i] = __fmaf_rn(ub, Db, acc[i]);
                 } else {
-                    if (i < oLa) acc[i] = __fmaf_rn(Ea, Da, acc[i]);
-                    if (i < oLb) acc[i] = __fmaf_rn(Eb, Db, acc[i]);
+                    if (i < oLa) acc[i] = __fmaf_rn(ua, Da, acc[i]);
+                    if (i < oLb) acc[i] = __fmaf_rn(ub, Db, acc[i]);
                 }
-                const float Bi = bp.B[i];
-                Ea = Ea * (qa * Bi);
-                Eb = Eb * (qb * Bi);
+                ua *= pa;
+                ub *= pb;
             }
         }
+#pragma unroll
+        for (int i = 0; i < R; ++i) acc[i] *= fc.C[i];  // acc'_i C_i -> trace samples
 
         // ---- flush the 32 register windows into the warp trace (fixed order, no atomics).
         // rows[] is all-zero between flushes: each lane writes its window at column J-Jmin,
@@ -424,7 +451,7 @@ struct AncS {  // anchor as stored in shared memory (12 words)
 };
 
 template <int LMIN, int SEG, bool POSE, bool ADJ>
-__global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, BPow bp, const float *__restrict__ poses,
+__global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, const float *__restrict__ poses,
                                                            const float *__restrict__ tmpl,
                                                            const float *__restrict__ p0,
                                                            const float *__restrict__ cot, float *__restrict__ grad_p0,
@@ -500,20 +527,24 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, BPow bp, cons
                     off = valid ? min(max(off, 0), SEG - LMAX) : 0;
                     const float *gs = seg + e * SEG + off;
                     const float D0 = __fmaf_rn(-(float)(p.jlo - s.JA), g.af, __fadd_rn(p.drel, s.CA));
-                    float Ev = ex2(-D0 * D0 * g.k2);
-                    const float q0 = ex2(__fmaf_rn(D0, g.two_a_k2, -g.a2_k2));
-                    float A1 = 0.0f, Bq = 0.0f;
+                    const float maa = (float)g.mA * g.af;
+                    const float Dm = D0 - maa;  // D at the window centre step mA
+                    float u = ex2(-g.k2 * Dm * (Dm + 2.0f * maa));
+                    const float pr = exp_small(g.af * g.inv_s2 * Dm);
+                    float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f;  // sum g E k^n, k = i - mA
 #pragma unroll
                     for (int i = 0; i < LMAX; ++i) {
-                        const float gv = gs[i];
-                        const float D = __fmaf_rn(-(float)i, g.af, D0);
-                        const float t = gv * Ev;
+                        const float t = gs[i] * u;
                         if (i < LMIN || i < p.L) {
-                            A1 = __fmaf_rn(t, D, A1);
-                            if (POSE) Bq = __fmaf_rn(t, __fmaf_rn(D, D, -g.s2), Bq);
+                            S0 = __fmaf_rn(t, ac.C0[i], S0);
+                            S1 = __fmaf_rn(t, ac.C1[i], S1);
+                            if (POSE) S2 = __fmaf_rn(t, ac.C2[i], S2);
                         }
-                        Ev = Ev * (q0 * bp.B[i]);
+                        u *= pr;
                     }
+                    // A1 = sum g D E = Dm S0 - a S1 ;  Bq = sum g E (D^2 - s^2)
+                    float A1 = __fmaf_rn(-g.af, S1, Dm * S0);
+                    float Bq = POSE ? (Dm * Dm - g.s2) * S0 - 2.0f * g.af * Dm * S1 + g.af * g.af * S2 : 0.0f;
                     if (!valid) {
                         A1 = 0.0f;
                         Bq = 0.0f;

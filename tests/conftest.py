@@ -17,3 +17,26 @@ def cuda_available():
     import torch
 
     return torch.cuda.is_available()
+
+
+_PARITY = []
+
+
+@pytest.fixture
+def record_parity(request):
+    """record_parity(metric, value, tol): collected into $PARITY_OUT (json) at session end."""
+
+    def _rec(metric, value, tol):
+        _PARITY.append({"test": request.node.nodeid, "metric": metric, "value": float(value), "tol": float(tol)})
+
+    return _rec
+
+
+def pytest_sessionfinish(session, exitstatus):
+    out = os.environ.get("PARITY_OUT")
+    if out and _PARITY:
+        import json
+
+        os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
+        with open(out, "w") as fh:
+            json.dump(_PARITY, fh, indent=1)

@@ -77,19 +77,22 @@ def random_scene(seed, grid, E, F, standoff=3.0):
 
 
 # ------------------------------------------------------------------------------------ C1 parity
-def test_c1_forward_adjoint_pose_parity(ctx):
+def test_c1_forward_adjoint_pose_parity(ctx, record_parity):
     """BASELINE config 1 in full: 32^3 @ 0.2 mm sphere phantom, 64-element linear array, 512 samples."""
     w = gen.workload("c1")
     p0 = gen.phantom(w)
     cot = gen.random_cotangent((1, 64, 512), seed=7)
     (y, yo), (z, zo), (gp, po), (ge, geo) = run_all(ctx, w.grid, w.acq, w.tmpl, w.poses_true(), p0, cot)
+    for m, a, b, t in (("forward", y, yo, TOL_FA), ("adjoint", z, zo, TOL_FA), ("pose", gp, po, TOL_POSE),
+                       ("elem", ge, geo, TOL_POSE)):
+        record_parity(m, rel(a, b), t)
     assert rel(y, yo) <= TOL_FA, rel(y, yo)
     assert rel(z, zo) <= TOL_FA, rel(z, zo)
     assert rel(gp, po) <= TOL_POSE, rel(gp, po)
     assert rel(ge, geo) <= TOL_POSE, rel(ge, geo)
 
 
-def test_c1_tilted_pose_and_residual_cotangent(ctx):
+def test_c1_tilted_pose_and_residual_cotangent(ctx, record_parity):
     w = gen.workload("c1")
     p0 = gen.phantom(w)
     e = w.euler_true.copy()
@@ -99,12 +102,14 @@ def test_c1_tilted_pose_and_residual_cotangent(ctx):
     y_true = oracle.forward(grid32(w.grid), acq32(w.acq), f64(w.tmpl), f64(w.poses_true()), f64(p0))
     cot = 2.0 * (oracle.forward(grid32(w.grid), acq32(w.acq), f64(w.tmpl), f64(poses), f64(p0)) - y_true)
     (y, yo), (z, zo), (gp, po), _ = run_all(ctx, w.grid, w.acq, w.tmpl, poses, p0, cot)
+    for m, a, b, t in (("forward", y, yo, TOL_FA), ("adjoint", z, zo, TOL_FA), ("pose", gp, po, TOL_POSE)):
+        record_parity(m, rel(a, b), t)
     assert rel(y, yo) <= TOL_FA and rel(z, zo) <= TOL_FA and rel(gp, po) <= TOL_POSE, (rel(y, yo), rel(z, zo), rel(gp, po))
 
 
 # ------------------------------------------------------------------------------------ ragged multi-tile
 @pytest.mark.parametrize("shape", [(21, 19, 13), (8, 8, 4), (1, 1, 1), (33, 9, 5)])
-def test_ragged_multi_tile_multi_frame(ctx, shape):
+def test_ragged_multi_tile_multi_frame(ctx, shape, record_parity):
     """Grids that span several 8x8x4 tiles with ragged edges, several frames with random poses,
     nt not a multiple of anything, windows clipped at t0 and at nt."""
     grid = gen.make_grid(shape, 0.2)
@@ -113,13 +118,15 @@ def test_ragged_multi_tile_multi_frame(ctx, shape):
     p0 = gen.random_volume(grid, 4)
     cot = gen.random_cotangent((3, 5, 301), seed=5)
     (y, yo), (z, zo), (gp, po), (ge, geo) = run_all(ctx, grid, acq, tmpl, poses, p0, cot)
+    for m, a, b, t in (("forward", y, yo, TOL_FA), ("adjoint", z, zo, TOL_FA), ("pose", gp, po, TOL_POSE)):
+        record_parity(m, rel(a, b), t)
     assert rel(y, yo) <= TOL_FA, rel(y, yo)
     assert rel(z, zo) <= TOL_FA, rel(z, zo)
     assert rel(gp, po) <= TOL_POSE, rel(gp, po)
 
 
 @pytest.mark.parametrize("sigma,pitch,t0", [(0.1, 0.1, 3.0), (0.4, 0.4, 1.0), (0.2, 0.1, 2.0)])
-def test_other_window_classes(ctx, sigma, pitch, t0):
+def test_other_window_classes(ctx, record_parity, sigma, pitch, t0):
     """The C5 class (sigma = h = 0.1), the C3-coarse class (sigma = h = 0.4), and a finer grid."""
     grid = gen.make_grid((20, 18, 12), pitch)
     acq = gen.make_acq(700, sigma, t0=t0)
@@ -127,11 +134,13 @@ def test_other_window_classes(ctx, sigma, pitch, t0):
     p0 = gen.random_volume(grid, 12)
     cot = gen.random_cotangent((2, 4, 700), seed=13)
     (y, yo), (z, zo), (gp, po), _ = run_all(ctx, grid, acq, tmpl, poses, p0, cot)
+    for m, a, b, t in (("forward", y, yo, TOL_FA), ("adjoint", z, zo, TOL_FA), ("pose", gp, po, TOL_POSE)):
+        record_parity(m, rel(a, b), t)
     assert rel(y, yo) <= TOL_FA and rel(z, zo) <= TOL_FA and rel(gp, po) <= TOL_POSE, (rel(y, yo), rel(z, zo), rel(gp, po))
 
 
 # ------------------------------------------------------------------------------------ C2 geometry
-def test_c2_geometry_frame_element_subset(ctx):
+def test_c2_geometry_frame_element_subset(ctx, record_parity):
     """BASELINE config 2 geometry (128^3 vascular phantom, 128-element array, 1024 samples) on a
     deterministic frame/element subset small enough for the oracle."""
     w = gen.workload("c2")
@@ -141,6 +150,8 @@ def test_c2_geometry_frame_element_subset(ctx):
     poses = w.poses_true()[frames]
     cot = gen.random_cotangent((2, tmpl.shape[0], 1024), seed=21)
     (y, yo), (z, zo), (gp, po), _ = run_all(ctx, w.grid, w.acq, tmpl, poses, p0, cot)
+    for m, a, b, t in (("forward", y, yo, TOL_FA), ("adjoint", z, zo, TOL_FA), ("pose", gp, po, TOL_POSE)):
+        record_parity(m, rel(a, b), t)
     assert rel(y, yo) <= TOL_FA and rel(z, zo) <= TOL_FA and rel(gp, po) <= TOL_POSE, (rel(y, yo), rel(z, zo), rel(gp, po))
 
 
@@ -219,7 +230,7 @@ def test_loss_parity(ctx, kind):
 
 
 @pytest.mark.parametrize("loss_kind", [0, 1])
-def test_step_parity(ctx, loss_kind):
+def test_step_parity(ctx, loss_kind, record_parity):
     """pa_step vs oracle_step: loss, dL/dp0 (1e-4), dL/dEuler (1e-3); Adam updates compared where
     |g| > 1e-3 max|g| (R13: the first Adam step is sign-like)."""
     grid = gen.make_grid((16, 14, 12), 0.2)
@@ -242,6 +253,8 @@ def test_step_parity(ctx, loss_kind):
     torch.cuda.synchronize()
     assert abs(float(loss[0]) - out["loss"]) <= 1e-4 * abs(out["loss"])
     g = gbuf.cpu().numpy().ravel()
+    record_parity("step_grad_p0", rel(g, out["grad_p0"]), TOL_FA)
+    record_parity("step_grad_euler", rel(geul.cpu().numpy(), out["grad_euler"]), TOL_POSE)
     assert rel(g, out["grad_p0"]) <= TOL_FA
     assert rel(geul.cpu().numpy(), out["grad_euler"]) <= TOL_POSE
     big = np.abs(out["grad_p0"]) > 1e-3 * np.abs(out["grad_p0"]).max()
@@ -293,7 +306,7 @@ def test_empty_and_far(ctx):
 
 # ------------------------------------------------------------------------------------ full-size sampled parity
 @pytest.mark.parametrize("name", ["c2", "c4"])
-def test_full_size_sampled_parity(ctx, name):
+def test_full_size_sampled_parity(ctx, name, record_parity):
     """At the full BASELINE size and in the launch configuration bench.py times (all frames, all
     elements, full grid), compare sampled outputs the oracle can compute one by one:
     trace rows (f, e), adjoint voxels (via 1-voxel oracle grids at the exact fp64 centre),
@@ -310,6 +323,7 @@ def test_full_size_sampled_parity(ctx, name):
     # sampled trace rows
     for f, e in [(0, 0), (w.F // 2, w.E // 2), (w.F - 1, w.E - 1)]:
         yo = oracle.forward(grid, acq, f64(w.tmpl[e:e + 1]), f64(poses[f:f + 1]), f64(p0))[0, 0]
+        record_parity(f"forward_row_{f}_{e}", rel(y[f, e], yo), TOL_FA)
         assert rel(y[f, e], yo) <= TOL_FA, (f, e, rel(y[f, e], yo))
     # sampled adjoint voxels
     zs, zo = [], []
@@ -321,8 +335,10 @@ def test_full_size_sampled_parity(ctx, name):
         g1 = dict(nx=1, ny=1, nz=1, origin=o, pitch=grid["pitch"])
         zo.append(oracle.adjoint(g1, acq, f64(w.tmpl), f64(poses), f64(cot))[0, 0, 0])
         zs.append(gz[k, j, i])
+    record_parity("adjoint_sampled_voxels", rel(zs, zo), TOL_FA)
     assert rel(zs, zo) <= TOL_FA, rel(zs, zo)
     # sampled element-gradient rows
     for f, e in [(0, w.E // 3), (w.F - 1, 2 * w.E // 3)]:
         go = oracle.elem_grad(grid, acq, f64(w.tmpl[e:e + 1]), f64(poses[f:f + 1]), f64(p0), f64(cot[f:f + 1, e:e + 1]))
+        record_parity(f"elem_row_{f}_{e}", rel(ge[f, e], go[0, 0]), TOL_POSE)
         assert rel(ge[f, e], go[0, 0]) <= TOL_POSE, (f, e, rel(ge[f, e], go[0, 0]))
