@@ -13,7 +13,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpa.so")
+LIB_PATH = os.environ.get("PA_LIB_PATH", os.path.join(_HERE, "libpa.so"))
 
 PA_OK, PA_EINVAL, PA_ESHAPE, PA_EDEGENERATE, PA_ECUDA, PA_ENOMEM, PA_EUNSUPPORTED = range(7)
 _NAMES = {1: "PA_EINVAL", 2: "PA_ESHAPE", 3: "PA_EDEGENERATE", 4: "PA_ECUDA", 5: "PA_ENOMEM", 6: "PA_EUNSUPPORTED"}
