@@ -124,6 +124,27 @@ def _stream(stream):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def make_allreduce_callback(tensors, allreduce):
+    """C callback for pa_step: maps the raw pointer libpa passes back to the torch tensor that
+    owns it and calls `allreduce(tensor)` (in place, e.g. torch.distributed SUM).  Non-zero return
+    = failure (pa_step then returns PA_ECUDA)."""
+    views = {t.data_ptr(): t for t in tensors}
+
+    def _cb(buf, n, stream_ptr, user):
+        try:
+            t = views[buf]
+            if t.numel() != n:
+                return 2
+            allreduce(t)
+            return 0
+        except Exception:  # noqa: BLE001 - reported through the status code
+            return 1
+
+    cb = ALLREDUCE_FN(_cb)
+    cb._views = views  # keep the tensors alive with the callback
+    return cb
+
+
 class Context:
     """Owns a pa_ctx (libpa's internal workspace) for one device; use one per stream."""
 
@@ -218,18 +239,7 @@ class Context:
         c.update_p0, c.update_pose = int(cfg.get("update_p0", 1)), int(cfg.get("update_pose", 1))
         cb = ALLREDUCE_FN(0)
         if allreduce is not None:
-            views = {grad_p0.data_ptr(): grad_p0.view(-1), loss.data_ptr() + 4: loss[1:2]}
-
-            def _cb(buf, n, stream_ptr, user):
-                try:
-                    t = views[buf]
-                    assert t.numel() == n
-                    allreduce(t)
-                    return 0
-                except Exception:  # noqa: BLE001 - reported through the status code
-                    return 1
-
-            cb = ALLREDUCE_FN(_cb)
+            cb = make_allreduce_callback([grad_p0.view(-1), loss[1:2]], allreduce)
         m = None if row_mask is None else row_mask.to(torch.uint8).contiguous()
         _check(self.lib.pa_step(self.h, ctypes.byref(make_grid(grid)), ctypes.byref(make_acq(acq)), _f32(tmpl), E, F,
                                 _f32(meas), _ptr(m), _f32(p0), _f32(euler_t), _f32(adam_p0), _f32(adam_pose),
