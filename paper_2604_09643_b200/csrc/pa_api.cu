@@ -117,7 +117,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     if (pl.klass >= 0) {
         const Klass &c = kClasses[pl.klass];
         const double kc = g.ksig_d / a;  // window half-width in samples
-        g.mF = (int)std::lround(kc + 0.5 * (c.omax - 1));
+        g.mF = (c.lmin + c.omax) / 2;  // == FwdMid<LMIN,OMAX>::m
         g.mA = (int)std::lround(kc);
         const double be = a * a / (2.0 * sig * sig);
         for (int i = 0; i < 128; ++i) {

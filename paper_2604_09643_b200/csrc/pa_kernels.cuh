@@ -194,13 +194,21 @@ __device__ __forceinline__ int warp_max(int v)
 template <int LMIN, int OMAX, int SPAN>
 struct FwdCfg {
     static constexpr int R = LMIN + OMAX;
-    static constexpr int SROW = R + SPAN + 1;  // +1: bank skew
+    static constexpr int NCOL = R + SPAN;   // columns of the flush buffer (window + tile spread)
+    static constexpr int CSTR = 36;         // column stride (floats): 16-B aligned, bank-skewed
     static constexpr int PADL = LMIN + 2;
-    static __host__ __device__ int trace_len(int nt) { return PADL + nt + R + SPAN + 1; }
-    static __host__ __device__ int warp_floats(int nt) { return trace_len(nt) + 32 * SROW; }
+    static __host__ __device__ int trace_len(int nt) { return PADL + nt + NCOL + 1; }
+    static __host__ __device__ int warp_floats(int nt) { return ((trace_len(nt) + 3) & ~3) + NCOL * CSTR; }
 };
 
 enum { FWD_TRACE = 0, FWD_MSE = 1, FWD_NC = 2 };
+
+// Centre step of the forward register window, m = round(L_min/2 + (OMAX-1)/2) — the host sets
+// Geo::mF to the same value (checked in make_plan).
+template <int LMIN, int OMAX>
+struct FwdMid {
+    static constexpr int m = (LMIN + OMAX) / 2;
+};
 
 template <int LMIN, int OMAX, int SPAN>
 __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
@@ -214,9 +222,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, FwdConst fc, 
     constexpr int R = C::R;
     extern __shared__ float sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int TL = C::trace_len(g.nt);
+    const int TL = (C::trace_len(g.nt) + 3) & ~3;
     float *trw = sm + warp * C::warp_floats(g.nt);
-    float *rows = trw + TL;
+    float *cols = trw + TL;  // [NCOL][CSTR]: entry (c, lane) = lane's window value at column c
     for (int i = lane; i < C::warp_floats(g.nt); i += 32) trw[i] = 0.0f;  // trace + rows
 
     const int fe = blockIdx.x;
@@ -232,42 +240,57 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, FwdConst fc, 
         const Anc A = make_anchor(g, x, tx, ty, tz);
         if (A.cull) continue;  // warp-uniform
 
-        float drel[8], coef[8];
-        int jlo[8], Lw[8];
-        int J = 0x7fffffff;
+        // cluster geometry: voxel (2cx+vx, 2cy+vy, 2cz+vz) of the tile; offsets from the tile centre
+        const int bx = TX * tx + 2 * cx, by = TY * ty + 2 * cy, bz = TZ * tz + 2 * cz;
+        const float ex0 = ((float)(2 * cx) - 0.5f * (TX - 1)) * g.hf;
+        const float ey0 = ((float)(2 * cy) - 0.5f * (TY - 1)) * g.hf;
+        const float ez0 = ((float)(2 * cz) - 0.5f * (TZ - 1)) * g.hf;
+        float P[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-            const int lx = 2 * cx + (v & 1), ly = 2 * cy + ((v >> 1) & 1), lz = 2 * cz + (v >> 2);
-            const int ix = TX * tx + lx, iy = TY * ty + ly, iz = TZ * tz + lz;
-            const bool inside = ix < g.nx && iy < g.ny && iz < g.nz;
-            const float ex = ((float)lx - 0.5f * (TX - 1)) * g.hf;
-            const float ey = ((float)ly - 0.5f * (TY - 1)) * g.hf;
-            const float ez = ((float)lz - 0.5f * (TZ - 1)) * g.hf;
-            const float e2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
-            const Pair p = pair<LMIN>(g, A, ex, ey, ez, e2);
-            const float P = inside ? __ldg(p0 + ((size_t)iz * g.ny + iy) * g.nx + ix) : 0.0f;
-            const bool valid = inside && p.jlo <= g.nt - 1 && p.jlo + p.L - 1 >= 0;
-            drel[v] = p.drel;
-            jlo[v] = p.jlo;
-            Lw[v] = p.L;
-            coef[v] = valid ? P * 0.5f * p.inv_r : 0.0f;
-            if (valid) J = min(J, p.jlo);
+            const int ix = bx + (v & 1), iy = by + ((v >> 1) & 1), iz = bz + (v >> 2);
+            P[v] = (ix < g.nx && iy < g.ny && iz < g.nz) ? __ldg(p0 + ((size_t)iz * g.ny + iy) * g.nx + ix) : 0.0f;
         }
-        const bool any = J != 0x7fffffff;
-        const unsigned anym = __ballot_sync(0xffffffffu, any);
-        if (anym == 0u) continue;
+        // window base: jlo of the cluster voxel closest to the element (exact minimiser of |d+delta|
+        // coordinate-wise); other voxels have jlo >= J (up to rounding, handled by the slow path)
+        const int qx = (A.dx + ex0 + 0.5f * g.hf > 0.0f) ? 0 : 1;
+        const int qy = (A.dy + ey0 + 0.5f * g.hf > 0.0f) ? 0 : 1;
+        const int qz = (A.dz + ez0 + 0.5f * g.hf > 0.0f) ? 0 : 1;
+        int J;
+        {
+            const float exq = ((float)(2 * cx + qx) - 0.5f * (TX - 1)) * g.hf;
+            const float eyq = ((float)(2 * cy + qy) - 0.5f * (TY - 1)) * g.hf;
+            const float ezq = ((float)(2 * cz + qz) - 0.5f * (TZ - 1)) * g.hf;
+            const float e2q = __fmaf_rn(exq, exq, __fmaf_rn(eyq, eyq, __fmul_rn(ezq, ezq)));
+            J = pair<LMIN>(g, A, exq, eyq, ezq, e2q).jlo;
+        }
+        J = max(J, -(LMIN + 1));  // windows ending before 0 contribute nothing
+        const bool any = J <= g.nt - 1;
+        if (!__any_sync(0xffffffffu, any)) continue;
         const int Jmin = warp_min(any ? J : 0x7fffffff);
         if (!any) J = Jmin;
 
         float acc[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) acc[i] = 0.0f;
-        unsigned ovf = 0u;  // voxels whose jlo spread exceeds OMAX (never for supported geometry)
-        // two voxels per pass: two independent exp-recurrence chains per lane (ILP 2)
+        unsigned ovf = 0u;  // voxels with jlo outside [J, J+OMAX) (rounding corner cases)
+        const float mfa = (float)g.mF * g.af;
+        const float jj = -(float)(J - A.JA);
+        // two voxels per pass (ILP 2); the recurrence runs centre-out from step mF
 #pragma unroll 1
         for (int v = 0; v < 8; v += 2) {
-            int oa = jlo[v] - J, ob = jlo[v + 1] - J;
-            float ca = coef[v], cb = coef[v + 1];
+            const int vy = (v >> 1) & 1, vz = v >> 2;
+            const float ey = ((float)(2 * cy + vy) - 0.5f * (TY - 1)) * g.hf;
+            const float ez = ((float)(2 * cz + vz) - 0.5f * (TZ - 1)) * g.hf;
+            const float exa = ex0, exb = ex0 + g.hf;
+            const float eyz2 = __fmaf_rn(ey, ey, __fmul_rn(ez, ez));
+            const Pair pa = pair<LMIN>(g, A, exa, ey, ez, __fmaf_rn(exa, exa, eyz2));
+            const Pair pb = pair<LMIN>(g, A, exb, ey, ez, __fmaf_rn(exb, exb, eyz2));
+            const bool ina = bx < g.nx && by + vy < g.ny && bz + vz < g.nz;
+            const bool inb = bx + 1 < g.nx && by + vy < g.ny && bz + vz < g.nz;
+            float ca = (ina && pa.jlo <= g.nt - 1 && pa.jlo + pa.L - 1 >= 0) ? P[v] * 0.5f * pa.inv_r : 0.0f;
+            float cb = (inb && pb.jlo <= g.nt - 1 && pb.jlo + pb.L - 1 >= 0) ? P[v + 1] * 0.5f * pb.inv_r : 0.0f;
+            int oa = pa.jlo - J, ob = pb.jlo - J;
             if (ca != 0.0f && (oa < 0 || oa >= OMAX)) {
                 ovf |= 1u << v;
                 ca = 0.0f;
@@ -278,69 +301,85 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, FwdConst fc, 
             }
             if (ca == 0.0f) oa = 0;
             if (cb == 0.0f) ob = 0;
-            const int oLa = oa + Lw[v], oLb = ob + Lw[v + 1];
-            const float jj = -(float)(J - A.JA);
-            const float DJa = __fmaf_rn(jj, g.af, __fadd_rn(drel[v], A.CA));
-            const float DJb = __fmaf_rn(jj, g.af, __fadd_rn(drel[v + 1], A.CA));
-            const float mfa = (float)g.mF * g.af;
-            const float Dma = DJa - mfa, Dmb = DJb - mfa;
-            // u_0 = coef * exp(-(Dm^2 + 2 m a Dm)/2s^2), p = exp(a Dm / s^2)
-            float ua = ca * ex2(-g.k2 * Dma * (Dma + 2.0f * mfa));
-            float ub = cb * ex2(-g.k2 * Dmb * (Dmb + 2.0f * mfa));
-            const float pa = exp_small(g.af * g.inv_s2 * Dma);
-            const float pb = exp_small(g.af * g.inv_s2 * Dmb);
+            const int oLa = oa + pa.L, oLb = ob + pb.L;
+            const float DJa = __fmaf_rn(jj, g.af, __fadd_rn(pa.drel, A.CA));
+            const float DJb = __fmaf_rn(jj, g.af, __fadd_rn(pb.drel, A.CA));
+            const float Dma = DJa - mfa, Dmb = DJb - mfa;  // D at the centre step mF
+            // u_mF = E(D_m) (C_mF = 1); p = exp(a D_m / s^2); walk up with p, down with 1/p
+            const float uma = ca * ex2(-g.k2 * Dma * Dma), umb = cb * ex2(-g.k2 * Dmb * Dmb);
+            const float la = 2.0f * g.k2 * g.af * Dma, lb = 2.0f * g.k2 * g.af * Dmb;
+            const float pa_ = ex2(la), pb_ = ex2(lb), qa_ = ex2(-la), qb_ = ex2(-lb);
+            float ua = uma, ub = umb;
 #pragma unroll
-            for (int i = 0; i < R; ++i) {
+            for (int i = FwdMid<LMIN, OMAX>::m; i < R; ++i) {
                 const float Da = __fmaf_rn(-(float)i, g.af, DJa);
                 const float Db = __fmaf_rn(-(float)i, g.af, DJb);
-                if (i < OMAX - 1) {
-                    if (i >= oa) acc[i] = __fmaf_rn(ua, Da, acc[i]);
-                    if (i >= ob) acc[i] = __fmaf_rn(ub, Db, acc[i]);
-                } else if (i < LMIN) {
+                if (i < LMIN) {
                     acc[i] = __fmaf_rn(ua, Da, acc[i]);
                     acc[i] = __fmaf_rn(ub, Db, acc[i]);
                 } else {
                     if (i < oLa) acc[i] = __fmaf_rn(ua, Da, acc[i]);
                     if (i < oLb) acc[i] = __fmaf_rn(ub, Db, acc[i]);
                 }
-                ua *= pa;
-                ub *= pb;
+                ua *= pa_;
+                ub *= pb_;
+            }
+            ua = uma * qa_;
+            ub = umb * qb_;
+#pragma unroll
+            for (int i = FwdMid<LMIN, OMAX>::m - 1; i >= 0; --i) {
+                const float Da = __fmaf_rn(-(float)i, g.af, DJa);
+                const float Db = __fmaf_rn(-(float)i, g.af, DJb);
+                if (i < OMAX - 1) {
+                    if (i >= oa) acc[i] = __fmaf_rn(ua, Da, acc[i]);
+                    if (i >= ob) acc[i] = __fmaf_rn(ub, Db, acc[i]);
+                } else {
+                    acc[i] = __fmaf_rn(ua, Da, acc[i]);
+                    acc[i] = __fmaf_rn(ub, Db, acc[i]);
+                }
+                ua *= qa_;
+                ub *= qb_;
             }
         }
-#pragma unroll
-        for (int i = 0; i < R; ++i) acc[i] *= fc.C[i];  // acc'_i C_i -> trace samples
 
-        // ---- flush the 32 register windows into the warp trace (fixed order, no atomics).
-        // rows[] is all-zero between flushes: each lane writes its window at column J-Jmin,
-        // the warp sums columns, then each lane clears what it wrote.
+        // ---- flush: lane l writes C_i acc'_i into column (J - Jmin + i), row l, of the
+        // column-major buffer (zero between flushes); each lane then sums whole columns with
+        // 128-bit loads (4 independent partial sums, fixed order) into the warp trace.
         const int Jmax = warp_max(J);
         if (Jmax - Jmin <= SPAN) {
-            float *row = rows + lane * C::SROW + (J - Jmin);
+            float *w = cols + (J - Jmin) * C::CSTR + lane;
 #pragma unroll
-            for (int i = 0; i < R; ++i) row[i] = acc[i];
+            for (int i = 0; i < R; ++i) w[i * C::CSTR] = acc[i] * fc.C[i];
             __syncwarp();
             const int ncol = Jmax - Jmin + R;
             for (int c = lane; c < ncol; c += 32) {
-                float s = 0.0f;
-#pragma unroll 8
-                for (int l = 0; l < 32; ++l) s += rows[l * C::SROW + c];
-                trw[C::PADL + Jmin + c] += s;
+                const float4 *col = reinterpret_cast<const float4 *>(cols + c * C::CSTR);
+                float4 s4 = col[0];
+#pragma unroll
+                for (int q = 1; q < 8; ++q) {
+                    const float4 t = col[q];
+                    s4.x += t.x;
+                    s4.y += t.y;
+                    s4.z += t.z;
+                    s4.w += t.w;
+                }
+                trw[C::PADL + Jmin + c] += (s4.x + s4.y) + (s4.z + s4.w);
             }
             __syncwarp();
 #pragma unroll
-            for (int i = 0; i < R; ++i) row[i] = 0.0f;
+            for (int i = 0; i < R; ++i) w[i * C::CSTR] = 0.0f;
             __syncwarp();
         } else {
             // serialized fallback (not reached for supported geometry)
             for (int l = 0; l < 32; ++l) {
                 if (lane == l) {
 #pragma unroll
-                    for (int i = 0; i < R; ++i) trw[C::PADL + J + i] += acc[i];
+                    for (int i = 0; i < R; ++i) trw[C::PADL + J + i] += acc[i] * fc.C[i];
                 }
                 __syncwarp();
             }
         }
-        // ---- exact slow path for any overflow voxel (lane-serialised, direct exp)
+        // ---- exact slow path for any voxel outside the register window (lane-serialised)
         const unsigned ovm = __ballot_sync(0xffffffffu, ovf != 0u);
         if (ovm) {
             for (int l = 0; l < 32; ++l) {
@@ -348,10 +387,16 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, FwdConst fc, 
                 if (lane == l) {
                     for (int v = 0; v < 8; ++v) {
                         if (!((ovf >> v) & 1u)) continue;
-                        for (int i = 0; i < Lw[v]; ++i) {
-                            const int j = jlo[v] + i;
-                            const float D = __fmaf_rn(-(float)(j - A.JA), g.af, __fadd_rn(drel[v], A.CA));
-                            trw[C::PADL + j] += coef[v] * D * ex2(-D * D * g.k2);
+                        const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
+                        const float ex = ((float)(2 * cx + vx) - 0.5f * (TX - 1)) * g.hf;
+                        const float ey = ((float)(2 * cy + vy) - 0.5f * (TY - 1)) * g.hf;
+                        const float ez = ((float)(2 * cz + vz) - 0.5f * (TZ - 1)) * g.hf;
+                        const Pair pv = pair<LMIN>(g, A, ex, ey, ez, __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez))));
+                        const float cv = P[v] * 0.5f * pv.inv_r;
+                        for (int i = 0; i < pv.L; ++i) {
+                            const int j = pv.jlo + i;
+                            const float D = __fmaf_rn(-(float)(j - A.JA), g.af, __fadd_rn(pv.drel, A.CA));
+                            if (j >= 0 && j < g.nt) trw[C::PADL + j] += cv * D * ex2(-D * D * g.k2);
                         }
                     }
                 }
