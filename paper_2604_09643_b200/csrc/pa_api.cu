@@ -118,7 +118,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
         const Klass &c = kClasses[pl.klass];
         const double kc = g.ksig_d / a;  // window half-width in samples
         g.mF = (c.lmin + c.omax) / 2;  // == FwdMid<LMIN,OMAX>::m
-        g.mA = (int)std::lround(kc);
+        g.mA = (c.lmin + 1) / 2;  // == AdjMid<LMIN>::m
         const double be = a * a / (2.0 * sig * sig);
         for (int i = 0; i < 128; ++i) {
             const double kf = i - g.mF, ka = i - g.mA;

@@ -490,6 +490,12 @@ struct AdjCfg {
     }
 };
 
+// Centre step of the adjoint pair window (host Geo::mA must equal it, set in make_plan).
+template <int LMIN>
+struct AdjMid {
+    static constexpr int m = (LMIN + 1) / 2;
+};
+
 struct AncS {  // anchor as stored in shared memory (12 words)
     float dx2, dy2, dz2, dx, dy, dz, rho, rho2, CA;
     int JA, cull, jseg;
@@ -552,60 +558,96 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                 }
                 __syncthreads();
 #pragma unroll 1
-                for (int e = 0; e < E; ++e) {
-                    const AncS s = anc[e];
-                    if (s.cull) {
-                        if (POSE && lane == 0) {
-                            wred[(warp * E + e) * 3 + 0] = 0.0f;
-                            wred[(warp * E + e) * 3 + 1] = 0.0f;
-                            wred[(warp * E + e) * 3 + 2] = 0.0f;
-                        }
-                        continue;
-                    }
-                    Anc A;
-                    A.dx2 = s.dx2; A.dy2 = s.dy2; A.dz2 = s.dz2;
-                    A.dx = s.dx; A.dy = s.dy; A.dz = s.dz;
-                    A.rho = s.rho; A.rho2 = s.rho2; A.CA = s.CA; A.JA = s.JA; A.cull = 0;
-                    const Pair p = pair<LMIN>(g, A, ex, ey, ez, e2);
-                    const bool valid = inside && p.jlo <= g.nt - 1 && p.jlo + p.L - 1 >= 0;
-                    int off = p.jlo - s.jseg;
-                    off = valid ? min(max(off, 0), SEG - LMAX) : 0;
-                    const float *gs = seg + e * SEG + off;
-                    const float D0 = __fmaf_rn(-(float)(p.jlo - s.JA), g.af, __fadd_rn(p.drel, s.CA));
-                    const float maa = (float)g.mA * g.af;
-                    const float Dm = D0 - maa;  // D at the window centre step mA
-                    float u = ex2(-g.k2 * Dm * (Dm + 2.0f * maa));
-                    const float pr = exp_small(g.af * g.inv_s2 * Dm);
-                    float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f;  // sum g E k^n, k = i - mA
+                for (int e0 = 0; e0 < E; e0 += 4) {
+                    float G[4][3];
 #pragma unroll
-                    for (int i = 0; i < LMAX; ++i) {
-                        const float t = gs[i] * u;
-                        if (i < LMIN || i < p.L) {
+                    for (int q = 0; q < 4; ++q) {
+                        const int e = e0 + q;
+                        G[q][0] = G[q][1] = G[q][2] = 0.0f;
+                        if (e >= E) continue;  // uniform
+                        const AncS s = anc[e];
+                        if (s.cull) continue;  // uniform
+                        Anc A;
+                        A.dx2 = s.dx2; A.dy2 = s.dy2; A.dz2 = s.dz2;
+                        A.dx = s.dx; A.dy = s.dy; A.dz = s.dz;
+                        A.rho = s.rho; A.rho2 = s.rho2; A.CA = s.CA; A.JA = s.JA; A.cull = 0;
+                        const Pair p = pair<LMIN>(g, A, ex, ey, ez, e2);
+                        const bool valid = inside && p.jlo <= g.nt - 1 && p.jlo + p.L - 1 >= 0;
+                        int off = p.jlo - s.jseg;
+                        off = valid ? min(max(off, 0), SEG - LMAX) : 0;
+                        const float *gs = seg + e * SEG + off;
+                        const float D0 = __fmaf_rn(-(float)(p.jlo - s.JA), g.af, __fadd_rn(p.drel, s.CA));
+                        constexpr int MA = AdjMid<LMIN>::m;
+                        const float Dm = D0 - (float)MA * g.af;  // D at the window centre step MA
+                        // centre-out: u_MA = E(D_m); up with p = exp(a D_m/s^2), down with 1/p
+                        const float um = ex2(-g.k2 * Dm * Dm);
+                        const float l2 = 2.0f * g.k2 * g.af * Dm;
+                        const float pu = ex2(l2), pd = ex2(-l2);
+                        float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f;  // sum g E k^n, k = i - MA
+                        float u = um;
+#pragma unroll
+                        for (int i = MA; i < LMAX; ++i) {
+                            const float t = gs[i] * u;
+                            if (i < LMIN || i < p.L) {
+                                S0 = __fmaf_rn(t, ac.C0[i], S0);
+                                S1 = __fmaf_rn(t, ac.C1[i], S1);
+                                if (POSE) S2 = __fmaf_rn(t, ac.C2[i], S2);
+                            }
+                            u *= pu;
+                        }
+                        u = um * pd;
+#pragma unroll
+                        for (int i = MA - 1; i >= 0; --i) {
+                            const float t = gs[i] * u;
                             S0 = __fmaf_rn(t, ac.C0[i], S0);
                             S1 = __fmaf_rn(t, ac.C1[i], S1);
                             if (POSE) S2 = __fmaf_rn(t, ac.C2[i], S2);
+                            u *= pd;
                         }
-                        u *= pr;
+                        // A1 = sum g D E = Dm S0 - a S1 ;  Bq = sum g E (D^2 - s^2)
+                        float A1 = __fmaf_rn(-g.af, S1, Dm * S0);
+                        float Bq = POSE ? (Dm * Dm - g.s2) * S0 - 2.0f * g.af * Dm * S1 + g.af * g.af * S2 : 0.0f;
+                        if (!valid) {
+                            A1 = 0.0f;
+                            Bq = 0.0f;
+                        }
+                        if (ADJ) z = __fmaf_rn(A1, 0.5f * p.inv_r, z);
+                        if (POSE) {
+                            const float dLdr = P * 0.5f * p.inv_r * (-Bq * g.inv_s2 - A1 * p.inv_r);
+                            const float sc = -dLdr * p.inv_r;  // x - y_k = -(d + delta)
+                            G[q][0] = sc * (s.dx + ex);
+                            G[q][1] = sc * (s.dy + ey);
+                            G[q][2] = sc * (s.dz + ez);
+                        }
                     }
-                    // A1 = sum g D E = Dm S0 - a S1 ;  Bq = sum g E (D^2 - s^2)
-                    float A1 = __fmaf_rn(-g.af, S1, Dm * S0);
-                    float Bq = POSE ? (Dm * Dm - g.s2) * S0 - 2.0f * g.af * Dm * S1 + g.af * g.af * S2 : 0.0f;
-                    if (!valid) {
-                        A1 = 0.0f;
-                        Bq = 0.0f;
-                    }
-                    if (ADJ) z = __fmaf_rn(A1, 0.5f * p.inv_r, z);
                     if (POSE) {
-                        const float dLdr = P * 0.5f * p.inv_r * (-Bq * g.inv_s2 - A1 * p.inv_r);
-                        const float sc = -dLdr * p.inv_r;  // x - y_k = -(d + delta)
-                        float gx = sc * (s.dx + ex), gy = sc * (s.dy + ey), gz = sc * (s.dz + ez);
-                        gx = warp_sum(gx);
-                        gy = warp_sum(gy);
-                        gz = warp_sum(gz);
-                        if (lane == 0) {
-                            wred[(warp * E + e) * 3 + 0] = gx;
-                            wred[(warp * E + e) * 3 + 1] = gy;
-                            wred[(warp * E + e) * 3 + 2] = gz;
+                        // transposed warp reduction of 4 elements x 3 components (54 instr / 4 elements)
+                        const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+                        float r6[6];
+#pragma unroll
+                        for (int j = 0; j < 6; ++j) {
+                            const float lo = G[j / 3][j % 3], hi = G[2 + j / 3][j % 3];
+                            const float snd = h16 ? lo : hi, kp = h16 ? hi : lo;
+                            r6[j] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+                        }
+                        float r3[3];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const float lo = r6[c], hi = r6[3 + c];
+                            const float snd = h8 ? lo : hi, kp = h8 ? hi : lo;
+                            r3[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 4);
+                            r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 2);
+                            r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 1);
+                        }
+                        const int e = e0 + ((lane >> 3) & 3);
+                        if ((lane & 7) == 0 && e < E) {
+                            wred[(warp * E + e) * 3 + 0] = r3[0];
+                            wred[(warp * E + e) * 3 + 1] = r3[1];
+                            wred[(warp * E + e) * 3 + 2] = r3[2];
                         }
                     }
                 }
