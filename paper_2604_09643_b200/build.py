@@ -10,7 +10,7 @@ SRC = [os.path.join(HERE, "csrc", "pa_api.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "pa_kernels.cuh"), os.path.join(ROOT, "include", "pa.h")]
 LIB = os.path.join(HERE, "libpa.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xcompiler", "-fPIC",
+FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-ftz=true", "-Xcompiler", "-fPIC",
          "-shared", "-Xptxas", "-warn-spills"]
 
 

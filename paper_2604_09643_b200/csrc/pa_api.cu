@@ -42,7 +42,7 @@ struct Klass {
 // Compiled window classes: sigma/(c dt) in {5.33, 2.67, 10.67} at kappa = 5
 // for the BASELINE configs; any geometry whose L_min, cluster spread, tile span and
 // segment need fit a class is supported.
-constexpr Klass kClasses[] = {{53, 11, 64, 128}, {26, 6, 32, 64}, {106, 21, 128, 256}};
+constexpr Klass kClasses[] = {{53, 11, 58, 128}, {26, 6, 30, 64}, {106, 21, 114, 256}};
 
 struct Plan {
     Geo g;
@@ -104,7 +104,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     const double K2 = 2.0 * g.ksig_d / a;
     const int wmin = (int)std::floor(K2);
     const int o_need = (int)std::floor(std::sqrt(3.0) * g.h / a) + 2;
-    const int span_need = (int)std::ceil(2.0 * g.rt_d / a) + 3;
+    const int span_need = (int)std::ceil(2.0 * g.rt_d / a) + 2;  // max lane window-base spread in a tile
     const int seg_need = (int)std::ceil(2.0 * g.rt_d / a) + 5 + (wmin + 1);
     pl.klass = -1;
     for (int k = 0; k < (int)(sizeof kClasses / sizeof kClasses[0]); ++k) {
@@ -484,9 +484,9 @@ pa_status launch_forward(const Plan &pl, const float *poses, const float *tmpl, 
                          const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
 {
     switch (pl.klass) {
-    case 0: return launch_forward_t<53, 11, 64>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    case 1: return launch_forward_t<26, 6, 32>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    default: return launch_forward_t<106, 21, 128>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    case 0: return launch_forward_t<53, 11, 58>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    case 1: return launch_forward_t<26, 6, 30>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    default: return launch_forward_t<106, 21, 114>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
     }
 }
 

@@ -195,7 +195,7 @@ template <int LMIN, int OMAX, int SPAN>
 struct FwdCfg {
     static constexpr int R = LMIN + OMAX;
     static constexpr int NCOL = R + SPAN;   // columns of the flush buffer (window + tile spread)
-    static constexpr int CSTR = 36;         // column stride (floats): 16-B aligned, bank-skewed
+    static constexpr int CSTR = 20;         // column stride (floats): 16 lanes + skew, 16-B aligned
     static constexpr int PADL = LMIN + 2;
     static __host__ __device__ int trace_len(int nt) { return PADL + nt + NCOL + 1; }
     static __host__ __device__ int warp_floats(int nt) { return ((trace_len(nt) + 3) & ~3) + NCOL * CSTR; }
@@ -211,7 +211,7 @@ struct FwdMid {
 };
 
 template <int LMIN, int OMAX, int SPAN>
-__global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
+__global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
                                                             const float *__restrict__ tmpl,
                                                             const float *__restrict__ p0, float *__restrict__ out,
                                                             int mode, const float *__restrict__ meas,
@@ -342,33 +342,34 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(Geo g, FwdConst fc, 
             }
         }
 
-        // ---- flush: lane l writes C_i acc'_i into column (J - Jmin + i), row l, of the
-        // column-major buffer (zero between flushes); each lane then sums whole columns with
-        // 128-bit loads (4 independent partial sums, fixed order) into the warp trace.
+        // ---- flush, in two half-warp phases: lanes (16 ph .. 16 ph + 15) write C_i acc'_i into
+        // column (J - Jmin + i), row lane%16, of the column-major buffer (zero between uses);
+        // every lane then sums whole columns with 128-bit loads (fixed order) into the warp trace.
         const int Jmax = warp_max(J);
         if (Jmax - Jmin <= SPAN) {
-            float *w = cols + (J - Jmin) * C::CSTR + lane;
-#pragma unroll
-            for (int i = 0; i < R; ++i) w[i * C::CSTR] = acc[i] * fc.C[i];
-            __syncwarp();
             const int ncol = Jmax - Jmin + R;
-            for (int c = lane; c < ncol; c += 32) {
-                const float4 *col = reinterpret_cast<const float4 *>(cols + c * C::CSTR);
-                float4 s4 = col[0];
+            float *w = cols + (J - Jmin) * C::CSTR + (lane & 15);
 #pragma unroll
-                for (int q = 1; q < 8; ++q) {
-                    const float4 t = col[q];
-                    s4.x += t.x;
-                    s4.y += t.y;
-                    s4.z += t.z;
-                    s4.w += t.w;
+            for (int ph = 0; ph < 2; ++ph) {
+                if ((lane >> 4) == ph) {
+#pragma unroll
+                    for (int i = 0; i < R; ++i) w[i * C::CSTR] = acc[i] * fc.C[i];
                 }
-                trw[C::PADL + Jmin + c] += (s4.x + s4.y) + (s4.z + s4.w);
-            }
-            __syncwarp();
+                __syncwarp();
+                for (int c = lane; c < ncol; c += 32) {
+                    const float4 *col = reinterpret_cast<const float4 *>(cols + c * C::CSTR);
+                    const float4 t0 = col[0], t1 = col[1], t2 = col[2], t3 = col[3];
+                    const float s4 = ((t0.x + t0.y) + (t0.z + t0.w)) + ((t1.x + t1.y) + (t1.z + t1.w)) +
+                                     (((t2.x + t2.y) + (t2.z + t2.w)) + ((t3.x + t3.y) + (t3.z + t3.w)));
+                    trw[C::PADL + Jmin + c] += s4;
+                }
+                __syncwarp();
+                if ((lane >> 4) == ph) {
 #pragma unroll
-            for (int i = 0; i < R; ++i) w[i * C::CSTR] = 0.0f;
-            __syncwarp();
+                    for (int i = 0; i < R; ++i) w[i * C::CSTR] = 0.0f;
+                }
+                __syncwarp();
+            }
         } else {
             // serialized fallback (not reached for supported geometry)
             for (int l = 0; l < 32; ++l) {
