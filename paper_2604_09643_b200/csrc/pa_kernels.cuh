@@ -235,8 +235,19 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
     const int cx = lane & 3, cy = (lane >> 2) & 3, cz = lane >> 4;
     __syncwarp();
 
+    // tile coordinates advanced incrementally (tile += FWD_WARPS), no integer division
+    int tx = warp % g.ntx, ty = (warp / g.ntx) % g.nty, tz = warp / (g.ntx * g.nty);
     for (int tile = warp; tile < g.ntiles; tile += FWD_WARPS) {
-        const int tx = tile % g.ntx, ty = (tile / g.ntx) % g.nty, tz = tile / (g.ntx * g.nty);
+        if (tile != warp) {
+            tx += FWD_WARPS;
+            while (tx >= g.ntx) {
+                tx -= g.ntx;
+                if (++ty == g.nty) {
+                    ty = 0;
+                    ++tz;
+                }
+            }
+        }
         const Anc A = make_anchor(g, x, tx, ty, tz);
         if (A.cull) continue;  // warp-uniform
 
@@ -246,10 +257,17 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
         const float ey0 = ((float)(2 * cy) - 0.5f * (TY - 1)) * g.hf;
         const float ez0 = ((float)(2 * cz) - 0.5f * (TZ - 1)) * g.hf;
         float P[8];
+        {
+            const float *pb = p0 + ((size_t)bz * g.ny + by) * g.nx + bx;
+            const size_t sy = (size_t)g.nx, sz = (size_t)g.nx * g.ny;
+            const bool okx1 = bx + 1 < g.nx, oky1 = by + 1 < g.ny, okz1 = bz + 1 < g.nz;
+            const bool ok0 = bx < g.nx && by < g.ny && bz < g.nz;
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-            const int ix = bx + (v & 1), iy = by + ((v >> 1) & 1), iz = bz + (v >> 2);
-            P[v] = (ix < g.nx && iy < g.ny && iz < g.nz) ? __ldg(p0 + ((size_t)iz * g.ny + iy) * g.nx + ix) : 0.0f;
+            for (int v = 0; v < 8; ++v) {
+                const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
+                const bool ok = ok0 && (!vx || okx1) && (!vy || oky1) && (!vz || okz1);
+                P[v] = ok ? __ldg(pb + vx + vy * sy + vz * sz) : 0.0f;
+            }
         }
         // window base: jlo of the cluster voxel closest to the element (exact minimiser of |d+delta|
         // coordinate-wise); other voxels have jlo >= J (up to rounding, handled by the slow path)
@@ -344,7 +362,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
 
         // ---- flush, in two half-warp phases: lanes (16 ph .. 16 ph + 15) write C_i acc'_i into
         // column (J - Jmin + i), row lane%16, of the column-major buffer (zero between uses);
-        // every lane then sums whole columns with 128-bit loads (fixed order) into the warp trace.
+        // every lane then sums whole columns with 128-bit loads (fixed order) into the warp
+        // trace and clears the columns it consumed.
         const int Jmax = warp_max(J);
         if (Jmax - Jmin <= SPAN) {
             const int ncol = Jmax - Jmin + R;
@@ -357,16 +376,16 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
                 }
                 __syncwarp();
                 for (int c = lane; c < ncol; c += 32) {
-                    const float4 *col = reinterpret_cast<const float4 *>(cols + c * C::CSTR);
+                    float4 *col = reinterpret_cast<float4 *>(cols + c * C::CSTR);
                     const float4 t0 = col[0], t1 = col[1], t2 = col[2], t3 = col[3];
                     const float s4 = ((t0.x + t0.y) + (t0.z + t0.w)) + ((t1.x + t1.y) + (t1.z + t1.w)) +
                                      (((t2.x + t2.y) + (t2.z + t2.w)) + ((t3.x + t3.y) + (t3.z + t3.w)));
                     trw[C::PADL + Jmin + c] += s4;
-                }
-                __syncwarp();
-                if ((lane >> 4) == ph) {
-#pragma unroll
-                    for (int i = 0; i < R; ++i) w[i * C::CSTR] = 0.0f;
+                    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);  // consume-and-clear
+                    col[0] = z4;
+                    col[1] = z4;
+                    col[2] = z4;
+                    col[3] = z4;
                 }
                 __syncwarp();
             }
