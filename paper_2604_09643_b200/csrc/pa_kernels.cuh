@@ -581,63 +581,78 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                 for (int e0 = 0; e0 < E; e0 += 4) {
                     float G[4][3];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int e = e0 + q;
-                        G[q][0] = G[q][1] = G[q][2] = 0.0f;
-                        if (e >= E) continue;  // uniform
-                        const AncS s = anc[e];
-                        if (s.cull) continue;  // uniform
-                        Anc A;
-                        A.dx2 = s.dx2; A.dy2 = s.dy2; A.dz2 = s.dz2;
-                        A.dx = s.dx; A.dy = s.dy; A.dz = s.dz;
-                        A.rho = s.rho; A.rho2 = s.rho2; A.CA = s.CA; A.JA = s.JA; A.cull = 0;
-                        const Pair p = pair<LMIN>(g, A, ex, ey, ez, e2);
-                        const bool valid = inside && p.jlo <= g.nt - 1 && p.jlo + p.L - 1 >= 0;
-                        int off = p.jlo - s.jseg;
-                        off = valid ? min(max(off, 0), SEG - LMAX) : 0;
-                        const float *gs = seg + e * SEG + off;
-                        const float D0 = __fmaf_rn(-(float)(p.jlo - s.JA), g.af, __fadd_rn(p.drel, s.CA));
+                    for (int q = 0; q < 4; q += 2) {
+                        // two elements per pass, packed fp32x2 arithmetic (FFMA2/FMUL2: half the
+                        // issue slots for the same FP32-pipe work)
+                        const int ea = e0 + q, eb = e0 + q + 1;
+                        G[q][0] = G[q][1] = G[q][2] = G[q + 1][0] = G[q + 1][1] = G[q + 1][2] = 0.0f;
+                        if (ea >= E) continue;  // uniform
+                        const bool hb = eb < E;
+                        const AncS sa = anc[ea], sb = anc[hb ? eb : ea];
+                        if (sa.cull && (!hb || sb.cull)) continue;  // uniform
+                        Anc Aa, Ab;
+                        Aa.dx2 = sa.dx2; Aa.dy2 = sa.dy2; Aa.dz2 = sa.dz2; Aa.dx = sa.dx; Aa.dy = sa.dy; Aa.dz = sa.dz;
+                        Aa.rho = sa.rho; Aa.rho2 = sa.rho2; Aa.CA = sa.CA; Aa.JA = sa.JA; Aa.cull = 0;
+                        Ab.dx2 = sb.dx2; Ab.dy2 = sb.dy2; Ab.dz2 = sb.dz2; Ab.dx = sb.dx; Ab.dy = sb.dy; Ab.dz = sb.dz;
+                        Ab.rho = sb.rho; Ab.rho2 = sb.rho2; Ab.CA = sb.CA; Ab.JA = sb.JA; Ab.cull = 0;
+                        const Pair pa = pair<LMIN>(g, Aa, ex, ey, ez, e2);
+                        const Pair pb = pair<LMIN>(g, Ab, ex, ey, ez, e2);
+                        const bool va = inside && !sa.cull && pa.jlo <= g.nt - 1 && pa.jlo + pa.L - 1 >= 0;
+                        const bool vb = inside && hb && !sb.cull && pb.jlo <= g.nt - 1 && pb.jlo + pb.L - 1 >= 0;
+                        const int offa = va ? min(max(pa.jlo - sa.jseg, 0), SEG - LMAX) : 0;
+                        const int offb = vb ? min(max(pb.jlo - sb.jseg, 0), SEG - LMAX) : 0;
+                        const float *gsa = seg + ea * SEG + offa;
+                        const float *gsb = seg + (hb ? eb : ea) * SEG + offb;
                         constexpr int MA = AdjMid<LMIN>::m;
-                        const float Dm = D0 - (float)MA * g.af;  // D at the window centre step MA
+                        const float Dma = __fmaf_rn(-(float)(pa.jlo - sa.JA), g.af, __fadd_rn(pa.drel, sa.CA)) - (float)MA * g.af;
+                        const float Dmb = __fmaf_rn(-(float)(pb.jlo - sb.JA), g.af, __fadd_rn(pb.drel, sb.CA)) - (float)MA * g.af;
                         // centre-out: u_MA = E(D_m); up with p = exp(a D_m/s^2), down with 1/p
-                        const float um = ex2(-g.k2 * Dm * Dm);
-                        const float l2 = 2.0f * g.k2 * g.af * Dm;
-                        const float pu = ex2(l2), pd = ex2(-l2);
-                        float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f;  // sum g E k^n, k = i - MA
-                        float u = um;
+                        const float2 um = make_float2(ex2(-g.k2 * Dma * Dma), ex2(-g.k2 * Dmb * Dmb));
+                        const float la = 2.0f * g.k2 * g.af * Dma, lb = 2.0f * g.k2 * g.af * Dmb;
+                        const float2 pu = make_float2(ex2(la), ex2(lb)), pd = make_float2(ex2(-la), ex2(-lb));
+                        float2 S0 = make_float2(0.f, 0.f), S1 = S0, S2 = S0;  // sum g E k^n, k = i - MA
+                        float2 u = um;
 #pragma unroll
                         for (int i = MA; i < LMAX; ++i) {
-                            const float t = gs[i] * u;
-                            if (i < LMIN || i < p.L) {
-                                S0 = __fmaf_rn(t, ac.C0[i], S0);
-                                S1 = __fmaf_rn(t, ac.C1[i], S1);
-                                if (POSE) S2 = __fmaf_rn(t, ac.C2[i], S2);
+                            float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), u);
+                            if (i >= LMIN) {
+                                t.x = i < pa.L ? t.x : 0.0f;
+                                t.y = i < pb.L ? t.y : 0.0f;
                             }
-                            u *= pu;
+                            S0 = __ffma2_rn(t, make_float2(ac.C0[i], ac.C0[i]), S0);
+                            S1 = __ffma2_rn(t, make_float2(ac.C1[i], ac.C1[i]), S1);
+                            if (POSE) S2 = __ffma2_rn(t, make_float2(ac.C2[i], ac.C2[i]), S2);
+                            u = __fmul2_rn(u, pu);
                         }
-                        u = um * pd;
+                        u = __fmul2_rn(um, pd);
 #pragma unroll
                         for (int i = MA - 1; i >= 0; --i) {
-                            const float t = gs[i] * u;
-                            S0 = __fmaf_rn(t, ac.C0[i], S0);
-                            S1 = __fmaf_rn(t, ac.C1[i], S1);
-                            if (POSE) S2 = __fmaf_rn(t, ac.C2[i], S2);
-                            u *= pd;
+                            const float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), u);
+                            S0 = __ffma2_rn(t, make_float2(ac.C0[i], ac.C0[i]), S0);
+                            S1 = __ffma2_rn(t, make_float2(ac.C1[i], ac.C1[i]), S1);
+                            if (POSE) S2 = __ffma2_rn(t, make_float2(ac.C2[i], ac.C2[i]), S2);
+                            u = __fmul2_rn(u, pd);
                         }
                         // A1 = sum g D E = Dm S0 - a S1 ;  Bq = sum g E (D^2 - s^2)
-                        float A1 = __fmaf_rn(-g.af, S1, Dm * S0);
-                        float Bq = POSE ? (Dm * Dm - g.s2) * S0 - 2.0f * g.af * Dm * S1 + g.af * g.af * S2 : 0.0f;
-                        if (!valid) {
-                            A1 = 0.0f;
-                            Bq = 0.0f;
-                        }
-                        if (ADJ) z = __fmaf_rn(A1, 0.5f * p.inv_r, z);
+                        float A1a = __fmaf_rn(-g.af, S1.x, Dma * S0.x), A1b = __fmaf_rn(-g.af, S1.y, Dmb * S0.y);
+                        float Bqa = 0.0f, Bqb = 0.0f;
                         if (POSE) {
-                            const float dLdr = P * 0.5f * p.inv_r * (-Bq * g.inv_s2 - A1 * p.inv_r);
-                            const float sc = -dLdr * p.inv_r;  // x - y_k = -(d + delta)
-                            G[q][0] = sc * (s.dx + ex);
-                            G[q][1] = sc * (s.dy + ey);
-                            G[q][2] = sc * (s.dz + ez);
+                            Bqa = (Dma * Dma - g.s2) * S0.x - 2.0f * g.af * Dma * S1.x + g.af * g.af * S2.x;
+                            Bqb = (Dmb * Dmb - g.s2) * S0.y - 2.0f * g.af * Dmb * S1.y + g.af * g.af * S2.y;
+                        }
+                        if (!va) A1a = Bqa = 0.0f;
+                        if (!vb) A1b = Bqb = 0.0f;
+                        if (ADJ) z = __fmaf_rn(A1b, 0.5f * pb.inv_r, __fmaf_rn(A1a, 0.5f * pa.inv_r, z));
+                        if (POSE) {
+                            const float dLa = P * 0.5f * pa.inv_r * (-Bqa * g.inv_s2 - A1a * pa.inv_r);
+                            const float dLb = P * 0.5f * pb.inv_r * (-Bqb * g.inv_s2 - A1b * pb.inv_r);
+                            const float sca = -dLa * pa.inv_r, scb = -dLb * pb.inv_r;  // x - y_k = -(d + delta)
+                            G[q][0] = sca * (sa.dx + ex);
+                            G[q][1] = sca * (sa.dy + ey);
+                            G[q][2] = sca * (sa.dz + ez);
+                            G[q + 1][0] = scb * (sb.dx + ex);
+                            G[q + 1][1] = scb * (sb.dy + ey);
+                            G[q + 1][2] = scb * (sb.dz + ez);
                         }
                     }
                     if (POSE) {
