@@ -117,12 +117,16 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     if (pl.klass >= 0) {
         const Klass &c = kClasses[pl.klass];
         const double kc = g.ksig_d / a;  // window half-width in samples
-        g.mF = (c.lmin + c.omax) / 2;  // == FwdMid<LMIN,OMAX>::m
+        g.mF = ((c.lmin + c.omax) / 2) & ~1;  // == FwdMid<LMIN,OMAX>::m
         g.mA = (c.lmin + 1) / 2;  // == AdjMid<LMIN>::m
         const double be = a * a / (2.0 * sig * sig);
+        for (int k = 0; k < 64; ++k) {
+            const double k0 = 2 * k - g.mF, k1 = 2 * k + 1 - g.mF;
+            pl.fc.C2[k] = make_float2((float)std::exp(-k0 * k0 * be), (float)std::exp(-k1 * k1 * be));
+            pl.fc.I2[k] = make_float2((float)(-2 * k), (float)(-2 * k - 1));
+        }
         for (int i = 0; i < 128; ++i) {
-            const double kf = i - g.mF, ka = i - g.mA;
-            pl.fc.C[i] = (float)std::exp(-kf * kf * be);
+            const double ka = i - g.mA;
             const double ca = std::exp(-ka * ka * be);
             pl.ac.C0[i] = (float)ca;
             pl.ac.C1[i] = (float)(ca * ka);

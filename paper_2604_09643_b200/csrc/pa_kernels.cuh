@@ -41,7 +41,8 @@ struct Geo {
 //   exp(-D_i^2/2s^2) = u_i * C_i,  D_i = D_m - (i - m) a,  C_i = exp(-(i-m)^2 a^2 / 2s^2),
 //   u_i = u_0 p^i,  p = exp(a D_m / s^2),  u_0 = exp(-(D_m^2 + 2 m a D_m) / 2s^2).
 struct FwdConst {
-    float C[128];  // C_i about the cluster-window centre mF
+    float2 C2[64];   // (C_2k, C_2k+1) about the cluster-window centre mF
+    float2 I2[64];   // (-2k, -2k-1): step indices for packed D_i = D_J - i a
 };
 struct AdjConst {
     float C0[128];  // C_i about the pair-window centre mA
@@ -207,7 +208,7 @@ enum { FWD_TRACE = 0, FWD_MSE = 1, FWD_NC = 2 };
 // Geo::mF to the same value (checked in make_plan).
 template <int LMIN, int OMAX>
 struct FwdMid {
-    static constexpr int m = (LMIN + OMAX) / 2;
+    static constexpr int m = ((LMIN + OMAX) / 2) & ~1;  // even: packed (i, i+1) pairs stay register-pair aligned
 };
 
 template <int LMIN, int OMAX, int SPAN>
@@ -288,13 +289,22 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
         const int Jmin = warp_min(any ? J : 0x7fffffff);
         if (!any) J = Jmin;
 
-        float acc[R];
+        constexpr int R2 = (R + 1) / 2;
+        float2 acc2[R2];  // acc'_i in register pairs (i even -> .x, odd -> .y)
 #pragma unroll
-        for (int i = 0; i < R; ++i) acc[i] = 0.0f;
+        for (int k = 0; k < R2; ++k) acc2[k] = make_float2(0.0f, 0.0f);
+#define ACC(i) (((i) & 1) ? acc2[(i) >> 1].y : acc2[(i) >> 1].x)
         unsigned ovf = 0u;  // voxels with jlo outside [J, J+OMAX) (rounding corner cases)
         const float mfa = (float)g.mF * g.af;
         const float jj = -(float)(J - A.JA);
-        // two voxels per pass (ILP 2); the recurrence runs centre-out from step mF
+        const float2 af2 = make_float2(g.af, g.af);
+        // steps [OMAX-1, LMIN) are in-window for every voxel of the cluster: there the recurrence
+        // runs packed on (i, i+1) pairs (FFMA2/FMUL2); the OMAX-1 head and the tail steps are
+        // scalar and predicated.
+        constexpr int M = FwdMid<LMIN, OMAX>::m;
+        constexpr int UPE = M + 2 * ((LMIN - M) / 2);   // upward packed pairs: [M, UPE)
+        constexpr int DNE = 2 * ((OMAX - 1 + 1) / 2);   // downward packed pairs: [DNE, M)
+        // two voxels per pass (ILP 2); the recurrence runs centre-out from step M
 #pragma unroll 1
         for (int v = 0; v < 8; v += 2) {
             const int vy = (v >> 1) & 1, vz = v >> 2;
@@ -322,43 +332,73 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
             const int oLa = oa + pa.L, oLb = ob + pb.L;
             const float DJa = __fmaf_rn(jj, g.af, __fadd_rn(pa.drel, A.CA));
             const float DJb = __fmaf_rn(jj, g.af, __fadd_rn(pb.drel, A.CA));
-            const float Dma = DJa - mfa, Dmb = DJb - mfa;  // D at the centre step mF
-            // u_mF = E(D_m) (C_mF = 1); p = exp(a D_m / s^2); walk up with p, down with 1/p
+            const float Dma = DJa - mfa, Dmb = DJb - mfa;  // D at the centre step M
+            // u_M = E(D_m) (C_M = 1); p = exp(a D_m / s^2); walk up with p, down with 1/p
             const float uma = ca * ex2(-g.k2 * Dma * Dma), umb = cb * ex2(-g.k2 * Dmb * Dmb);
             const float la = 2.0f * g.k2 * g.af * Dma, lb = 2.0f * g.k2 * g.af * Dmb;
             const float pa_ = ex2(la), pb_ = ex2(lb), qa_ = ex2(-la), qb_ = ex2(-lb);
-            float ua = uma, ub = umb;
+            const float2 pa2 = make_float2(ex2(2.0f * la), 0.0f), pb2 = make_float2(ex2(2.0f * lb), 0.0f);
+            const float2 qa2 = make_float2(ex2(-2.0f * la), 0.0f), qb2 = make_float2(ex2(-2.0f * lb), 0.0f);
+            const float2 DJa2 = make_float2(DJa, DJa), DJb2 = make_float2(DJb, DJb);
+            // -- upward, packed
+            float2 ua2 = make_float2(uma, uma * pa_), ub2 = make_float2(umb, umb * pb_);
 #pragma unroll
-            for (int i = FwdMid<LMIN, OMAX>::m; i < R; ++i) {
+            for (int i = M; i < UPE; i += 2) {
+                const float2 Da = __ffma2_rn(fc.I2[i >> 1], af2, DJa2);
+                const float2 Db = __ffma2_rn(fc.I2[i >> 1], af2, DJb2);
+                acc2[i >> 1] = __ffma2_rn(ua2, Da, acc2[i >> 1]);
+                acc2[i >> 1] = __ffma2_rn(ub2, Db, acc2[i >> 1]);
+                ua2 = __fmul2_rn(ua2, make_float2(pa2.x, pa2.x));
+                ub2 = __fmul2_rn(ub2, make_float2(pb2.x, pb2.x));
+            }
+            // -- upward tail, scalar (predicated on the window end)
+            float ua = ua2.x, ub = ub2.x;
+#pragma unroll
+            for (int i = UPE; i < R; ++i) {
                 const float Da = __fmaf_rn(-(float)i, g.af, DJa);
                 const float Db = __fmaf_rn(-(float)i, g.af, DJb);
                 if (i < LMIN) {
-                    acc[i] = __fmaf_rn(ua, Da, acc[i]);
-                    acc[i] = __fmaf_rn(ub, Db, acc[i]);
+                    ACC(i) = __fmaf_rn(ua, Da, ACC(i));
+                    ACC(i) = __fmaf_rn(ub, Db, ACC(i));
                 } else {
-                    if (i < oLa) acc[i] = __fmaf_rn(ua, Da, acc[i]);
-                    if (i < oLb) acc[i] = __fmaf_rn(ub, Db, acc[i]);
+                    if (i < oLa) ACC(i) = __fmaf_rn(ua, Da, ACC(i));
+                    if (i < oLb) ACC(i) = __fmaf_rn(ub, Db, ACC(i));
                 }
                 ua *= pa_;
                 ub *= pb_;
             }
-            ua = uma * qa_;
-            ub = umb * qb_;
+            // -- downward, packed on pairs (i, i+1), i = M-2, M-4, ..., DNE
+            ua2 = make_float2(uma * qa2.x, uma * qa_);
+            ub2 = make_float2(umb * qb2.x, umb * qb_);
 #pragma unroll
-            for (int i = FwdMid<LMIN, OMAX>::m - 1; i >= 0; --i) {
+            for (int i = M - 2; i >= DNE; i -= 2) {
+                const float2 Da = __ffma2_rn(fc.I2[i >> 1], af2, DJa2);
+                const float2 Db = __ffma2_rn(fc.I2[i >> 1], af2, DJb2);
+                acc2[i >> 1] = __ffma2_rn(ua2, Da, acc2[i >> 1]);
+                acc2[i >> 1] = __ffma2_rn(ub2, Db, acc2[i >> 1]);
+                ua2 = __fmul2_rn(ua2, make_float2(qa2.x, qa2.x));
+                ub2 = __fmul2_rn(ub2, make_float2(qb2.x, qb2.x));
+            }
+            // -- downward head, scalar (predicated on the window start)
+            ua = ua2.y;
+            ub = ub2.y;
+#pragma unroll
+            for (int i = DNE - 1; i >= 0; --i) {
                 const float Da = __fmaf_rn(-(float)i, g.af, DJa);
                 const float Db = __fmaf_rn(-(float)i, g.af, DJb);
                 if (i < OMAX - 1) {
-                    if (i >= oa) acc[i] = __fmaf_rn(ua, Da, acc[i]);
-                    if (i >= ob) acc[i] = __fmaf_rn(ub, Db, acc[i]);
+                    if (i >= oa) ACC(i) = __fmaf_rn(ua, Da, ACC(i));
+                    if (i >= ob) ACC(i) = __fmaf_rn(ub, Db, ACC(i));
                 } else {
-                    acc[i] = __fmaf_rn(ua, Da, acc[i]);
-                    acc[i] = __fmaf_rn(ub, Db, acc[i]);
+                    ACC(i) = __fmaf_rn(ua, Da, ACC(i));
+                    ACC(i) = __fmaf_rn(ub, Db, ACC(i));
                 }
                 ua *= qa_;
                 ub *= qb_;
             }
         }
+#pragma unroll
+        for (int k = 0; k < R2; ++k) acc2[k] = __fmul2_rn(acc2[k], fc.C2[k]);  // acc'_i C_i -> samples
 
         // ---- flush, in two half-warp phases: lanes (16 ph .. 16 ph + 15) write C_i acc'_i into
         // column (J - Jmin + i), row lane%16, of the column-major buffer (zero between uses);
@@ -372,7 +412,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
             for (int ph = 0; ph < 2; ++ph) {
                 if ((lane >> 4) == ph) {
 #pragma unroll
-                    for (int i = 0; i < R; ++i) w[i * C::CSTR] = acc[i] * fc.C[i];
+                    for (int i = 0; i < R; ++i) w[i * C::CSTR] = ACC(i);
                 }
                 __syncwarp();
                 for (int c = lane; c < ncol; c += 32) {
@@ -394,11 +434,12 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
             for (int l = 0; l < 32; ++l) {
                 if (lane == l) {
 #pragma unroll
-                    for (int i = 0; i < R; ++i) trw[C::PADL + J + i] += acc[i] * fc.C[i];
+                    for (int i = 0; i < R; ++i) trw[C::PADL + J + i] += ACC(i);
                 }
                 __syncwarp();
             }
         }
+#undef ACC
         // ---- exact slow path for any voxel outside the register window (lane-serialised)
         const unsigned ovm = __ballot_sync(0xffffffffu, ovf != 0u);
         if (ovm) {
