@@ -124,10 +124,11 @@ pa_status pa_count(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const fl
  *   kind 0 (MSE): L = sum (y - S)^2, cot = 2 (y - S)
  *   kind 1 (NC):  per row (f,e): L_fe = -cov(y,S)/(sd_y sd_S) (population), cot = dL/dy
  *   y, S, cot [F][E][nt]; row_mask [F][E] uint8 or NULL (masked rows: zero loss and cotangent);
- *   cot may alias y.  loss (device, 1 float) = sum of row losses in fixed order.
+ *   cot may alias y.  loss (device, 1 float) = sum of row losses in fixed order;
+ *   row_loss (device [F][E] float, nullable) receives the per-row losses (NC: -correlation).
  */
 pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, const uint8_t *row_mask, int32_t F,
-                  int32_t E, int32_t nt, float *cot, float *loss, void *stream);
+                  int32_t E, int32_t nt, float *cot, float *loss, float *row_loss, void *stream);
 
 /* All-reduce callback (sum, in place, on `stream`) — lets the caller's NCCL process group
  * combine dL/dp0 across frame shards (Stage 5).  Return 0 on success.  NULL = one rank. */
@@ -153,11 +154,13 @@ typedef struct {
  *   grad_p0   [nz*ny*nx]   out (after the all-reduce), caller-owned so `ar` can name it
  *   loss      [2]          out: local loss, global loss (after `ar` on a copy)
  *   grad_euler [F][6]      out or NULL
+ *   row_loss  [F][E]       out or NULL: per-row losses of this rank's frames (before the update),
+ *                          for host-side inlier decisions (Eq. 4 mask)
  */
 pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E, int32_t F,
                   const float *meas, const uint8_t *row_mask, float *p0, float *euler_t, float *adam_p0,
                   float *adam_pose, const pa_step_cfg *cfg, pa_allreduce_fn ar, void *user, float *grad_p0,
-                  float *loss, float *grad_euler, void *stream);
+                  float *loss, float *grad_euler, float *row_loss, void *stream);
 
 /* Kernel-level timing of the last pa_step / pa_forward / pa_adjoint_pose call on this context
  * (CUDA events recorded on `stream`): ms of the forward kernel and of the adjoint+pose kernel.

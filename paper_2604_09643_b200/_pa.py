@@ -73,9 +73,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             lib.pa_pose_grad.argtypes = [vp, g, a, vp, i32, vp, i32, vp, vp, vp, vp, vp]
             lib.pa_adjoint_pose.argtypes = [vp, g, a, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp]
             lib.pa_count.argtypes = [vp, g, a, vp, i32, vp, i32, ctypes.POINTER(ctypes.c_int64), vp, vp]
-            lib.pa_loss.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, vp, vp, vp]
+            lib.pa_loss.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp]
             lib.pa_step.argtypes = [vp, g, a, vp, i32, i32, vp, vp, vp, vp, vp, vp, ctypes.POINTER(StepCfg),
-                                    ALLREDUCE_FN, vp, vp, vp, vp, vp]
+                                    ALLREDUCE_FN, vp, vp, vp, vp, vp, vp]
             lib.pa_last_kernel_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
             _lib = lib
     return _lib
@@ -214,20 +214,21 @@ class Context:
                                  _stream(stream)))
         return int(tot.value), pf[:F]
 
-    def loss(self, kind, y, S, row_mask=None, cot=None, stream=None):
+    def loss(self, kind, y, S, row_mask=None, cot=None, row_loss=False, stream=None):
         F, E, nt = y.shape
         if cot is None:
             cot = torch.empty_like(y)
         L = torch.empty(2, device=y.device, dtype=torch.float32)
+        rl = torch.empty((F, E), device=y.device, dtype=torch.float32) if row_loss else None
         m = None
         if row_mask is not None:
             m = row_mask.to(torch.uint8).contiguous()
-        _check(self.lib.pa_loss(self.h, int(kind), _f32(y), _f32(S), _ptr(m), F, E, nt, _f32(cot), _f32(L),
+        _check(self.lib.pa_loss(self.h, int(kind), _f32(y), _f32(S), _ptr(m), F, E, nt, _f32(cot), _f32(L), _ptr(rl),
                                 _stream(stream)))
-        return L[0], cot
+        return (L[0], cot, rl) if row_loss else (L[0], cot)
 
     def step(self, grid, acq, tmpl, meas, p0, euler_t, adam_p0, adam_pose, grad_p0, loss, cfg: dict, row_mask=None,
-             allreduce=None, grad_euler=None, stream=None):
+             allreduce=None, grad_euler=None, row_loss=None, stream=None):
         """One SfM iteration (pa_step).  `allreduce(tensor)` (optional) sums a CUDA tensor in place across ranks;
         it is called for grad_p0 and for the global loss slot."""
         F, E = euler_t.shape[0], tmpl.shape[0]
@@ -244,7 +245,7 @@ class Context:
         _check(self.lib.pa_step(self.h, ctypes.byref(make_grid(grid)), ctypes.byref(make_acq(acq)), _f32(tmpl), E, F,
                                 _f32(meas), _ptr(m), _f32(p0), _f32(euler_t), _f32(adam_p0), _f32(adam_pose),
                                 ctypes.byref(c), cb, None, _f32(grad_p0), _f32(loss), _ptr(grad_euler),
-                                _stream(stream)))
+                                _ptr(row_loss), _stream(stream)))
         return loss
 
     def last_kernel_ms(self):

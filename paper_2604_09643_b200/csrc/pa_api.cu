@@ -345,8 +345,11 @@ __global__ void k_adam_pose(float *__restrict__ x, float *__restrict__ m, float 
 }
 
 // Fixed-order sum of the per-row losses -> loss[0] (local) and loss[1] (pre-all-reduce copy).
-__global__ void k_rowloss_sum(const double *__restrict__ rl, long long n, float *__restrict__ loss)
+__global__ void k_rowloss_sum(const double *__restrict__ rl, long long n, float *__restrict__ loss,
+                              float *__restrict__ row_out)
 {
+    if (row_out)
+        for (long long i = threadIdx.x; i < n; i += blockDim.x) row_out[i] = (float)rl[i];
     __shared__ double red[256];
     double s = 0.0;
     const long long chunk = (n + blockDim.x - 1) / blockDim.x;
@@ -734,7 +737,7 @@ pa_status pa_count(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const fl
 }
 
 pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, const uint8_t *row_mask, int32_t F,
-                  int32_t E, int32_t nt, float *cot, float *loss, void *stream)
+                  int32_t E, int32_t nt, float *cot, float *loss, float *row_loss, void *stream)
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     if (kind != 0 && kind != 1) return fail(PA_EINVAL, "loss kind must be 0 (MSE) or 1 (NC)");
@@ -750,7 +753,8 @@ pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, con
         k_loss_rows<<<(unsigned)rows, 128, 0, st>>>(kind, y, S, row_mask, nt, cot, rl);
         CUDA_TRY(cudaGetLastError());
     }
-    k_rowloss_sum<<<1, 256, 0, st>>>(rl, rows, loss);
+    if (row_loss && !aligned4(row_loss)) return fail(PA_ESHAPE, "misaligned row_loss");
+    k_rowloss_sum<<<1, 256, 0, st>>>(rl, rows, loss, row_loss);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
@@ -758,7 +762,7 @@ pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, con
 pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E, int32_t F,
                   const float *meas, const uint8_t *row_mask, float *p0, float *euler_t, float *adam_p0,
                   float *adam_pose, const pa_step_cfg *cfg, pa_allreduce_fn ar, void *user, float *grad_p0,
-                  float *loss, float *grad_euler, void *stream)
+                  float *loss, float *grad_euler, float *row_loss, void *stream)
 {
     if (!ctx || !cfg) return fail(PA_EINVAL, "null ctx/cfg");
     Plan pl;
@@ -771,6 +775,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     if ((s = check_ptrs({tmpl, p0, adam_p0, grad_p0, loss}))) return s;
     if (F > 0 && (s = check_ptrs({meas, euler_t, adam_pose}))) return s;
     if (grad_euler && !aligned4(grad_euler)) return fail(PA_ESHAPE, "misaligned grad_euler");
+    if (row_loss && !aligned4(row_loss)) return fail(PA_ESHAPE, "misaligned row_loss");
     DevGuard dg(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
     const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
@@ -809,7 +814,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
                                 st)))
             return s;
         ctx->ev_fwd = true;
-        k_rowloss_sum<<<1, 256, 0, st>>>(rl, (long long)F * E, loss);
+        k_rowloss_sum<<<1, 256, 0, st>>>(rl, (long long)F * E, loss, row_loss);
         CUDA_TRY(cudaGetLastError());
         // a4 + a5 + a6 (records ev[1], ev[2])
         if ((s = adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, gpose, nullptr, true, st, ws, off))) return s;
