@@ -21,6 +21,9 @@
 namespace pa {
 
 constexpr int TX = 8, TY = 8, TZ = 4;  // voxel tile (anchor unit) — 256 voxels
+#ifndef PA_FWD_PHASES
+#define PA_FWD_PHASES 2
+#endif
 constexpr int FWD_WARPS = 4;           // warps per forward CTA
 constexpr int ADJ_THREADS = 256;       // one thread per tile voxel
 
@@ -196,7 +199,9 @@ template <int LMIN, int OMAX, int SPAN>
 struct FwdCfg {
     static constexpr int R = LMIN + OMAX;
     static constexpr int NCOL = R + SPAN;   // columns of the flush buffer (window + tile spread)
-    static constexpr int CSTR = 20;         // column stride (floats): 16 lanes + skew, 16-B aligned
+    static constexpr int NPH = PA_FWD_PHASES;         // flush phases (rows per phase = 32 / NPH)
+    static constexpr int ROWS = 32 / NPH;
+    static constexpr int CSTR = ROWS + 4;              // column stride (floats): rows + skew, 16-B aligned
     static constexpr int PADL = LMIN + 2;
     static __host__ __device__ int trace_len(int nt) { return PADL + nt + NCOL + 1; }
     static __host__ __device__ int warp_floats(int nt) { return ((trace_len(nt) + 3) & ~3) + NCOL * CSTR; }
@@ -212,7 +217,7 @@ struct FwdMid {
 };
 
 template <int LMIN, int OMAX, int SPAN>
-__global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
+__global__ void __launch_bounds__(FWD_WARPS * 32, PA_FWD_PHASES == 2 ? 3 : 2) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
                                                             const float *__restrict__ tmpl,
                                                             const float *__restrict__ p0, float *__restrict__ out,
                                                             int mode, const float *__restrict__ meas,
@@ -351,10 +356,13 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
                 ua2 = __fmul2_rn(ua2, make_float2(pa2.x, pa2.x));
                 ub2 = __fmul2_rn(ub2, make_float2(pb2.x, pb2.x));
             }
-            // -- upward tail, scalar (predicated on the window end)
+            // -- upward tail, scalar (predicated on the window end); steps past every lane's
+            // window end are skipped with a warp-uniform exit
+            const int tail_end = (int)__reduce_max_sync(0xffffffffu, (unsigned)max(oLa, oLb));
             float ua = ua2.x, ub = ub2.x;
 #pragma unroll
             for (int i = UPE; i < R; ++i) {
+                if (i >= tail_end) break;
                 const float Da = __fmaf_rn(-(float)i, g.af, DJa);
                 const float Db = __fmaf_rn(-(float)i, g.af, DJb);
                 if (i < LMIN) {
@@ -379,11 +387,14 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
                 ua2 = __fmul2_rn(ua2, make_float2(qa2.x, qa2.x));
                 ub2 = __fmul2_rn(ub2, make_float2(qb2.x, qb2.x));
             }
-            // -- downward head, scalar (predicated on the window start)
+            // -- downward head, scalar (predicated on the window start); steps before every
+            // lane's window start are skipped with a warp-uniform exit
+            const int head_beg = (int)__reduce_min_sync(0xffffffffu, (unsigned)min(oa, ob));
             ua = ua2.y;
             ub = ub2.y;
 #pragma unroll
             for (int i = DNE - 1; i >= 0; --i) {
+                if (i < head_beg) break;
                 const float Da = __fmaf_rn(-(float)i, g.af, DJa);
                 const float Db = __fmaf_rn(-(float)i, g.af, DJb);
                 if (i < OMAX - 1) {
@@ -407,25 +418,29 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_forward(Geo g, FwdConst f
         const int Jmax = warp_max(J);
         if (Jmax - Jmin <= SPAN) {
             const int ncol = Jmax - Jmin + R;
-            float *w = cols + (J - Jmin) * C::CSTR + (lane & 15);
+            float *w = cols + (J - Jmin) * C::CSTR + (lane % C::ROWS);
 #pragma unroll
-            for (int ph = 0; ph < 2; ++ph) {
-                if ((lane >> 4) == ph) {
+            for (int ph = 0; ph < C::NPH; ++ph) {
+                if (lane / C::ROWS == ph) {
 #pragma unroll
                     for (int i = 0; i < R; ++i) w[i * C::CSTR] = ACC(i);
                 }
                 __syncwarp();
                 for (int c = lane; c < ncol; c += 32) {
                     float4 *col = reinterpret_cast<float4 *>(cols + c * C::CSTR);
-                    const float4 t0 = col[0], t1 = col[1], t2 = col[2], t3 = col[3];
-                    const float s4 = ((t0.x + t0.y) + (t0.z + t0.w)) + ((t1.x + t1.y) + (t1.z + t1.w)) +
-                                     (((t2.x + t2.y) + (t2.z + t2.w)) + ((t3.x + t3.y) + (t3.z + t3.w)));
-                    trw[C::PADL + Jmin + c] += s4;
+                    float4 a = col[0];
+#pragma unroll
+                    for (int q = 1; q < C::ROWS / 4; ++q) {
+                        const float4 t = col[q];
+                        a.x += t.x;
+                        a.y += t.y;
+                        a.z += t.z;
+                        a.w += t.w;
+                    }
+                    trw[C::PADL + Jmin + c] += (a.x + a.y) + (a.z + a.w);
                     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);  // consume-and-clear
-                    col[0] = z4;
-                    col[1] = z4;
-                    col[2] = z4;
-                    col[3] = z4;
+#pragma unroll
+                    for (int q = 0; q < C::ROWS / 4; ++q) col[q] = z4;
                 }
                 __syncwarp();
             }
