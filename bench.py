@@ -335,8 +335,9 @@ def main():
                 "frac_at_measured_clock": (dom["achieved"] * 1e12 / (N_SM * LANES * f_meas)) if (dom["achieved"] and f_meas) else None,
                 "other_kernel": other,
                 "step_frac": (U_local_max * (OPS_FWD + OPS_ADJ) / (ms / 1e3) / 1e12) / peak if ms > 0 else None,
-                "traffic_note": "dram bytes per launch from ncu --set full at C2 (profiles/r1_ncu_c2_*.md): "
-                                "K2 63.4 MB read + 24.1 MB written ~= algorithmic (cotangent + p0 + gradient)"}
+                "traffic_note": "DRAM bytes per launch from ncu --set full on the C4 geometry with 16 frames "
+                                "(profiles/r1_ncu_c4_k_*.md): k_adjoint 89 MB read + 42 MB written, k_forward 257 MB "
+                                "read + 22 MB written; both are ALU-bound (>= 5e4 updates per DRAM byte)"}
     cpu = None
     if world == 1 and not args.no_cpu:
         v, cores, sample = cpu_oracle_sample(w, p_true.astype(np.float64), w.poses_true())
