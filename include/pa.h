@@ -140,7 +140,20 @@ typedef struct {
     int32_t step;                   /* Adam step t >= 1 (bias correction)                         */
     int32_t loss_kind;              /* 0 MSE (Eq. 2), 1 NC (Eq. 3/4)                              */
     int32_t update_p0, update_pose; /* apply the p0 / pose updates                                */
+    float tgv_lambda;               /* Eq. 2 weight of the TGV^2 term (0 = off; R20)        */
+    float tgv_alpha1, tgv_alpha0;   /* TGV^2 first / second order weights (R20)        */
+    float tgv_eps;                  /* smoothing of the norms, phi(v) = sqrt(|v|^2+eps^2) - eps   */
 } pa_step_cfg;
+
+/*
+ * Eq. 2 regulariser, TGV^2 reading R20: with forward differences and
+ * O = {x : x_d <= n_d - 2},
+ *   L = alpha1 sum_O phi(grad P - w) + alpha0 sum_O phi(E w),  E w = (grad w + grad w^T)/2
+ *   P [nz][ny][nx], w [3][nz][ny][nx] (components x, y, z); value (device, 1 float);
+ *   grad_P, grad_w outputs (overwritten).  HBM-bound stencil, deterministic.
+ */
+pa_status pa_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const float *w, float alpha1, float alpha0,
+                 float eps, float *value, float *grad_P, float *grad_w, void *stream);
 
 /*
  * One SfM iteration over this rank's F frames (Alg. 1 Stages 1/4/5 objective):
@@ -156,11 +169,15 @@ typedef struct {
  *   grad_euler [F][6]      out or NULL
  *   row_loss  [F][E]       out or NULL: per-row losses of this rank's frames (before the update),
  *                          for host-side inlier decisions (Eq. 4 mask)
+ *   tgv_w     [3][nvox]    TGV auxiliary field, in/out (Adam with lr_p0); NULL iff tgv_lambda == 0
+ *   adam_w    [2][3][nvox] its Adam state; NULL iff tgv_lambda == 0
+ *   With tgv_lambda > 0, grad_p0 on return includes lambda * dTGV/dP (added after the
+ *   all-reduce, identically on every rank) and loss[1] includes lambda * TGV.
  */
 pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E, int32_t F,
                   const float *meas, const uint8_t *row_mask, float *p0, float *euler_t, float *adam_p0,
                   float *adam_pose, const pa_step_cfg *cfg, pa_allreduce_fn ar, void *user, float *grad_p0,
-                  float *loss, float *grad_euler, float *row_loss, void *stream);
+                  float *loss, float *grad_euler, float *row_loss, float *tgv_w, float *adam_w, void *stream);
 
 /* Kernel-level timing of the last pa_step / pa_forward / pa_adjoint_pose call on this context
  * (CUDA events recorded on `stream`): ms of the forward kernel and of the adjoint+pose kernel.

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("PA_LIB_PATH", os.path.join(_HERE, "libpa.so"))
 PA_OK, PA_EINVAL, PA_ESHAPE, PA_EDEGENERATE, PA_ECUDA, PA_ENOMEM, PA_EUNSUPPORTED = range(7)
 _NAMES = {1: "PA_EINVAL", 2: "PA_ESHAPE", 3: "PA_EDEGENERATE", 4: "PA_ECUDA", 5: "PA_ENOMEM", 6: "PA_EUNSUPPORTED"}
 EXPORTS = ("pa_create", "pa_destroy", "pa_last_error", "pa_version", "pa_forward", "pa_adjoint", "pa_pose_grad",
-           "pa_adjoint_pose", "pa_count", "pa_loss", "pa_step", "pa_last_kernel_ms")
+           "pa_adjoint_pose", "pa_count", "pa_loss", "pa_tgv", "pa_step", "pa_last_kernel_ms")
 
 
 class PAError(RuntimeError):
@@ -41,7 +41,8 @@ class StepCfg(ctypes.Structure):
     _fields_ = [("lr_p0", ctypes.c_float), ("lr_rot", ctypes.c_float), ("lr_trans", ctypes.c_float),
                 ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
                 ("step", ctypes.c_int32), ("loss_kind", ctypes.c_int32), ("update_p0", ctypes.c_int32),
-                ("update_pose", ctypes.c_int32)]
+                ("update_pose", ctypes.c_int32), ("tgv_lambda", ctypes.c_float), ("tgv_alpha1", ctypes.c_float),
+                ("tgv_alpha0", ctypes.c_float), ("tgv_eps", ctypes.c_float)]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -75,7 +76,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             lib.pa_count.argtypes = [vp, g, a, vp, i32, vp, i32, ctypes.POINTER(ctypes.c_int64), vp, vp]
             lib.pa_loss.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp]
             lib.pa_step.argtypes = [vp, g, a, vp, i32, i32, vp, vp, vp, vp, vp, vp, ctypes.POINTER(StepCfg),
-                                    ALLREDUCE_FN, vp, vp, vp, vp, vp, vp]
+                                    ALLREDUCE_FN, vp, vp, vp, vp, vp, vp, vp, vp]
+            lib.pa_tgv.argtypes = [vp, g, vp, vp, ctypes.c_float, ctypes.c_float, ctypes.c_float, vp, vp, vp, vp]
             lib.pa_last_kernel_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
             _lib = lib
     return _lib
@@ -227,8 +229,17 @@ class Context:
                                 _stream(stream)))
         return (L[0], cot, rl) if row_loss else (L[0], cot)
 
+    def tgv(self, grid, P, w, alpha1=1.0, alpha0=2.0, eps=1e-6, stream=None):
+        """TGV^2 value and gradients (pa_tgv): returns (value tensor[1], grad_P, grad_w)."""
+        val = torch.empty(1, device=P.device, dtype=torch.float32)
+        gP = torch.empty_like(P)
+        gw = torch.empty_like(w)
+        _check(self.lib.pa_tgv(self.h, ctypes.byref(make_grid(grid)), _f32(P), _f32(w), float(alpha1), float(alpha0),
+                               float(eps), _f32(val), _f32(gP), _f32(gw), _stream(stream)))
+        return val, gP, gw
+
     def step(self, grid, acq, tmpl, meas, p0, euler_t, adam_p0, adam_pose, grad_p0, loss, cfg: dict, row_mask=None,
-             allreduce=None, grad_euler=None, row_loss=None, stream=None):
+             allreduce=None, grad_euler=None, row_loss=None, tgv_w=None, adam_w=None, stream=None):
         """One SfM iteration (pa_step).  `allreduce(tensor)` (optional) sums a CUDA tensor in place across ranks;
         it is called for grad_p0 and for the global loss slot."""
         F, E = euler_t.shape[0], tmpl.shape[0]
@@ -238,6 +249,9 @@ class Context:
         c.step = int(cfg["step"])
         c.loss_kind = int(cfg.get("loss_kind", 0))
         c.update_p0, c.update_pose = int(cfg.get("update_p0", 1)), int(cfg.get("update_pose", 1))
+        c.tgv_lambda = float(cfg.get("tgv_lambda", 0.0))
+        c.tgv_alpha1, c.tgv_alpha0 = float(cfg.get("tgv_alpha1", 1.0)), float(cfg.get("tgv_alpha0", 2.0))
+        c.tgv_eps = float(cfg.get("tgv_eps", 1e-6))
         cb = ALLREDUCE_FN(0)
         if allreduce is not None:
             cb = make_allreduce_callback([grad_p0.view(-1), loss[1:2]], allreduce)
@@ -245,7 +259,7 @@ class Context:
         _check(self.lib.pa_step(self.h, ctypes.byref(make_grid(grid)), ctypes.byref(make_acq(acq)), _f32(tmpl), E, F,
                                 _f32(meas), _ptr(m), _f32(p0), _f32(euler_t), _f32(adam_p0), _f32(adam_pose),
                                 ctypes.byref(c), cb, None, _f32(grad_p0), _f32(loss), _ptr(grad_euler),
-                                _ptr(row_loss), _stream(stream)))
+                                _ptr(row_loss), _ptr(tgv_w), _ptr(adam_w), _stream(stream)))
         return loss
 
     def last_kernel_ms(self):

@@ -367,6 +367,31 @@ __global__ void k_rowloss_sum(const double *__restrict__ rl, long long n, float 
     }
 }
 
+// Fixed-order sum of per-block partials: out[0] = scale * sum (+ out[0] if accumulate).
+__global__ void k_sum_parts(const double *__restrict__ part, long long n, float scale, int accumulate,
+                            float *__restrict__ out)
+{
+    __shared__ double red[256];
+    double s = 0.0;
+    const long long chunk = (n + blockDim.x - 1) / blockDim.x;
+    const long long b = threadIdx.x * chunk, e = min(n, b + chunk);
+    for (long long i = b; i < e; ++i) s += part[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = (accumulate ? out[0] : 0.0f) + scale * (float)red[0];
+}
+
+// y += a x (elementwise)
+__global__ void k_axpy(float *__restrict__ y, const float *__restrict__ x, float a, long long n)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] += a * x[i];
+}
+
 // Standalone a3 (pa_loss): one CTA per row.
 __global__ void k_loss_rows(int kind, const float *__restrict__ y, const float *__restrict__ S,
                             const uint8_t *__restrict__ mask, int nt, float *__restrict__ cot,
@@ -583,6 +608,31 @@ pa_status adjoint_pose_core(pa_ctx *ctx, const Plan &pl, const float *tmpl, cons
     return PA_OK;
 }
 
+pa_status launch_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const float *w, float a1, float a0, float eps,
+                     float *gP, float *gw, double *part, float *value, float scale, int accumulate, cudaStream_t st)
+{
+    TgvArgs t;
+    t.nx = grid->nx;
+    t.ny = grid->ny;
+    t.nz = grid->nz;
+    t.inv_h = 1.0f / grid->pitch;
+    t.a1 = a1;
+    t.a0 = a0;
+    t.eps = eps;
+    dim3 gd((t.nx + TGV_BX - 1) / TGV_BX, (t.ny + TGV_BY - 1) / TGV_BY, (t.nz + TGV_ZS - 1) / TGV_ZS);
+    k_tgv<<<gd, TGV_BX * TGV_BY, 0, st>>>(t, P, w, gP, gw, part);
+    CUDA_TRY(cudaGetLastError());
+    k_sum_parts<<<1, 256, 0, st>>>(part, (long long)gd.x * gd.y * gd.z, scale, accumulate, value);
+    CUDA_TRY(cudaGetLastError());
+    (void)ctx;
+    return PA_OK;
+}
+
+inline size_t tgv_parts(const pa_grid *g)
+{
+    return (size_t)((g->nx + TGV_BX - 1) / TGV_BX) * ((g->ny + TGV_BY - 1) / TGV_BY) * ((g->nz + TGV_ZS - 1) / TGV_ZS);
+}
+
 }  // namespace
 
 // ============================================================================ C ABI
@@ -759,10 +809,26 @@ pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, con
     return PA_OK;
 }
 
+pa_status pa_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const float *w, float alpha1, float alpha0, float eps,
+                 float *value, float *grad_P, float *grad_w, void *stream)
+{
+    if (!ctx || !grid) return fail(PA_EINVAL, "null ctx/grid");
+    if (grid->nx <= 0 || grid->ny <= 0 || grid->nz <= 0 || !(grid->pitch > 0.f))
+        return fail(PA_EINVAL, "grid dims and pitch must be positive");
+    if (!(alpha1 >= 0.f) || !(alpha0 >= 0.f) || !(eps > 0.f)) return fail(PA_EINVAL, "need alpha >= 0, eps > 0");
+    pa_status s;
+    if ((s = check_ptrs({P, w, value, grad_P, grad_w}))) return s;
+    DevGuard dg(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((s = ws_reserve(ctx, tgv_parts(grid) * sizeof(double)))) return s;
+    return launch_tgv(ctx, grid, P, w, alpha1, alpha0, eps, grad_P, grad_w, static_cast<double *>(ctx->ws), value, 1.0f,
+                      0, st);
+}
+
 pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E, int32_t F,
                   const float *meas, const uint8_t *row_mask, float *p0, float *euler_t, float *adam_p0,
                   float *adam_pose, const pa_step_cfg *cfg, pa_allreduce_fn ar, void *user, float *grad_p0,
-                  float *loss, float *grad_euler, float *row_loss, void *stream)
+                  float *loss, float *grad_euler, float *row_loss, float *tgv_w, float *adam_w, void *stream)
 {
     if (!ctx || !cfg) return fail(PA_EINVAL, "null ctx/cfg");
     Plan pl;
@@ -776,6 +842,12 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     if (F > 0 && (s = check_ptrs({meas, euler_t, adam_pose}))) return s;
     if (grad_euler && !aligned4(grad_euler)) return fail(PA_ESHAPE, "misaligned grad_euler");
     if (row_loss && !aligned4(row_loss)) return fail(PA_ESHAPE, "misaligned row_loss");
+    const bool use_tgv = cfg->tgv_lambda != 0.0f;
+    if (use_tgv) {
+        if (!(cfg->tgv_lambda > 0.f) || !(cfg->tgv_alpha1 >= 0.f) || !(cfg->tgv_alpha0 >= 0.f) || !(cfg->tgv_eps > 0.f))
+            return fail(PA_EINVAL, "bad TGV parameters");
+        if ((s = check_ptrs({tgv_w, adam_w}))) return s;
+    }
     DevGuard dg(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
     const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
@@ -789,6 +861,8 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     const size_t o_rl = off; off += align256(sizeof(double) * (size_t)(F > 0 ? F * E : 1));
     const size_t o_gp = off; off += align256(sizeof(float) * 12 * (size_t)(F > 0 ? F : 1));
     const size_t o_ge = off; off += align256(sizeof(float) * 6 * (size_t)(F > 0 ? F : 1));
+    const size_t o_tg = off; off += use_tgv ? align256(sizeof(float) * 4 * (size_t)nvox) : 0;
+    const size_t o_tp = off; off += use_tgv ? align256(sizeof(double) * tgv_parts(grid)) : 0;
     // reserve enough for the core as well (partials + grad_elem)
     AdjLaunch L;
     if (F > 0 && (s = launch_adjoint<true, true>(ctx, pl, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, true, st)))
@@ -803,6 +877,9 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     double *rl = reinterpret_cast<double *>(ws + o_rl);
     float *gpose = reinterpret_cast<float *>(ws + o_gp);
     float *geul = grad_euler ? grad_euler : reinterpret_cast<float *>(ws + o_ge);
+    float *tg_p = use_tgv ? reinterpret_cast<float *>(ws + o_tg) : nullptr;
+    float *tg_w = use_tgv ? tg_p + nvox : nullptr;
+    double *tg_parts = use_tgv ? reinterpret_cast<double *>(ws + o_tp) : nullptr;
 
     if (F > 0) {
         k_euler_pose<<<(F + 127) / 128, 128, 0, st>>>(euler_t, F, poses, dR);
@@ -829,12 +906,28 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
         if (ar(grad_p0, (size_t)nvox, stream, user) != 0) return fail(PA_ECUDA, "all-reduce callback failed (grad_p0)");
         if (ar(loss + 1, 1, stream, user) != 0) return fail(PA_ECUDA, "all-reduce callback failed (loss)");
     }
+    // Eq. 2 regulariser (f4): replicated on every rank after the data all-reduce, so every rank
+    // applies the identical update; loss[1] += lambda * TGV
+    if (use_tgv) {
+        if ((s = launch_tgv(ctx, grid, p0, tgv_w, cfg->tgv_alpha1, cfg->tgv_alpha0, cfg->tgv_eps, tg_p, tg_w, tg_parts,
+                            loss + 1, cfg->tgv_lambda, 1, st)))
+            return s;
+        k_axpy<<<ctx->nsm * 8, 256, 0, st>>>(grad_p0, tg_p, cfg->tgv_lambda, nvox);
+        CUDA_TRY(cudaGetLastError());
+    }
     // a8: Adam
     const double bc1 = 1.0 - std::pow((double)cfg->beta1, cfg->step), bc2 = 1.0 - std::pow((double)cfg->beta2, cfg->step);
     if (cfg->update_p0) {
         int blocks = ctx->nsm * 8;
         k_adam<<<blocks, 256, 0, st>>>(p0, adam_p0, adam_p0 + nvox, grad_p0, nvox, cfg->lr_p0, cfg->beta1, cfg->beta2,
                                       cfg->eps, (float)bc1, (float)bc2, 1);
+        CUDA_TRY(cudaGetLastError());
+    }
+    if (use_tgv && cfg->update_p0) {  // Adam on the TGV auxiliary field w with lambda * dTGV/dw
+        int blocks = ctx->nsm * 8;
+        k_axpy<<<blocks, 256, 0, st>>>(tg_w, tg_w, cfg->tgv_lambda - 1.0f, 3 * nvox);  // tg_w *= lambda
+        k_adam<<<blocks, 256, 0, st>>>(tgv_w, adam_w, adam_w + 3 * nvox, tg_w, 3 * nvox, cfg->lr_p0, cfg->beta1,
+                                       cfg->beta2, cfg->eps, (float)bc1, (float)bc2, 0);
         CUDA_TRY(cudaGetLastError());
     }
     if (cfg->update_pose && F > 0) {

@@ -764,3 +764,152 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
 }
 
 }  // namespace pa
+
+namespace pa {
+
+// ============================================================================================
+// K7 — TGV^2 regulariser of Eq. 2 (reading R20): value and gradients
+//   L = a1 sum_O phi(grad P - w) + a0 sum_O phi(E w),  phi(v) = sqrt(|v|^2 + eps^2) - eps,
+//   forward differences, O = {x : x_d <= n_d - 2}.
+// One thread per voxel x; the gradient is a gather: the dphi fields n(y) = g/|g|_eps and
+// m(y) = Ew/|Ew|_eps are recomputed at y in {x, x - e_x, x - e_y, x - e_z} from cached P, w
+// (no workspace, one pass, HBM traffic ~ 32 B per voxel).  The value is reduced per block in
+// fp64 (fixed order) into `part`, summed by k_sum_parts.
+// ============================================================================================
+struct TgvArgs {
+    int nx, ny, nz;
+    float inv_h, a1, a0, eps;
+};
+
+__device__ __forceinline__ bool tgv_in(const TgvArgs &t, int x, int y, int z)
+{
+    return x >= 0 && y >= 0 && z >= 0 && x <= t.nx - 2 && y <= t.ny - 2 && z <= t.nz - 2;
+}
+
+// n(y) and m(y) (6 unique: xx, yy, zz, xy, xz, yz) at an interior point y; also |g|_eps, |Ew|_eps
+__device__ __forceinline__ void tgv_fields(const TgvArgs &t, const float *__restrict__ P, const float *__restrict__ w,
+                                           int x, int y, int z, float n[3], float m[6], float &ng, float &ne)
+{
+    const size_t sy = (size_t)t.nx, sz = (size_t)t.nx * t.ny, nv = sz * t.nz;
+    const size_t k = (size_t)z * sz + (size_t)y * sy + x;
+    const size_t off[3] = {1, sy, sz};
+    const float p = __ldg(P + k);
+    float wv[3], D[3][3];  // D[a][b] = d_a w_b
+#pragma unroll
+    for (int b = 0; b < 3; ++b) wv[b] = __ldg(w + b * nv + k);
+    float g[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        g[a] = (__ldg(P + k + off[a]) - p) * t.inv_h - wv[a];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) D[a][b] = (__ldg(w + b * nv + k + off[a]) - wv[b]) * t.inv_h;
+    }
+    ng = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + t.eps * t.eps);
+    const float ig = 1.0f / ng;
+    n[0] = g[0] * ig;
+    n[1] = g[1] * ig;
+    n[2] = g[2] * ig;
+    const float exx = D[0][0], eyy = D[1][1], ezz = D[2][2];
+    const float exy = 0.5f * (D[0][1] + D[1][0]), exz = 0.5f * (D[0][2] + D[2][0]), eyz = 0.5f * (D[1][2] + D[2][1]);
+    ne = sqrtf(exx * exx + eyy * eyy + ezz * ezz + 2.0f * (exy * exy + exz * exz + eyz * eyz) + t.eps * t.eps);
+    const float ie = 1.0f / ne;
+    m[0] = exx * ie;
+    m[1] = eyy * ie;
+    m[2] = ezz * ie;
+    m[3] = exy * ie;
+    m[4] = exz * ie;
+    m[5] = eyz * ie;
+}
+
+__device__ __forceinline__ float msym(const float m[6], int a, int b)
+{
+    if (a == b) return m[a];
+    const int s = a + b;  // (0,1)->1 xy, (0,2)->2 xz, (1,2)->3 yz
+    return s == 1 ? m[3] : (s == 2 ? m[4] : m[5]);
+}
+
+// 2.5-D streaming version: a CTA owns a 32 x 8 column of (x, y) and walks z through a slab;
+// the dphi fields (n: 3, m: 6) of each point are computed ONCE into a shared-memory plane
+// (with the x-1 / y-1 halo), the previous plane is kept, and the gradient of plane z is a
+// gather from planes z and z-1.
+constexpr int TGV_BX = 32, TGV_BY = 8, TGV_ZS = 32;
+
+__global__ void __launch_bounds__(TGV_BX *TGV_BY) k_tgv(TgvArgs t, const float *__restrict__ P,
+                                                        const float *__restrict__ w, float *__restrict__ gP,
+                                                        float *__restrict__ gw, double *__restrict__ part)
+{
+    constexpr int PX = TGV_BX + 1, PY = TGV_BY + 1, NF = 9;
+    __shared__ float fld[2][NF][PY][PX];  // plane buffers: n0..2, m0..5 at (x - 1 .. x + 31, y - 1 .. y + 7)
+    const int tx = threadIdx.x % TGV_BX, ty = threadIdx.x / TGV_BX;
+    const int x0 = blockIdx.x * TGV_BX, y0 = blockIdx.y * TGV_BY, z0 = blockIdx.z * TGV_ZS;
+    const int x = x0 + tx, y = y0 + ty;
+    const size_t sz = (size_t)t.nx * t.ny, nv = sz * t.nz;
+    double val = 0.0;
+    auto fill = [&](int buf, int z) {
+        // points (x0 - 1 + i, y0 - 1 + j), i < PX, j < PY: PX*PY = 297 points over 256 threads
+        for (int q = threadIdx.x; q < PX * PY; q += TGV_BX * TGV_BY) {
+            const int i = q % PX, j = q / PX;
+            const int xx = x0 - 1 + i, yy = y0 - 1 + j;
+            float n[3] = {0.f, 0.f, 0.f}, m[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (tgv_in(t, xx, yy, z)) {
+                float ng, ne;
+                tgv_fields(t, P, w, xx, yy, z, n, m, ng, ne);
+                // the value is counted once, by the owner of the interior point (i, j >= 1)
+                if (i >= 1 && j >= 1) val += (double)t.a1 * (ng - t.eps) + (double)t.a0 * (ne - t.eps);
+            }
+#pragma unroll
+            for (int f = 0; f < 3; ++f) fld[buf][f][j][i] = n[f];
+#pragma unroll
+            for (int f = 0; f < 6; ++f) fld[buf][3 + f][j][i] = m[f];
+        }
+    };
+    const int zend = min(z0 + TGV_ZS, t.nz);
+    fill(0, z0 - 1);  // plane below the slab (zero fields if outside O)
+    int cur = 1;
+    for (int z = z0; z < zend; ++z) {
+        fill(cur, z);
+        __syncthreads();
+        if (x < t.nx && y < t.ny) {
+            const int i = tx + 1, j = ty + 1, prv = cur ^ 1;
+            const float *n0 = &fld[cur][0][j][i];
+            float gpv = 0.0f, gwv[3];
+            float m0[6], mx[6], my[6], mz[6];
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                m0[f] = fld[cur][3 + f][j][i];
+                mx[f] = fld[cur][3 + f][j][i - 1];
+                my[f] = fld[cur][3 + f][j - 1][i];
+                mz[f] = fld[prv][3 + f][j][i];
+            }
+            const float nxm = fld[cur][0][j][i - 1], nym = fld[cur][1][j - 1][i], nzm = fld[prv][2][j][i];
+            const float n00 = fld[cur][0][j][i], n01 = fld[cur][1][j][i], n02 = fld[cur][2][j][i];
+            (void)n0;
+            gpv = t.a1 * t.inv_h * ((nxm - n00) + (nym - n01) + (nzm - n02));
+            const float nn[3] = {n00, n01, n02};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                float s = 0.0f;
+                s += msym(mx, 0, d) - msym(m0, 0, d);
+                s += msym(my, 1, d) - msym(m0, 1, d);
+                s += msym(mz, 2, d) - msym(m0, 2, d);
+                gwv[d] = -t.a1 * nn[d] + t.a0 * t.inv_h * s;
+            }
+            const size_t k = (size_t)z * sz + (size_t)y * t.nx + x;
+            gP[k] = gpv;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) gw[d * nv + k] = gwv[d];
+        }
+        __syncthreads();
+        cur ^= 1;
+    }
+    __shared__ double red[TGV_BX * TGV_BY];
+    red[threadIdx.x] = val;
+    __syncthreads();
+    for (int s2 = TGV_BX * TGV_BY / 2; s2 > 0; s2 >>= 1) {
+        if (threadIdx.x < s2) red[threadIdx.x] += red[threadIdx.x + s2];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = red[0];
+}
+
+}  // namespace pa
