@@ -626,12 +626,19 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                     anc[e] = s;
                 }
                 __syncthreads();
+                // stage the E cotangent segments with asynchronous global->shared copies (LDGSTS,
+                // zero-filled outside [0, nt) and for culled elements): all loads in flight at once
                 const float *cf = cot + (size_t)f * E * g.nt;
                 for (int q = tid; q < E * SEG; q += ADJ_THREADS) {
                     const int e = q / SEG, i = q - e * SEG;
                     const int j = anc[e].jseg + i;
-                    seg[q] = (!anc[e].cull && j >= 0 && j < g.nt) ? __ldg(cf + (size_t)e * g.nt + j) : 0.0f;
+                    const bool ok = !anc[e].cull && j >= 0 && j < g.nt;
+                    const float *src = ok ? cf + (size_t)e * g.nt + j : cf;
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(seg + q);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src),
+                                 "r"(ok ? 4 : 0));
                 }
+                asm volatile("cp.async.wait_all;\n" ::);
                 __syncthreads();
 #pragma unroll 1
                 for (int e0 = 0; e0 < E; e0 += 4) {
