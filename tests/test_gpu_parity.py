@@ -305,13 +305,14 @@ def test_empty_and_far(ctx):
 
 
 # ------------------------------------------------------------------------------------ full-size sampled parity
-@pytest.mark.parametrize("name", ["c2", "c4"])
-def test_full_size_sampled_parity(ctx, name, record_parity):
+@pytest.mark.parametrize("name,frames", [("c2", None), ("c4", None), ("c5", 100)])
+def test_full_size_sampled_parity(ctx, name, frames, record_parity):
     """At the full BASELINE size and in the launch configuration bench.py times (all frames, all
     elements, full grid), compare sampled outputs the oracle can compute one by one:
     trace rows (f, e), adjoint voxels (via 1-voxel oracle grids at the exact fp64 centre),
-    and element-gradient rows."""
-    w = gen.workload(name)
+    and element-gradient rows.  C5 (512x512x256 @ 0.1 mm, 256-element bowl, sigma = 0.1) runs
+    its full grid, array and record length on 100 of its 800 frames (one GPU's shard at 8 GPUs)."""
+    w = gen.workload(name, frames=frames)
     grid, acq = grid32(w.grid), acq32(w.acq)
     p0 = gen.phantom(w).astype(np.float32)
     poses = w.poses_true()
