@@ -24,6 +24,9 @@ constexpr int TX = 8, TY = 8, TZ = 4;  // voxel tile (anchor unit) — 256 voxel
 #ifndef PA_FWD_PHASES
 #define PA_FWD_PHASES 2
 #endif
+#ifndef PA_FWD_NV
+#define PA_FWD_NV 4
+#endif
 constexpr int FWD_WARPS = 4;           // warps per forward CTA
 constexpr int ADJ_THREADS = 256;       // one thread per tile voxel
 
@@ -217,7 +220,7 @@ struct FwdMid {
 };
 
 template <int LMIN, int OMAX, int SPAN>
-__global__ void __launch_bounds__(FWD_WARPS * 32, PA_FWD_PHASES == 2 ? 3 : 2) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
+__global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <= 64) ? 3 : 2) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
                                                             const float *__restrict__ tmpl,
                                                             const float *__restrict__ p0, float *__restrict__ out,
                                                             int mode, const float *__restrict__ meas,
@@ -309,103 +312,102 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, PA_FWD_PHASES == 2 ? 3 : 2) k_
         constexpr int M = FwdMid<LMIN, OMAX>::m;
         constexpr int UPE = M + 2 * ((LMIN - M) / 2);   // upward packed pairs: [M, UPE)
         constexpr int DNE = 2 * ((OMAX - 1 + 1) / 2);   // downward packed pairs: [DNE, M)
-        // two voxels per pass (ILP 2); the recurrence runs centre-out from step M
+        // NV voxels per pass (independent recurrence chains, ILP NV); the recurrence runs
+        // centre-out from step M
+        constexpr int NV = PA_FWD_NV;
 #pragma unroll 1
-        for (int v = 0; v < 8; v += 2) {
-            const int vy = (v >> 1) & 1, vz = v >> 2;
-            const float ey = ((float)(2 * cy + vy) - 0.5f * (TY - 1)) * g.hf;
-            const float ez = ((float)(2 * cz + vz) - 0.5f * (TZ - 1)) * g.hf;
-            const float exa = ex0, exb = ex0 + g.hf;
-            const float eyz2 = __fmaf_rn(ey, ey, __fmul_rn(ez, ez));
-            const Pair pa = pair<LMIN>(g, A, exa, ey, ez, __fmaf_rn(exa, exa, eyz2));
-            const Pair pb = pair<LMIN>(g, A, exb, ey, ez, __fmaf_rn(exb, exb, eyz2));
-            const bool ina = bx < g.nx && by + vy < g.ny && bz + vz < g.nz;
-            const bool inb = bx + 1 < g.nx && by + vy < g.ny && bz + vz < g.nz;
-            float ca = (ina && pa.jlo <= g.nt - 1 && pa.jlo + pa.L - 1 >= 0) ? P[v] * 0.5f * pa.inv_r : 0.0f;
-            float cb = (inb && pb.jlo <= g.nt - 1 && pb.jlo + pb.L - 1 >= 0) ? P[v + 1] * 0.5f * pb.inv_r : 0.0f;
-            int oa = pa.jlo - J, ob = pb.jlo - J;
-            if (ca != 0.0f && (oa < 0 || oa >= OMAX)) {
-                ovf |= 1u << v;
-                ca = 0.0f;
+        for (int v0 = 0; v0 < 8; v0 += NV) {
+            float cq[NV], DJ[NV], pq[NV], qq[NV], um[NV];
+            int oq[NV], oLq[NV];
+            float2 p2[NV], q2[NV], DJ2[NV], u2[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const int v = v0 + q, vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
+                const float ex = ex0 + (float)vx * g.hf;
+                const float ey = ((float)(2 * cy + vy) - 0.5f * (TY - 1)) * g.hf;
+                const float ez = ((float)(2 * cz + vz) - 0.5f * (TZ - 1)) * g.hf;
+                const Pair pv = pair<LMIN>(g, A, ex, ey, ez, __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez))));
+                const bool in = bx + vx < g.nx && by + vy < g.ny && bz + vz < g.nz;
+                float c = (in && pv.jlo <= g.nt - 1 && pv.jlo + pv.L - 1 >= 0) ? P[v] * 0.5f * pv.inv_r : 0.0f;
+                int o = pv.jlo - J;
+                if (c != 0.0f && (o < 0 || o >= OMAX)) {
+                    ovf |= 1u << v;
+                    c = 0.0f;
+                }
+                if (c == 0.0f) o = 0;
+                cq[q] = c;
+                oq[q] = o;
+                oLq[q] = o + pv.L;
+                DJ[q] = __fmaf_rn(jj, g.af, __fadd_rn(pv.drel, A.CA));
+                const float Dm = DJ[q] - mfa;  // D at the centre step M
+                // u_M = E(D_m) (C_M = 1); p = exp(a D_m / s^2); walk up with p, down with 1/p
+                um[q] = c * ex2(-g.k2 * Dm * Dm);
+                const float l = 2.0f * g.k2 * g.af * Dm;
+                pq[q] = ex2(l);
+                qq[q] = ex2(-l);
+                p2[q] = make_float2(ex2(2.0f * l), 0.0f);
+                q2[q] = make_float2(ex2(-2.0f * l), 0.0f);
+                DJ2[q] = make_float2(DJ[q], DJ[q]);
+                u2[q] = make_float2(um[q], um[q] * pq[q]);
             }
-            if (cb != 0.0f && (ob < 0 || ob >= OMAX)) {
-                ovf |= 2u << v;
-                cb = 0.0f;
-            }
-            if (ca == 0.0f) oa = 0;
-            if (cb == 0.0f) ob = 0;
-            const int oLa = oa + pa.L, oLb = ob + pb.L;
-            const float DJa = __fmaf_rn(jj, g.af, __fadd_rn(pa.drel, A.CA));
-            const float DJb = __fmaf_rn(jj, g.af, __fadd_rn(pb.drel, A.CA));
-            const float Dma = DJa - mfa, Dmb = DJb - mfa;  // D at the centre step M
-            // u_M = E(D_m) (C_M = 1); p = exp(a D_m / s^2); walk up with p, down with 1/p
-            const float uma = ca * ex2(-g.k2 * Dma * Dma), umb = cb * ex2(-g.k2 * Dmb * Dmb);
-            const float la = 2.0f * g.k2 * g.af * Dma, lb = 2.0f * g.k2 * g.af * Dmb;
-            const float pa_ = ex2(la), pb_ = ex2(lb), qa_ = ex2(-la), qb_ = ex2(-lb);
-            const float2 pa2 = make_float2(ex2(2.0f * la), 0.0f), pb2 = make_float2(ex2(2.0f * lb), 0.0f);
-            const float2 qa2 = make_float2(ex2(-2.0f * la), 0.0f), qb2 = make_float2(ex2(-2.0f * lb), 0.0f);
-            const float2 DJa2 = make_float2(DJa, DJa), DJb2 = make_float2(DJb, DJb);
             // -- upward, packed
-            float2 ua2 = make_float2(uma, uma * pa_), ub2 = make_float2(umb, umb * pb_);
 #pragma unroll
             for (int i = M; i < UPE; i += 2) {
-                const float2 Da = __ffma2_rn(fc.I2[i >> 1], af2, DJa2);
-                const float2 Db = __ffma2_rn(fc.I2[i >> 1], af2, DJb2);
-                acc2[i >> 1] = __ffma2_rn(ua2, Da, acc2[i >> 1]);
-                acc2[i >> 1] = __ffma2_rn(ub2, Db, acc2[i >> 1]);
-                ua2 = __fmul2_rn(ua2, make_float2(pa2.x, pa2.x));
-                ub2 = __fmul2_rn(ub2, make_float2(pb2.x, pb2.x));
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
+                    acc2[i >> 1] = __ffma2_rn(u2[q], D, acc2[i >> 1]);
+                    u2[q] = __fmul2_rn(u2[q], make_float2(p2[q].x, p2[q].x));
+                }
             }
             // -- upward tail, scalar (predicated on the window end); steps past every lane's
             // window end are skipped with a warp-uniform exit
-            const int tail_end = (int)__reduce_max_sync(0xffffffffu, (unsigned)max(oLa, oLb));
-            float ua = ua2.x, ub = ub2.x;
+            int mx = 0, mn = 0x7fffffff;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                mx = max(mx, oLq[q]);
+                mn = min(mn, oq[q]);
+            }
+            const int tail_end = (int)__reduce_max_sync(0xffffffffu, (unsigned)mx);
+            float us[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) us[q] = u2[q].x;
 #pragma unroll
             for (int i = UPE; i < R; ++i) {
                 if (i >= tail_end) break;
-                const float Da = __fmaf_rn(-(float)i, g.af, DJa);
-                const float Db = __fmaf_rn(-(float)i, g.af, DJb);
-                if (i < LMIN) {
-                    ACC(i) = __fmaf_rn(ua, Da, ACC(i));
-                    ACC(i) = __fmaf_rn(ub, Db, ACC(i));
-                } else {
-                    if (i < oLa) ACC(i) = __fmaf_rn(ua, Da, ACC(i));
-                    if (i < oLb) ACC(i) = __fmaf_rn(ub, Db, ACC(i));
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    const float D = __fmaf_rn(-(float)i, g.af, DJ[q]);
+                    if (i < LMIN || i < oLq[q]) ACC(i) = __fmaf_rn(us[q], D, ACC(i));
+                    us[q] *= pq[q];
                 }
-                ua *= pa_;
-                ub *= pb_;
             }
             // -- downward, packed on pairs (i, i+1), i = M-2, M-4, ..., DNE
-            ua2 = make_float2(uma * qa2.x, uma * qa_);
-            ub2 = make_float2(umb * qb2.x, umb * qb_);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) u2[q] = make_float2(um[q] * q2[q].x, um[q] * qq[q]);
 #pragma unroll
             for (int i = M - 2; i >= DNE; i -= 2) {
-                const float2 Da = __ffma2_rn(fc.I2[i >> 1], af2, DJa2);
-                const float2 Db = __ffma2_rn(fc.I2[i >> 1], af2, DJb2);
-                acc2[i >> 1] = __ffma2_rn(ua2, Da, acc2[i >> 1]);
-                acc2[i >> 1] = __ffma2_rn(ub2, Db, acc2[i >> 1]);
-                ua2 = __fmul2_rn(ua2, make_float2(qa2.x, qa2.x));
-                ub2 = __fmul2_rn(ub2, make_float2(qb2.x, qb2.x));
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
+                    acc2[i >> 1] = __ffma2_rn(u2[q], D, acc2[i >> 1]);
+                    u2[q] = __fmul2_rn(u2[q], make_float2(q2[q].x, q2[q].x));
+                }
             }
             // -- downward head, scalar (predicated on the window start); steps before every
             // lane's window start are skipped with a warp-uniform exit
-            const int head_beg = (int)__reduce_min_sync(0xffffffffu, (unsigned)min(oa, ob));
-            ua = ua2.y;
-            ub = ub2.y;
+            const int head_beg = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) us[q] = u2[q].y;
 #pragma unroll
             for (int i = DNE - 1; i >= 0; --i) {
                 if (i < head_beg) break;
-                const float Da = __fmaf_rn(-(float)i, g.af, DJa);
-                const float Db = __fmaf_rn(-(float)i, g.af, DJb);
-                if (i < OMAX - 1) {
-                    if (i >= oa) ACC(i) = __fmaf_rn(ua, Da, ACC(i));
-                    if (i >= ob) ACC(i) = __fmaf_rn(ub, Db, ACC(i));
-                } else {
-                    ACC(i) = __fmaf_rn(ua, Da, ACC(i));
-                    ACC(i) = __fmaf_rn(ub, Db, ACC(i));
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    const float D = __fmaf_rn(-(float)i, g.af, DJ[q]);
+                    if (i >= OMAX - 1 || i >= oq[q]) ACC(i) = __fmaf_rn(us[q], D, ACC(i));
+                    us[q] *= qq[q];
                 }
-                ua *= qa_;
-                ub *= qb_;
             }
         }
 #pragma unroll
@@ -878,7 +880,6 @@ __global__ void __launch_bounds__(TGV_BX *TGV_BY) k_tgv(TgvArgs t, const float *
         __syncthreads();
         if (x < t.nx && y < t.ny) {
             const int i = tx + 1, j = ty + 1, prv = cur ^ 1;
-            const float *n0 = &fld[cur][0][j][i];
             float gpv = 0.0f, gwv[3];
             float m0[6], mx[6], my[6], mz[6];
 #pragma unroll
@@ -890,7 +891,6 @@ __global__ void __launch_bounds__(TGV_BX *TGV_BY) k_tgv(TgvArgs t, const float *
             }
             const float nxm = fld[cur][0][j][i - 1], nym = fld[cur][1][j - 1][i], nzm = fld[prv][2][j][i];
             const float n00 = fld[cur][0][j][i], n01 = fld[cur][1][j][i], n02 = fld[cur][2][j][i];
-            (void)n0;
             gpv = t.a1 * t.inv_h * ((nxm - n00) + (nym - n01) + (nzm - n02));
             const float nn[3] = {n00, n01, n02};
 #pragma unroll
