@@ -39,7 +39,12 @@ class _Grid(ctypes.Structure):
 
 class _Acq(ctypes.Structure):
     _fields_ = [("c", ctypes.c_double), ("t0", ctypes.c_double), ("dt", ctypes.c_double),
-                ("nt", ctypes.c_int32), ("sigma", ctypes.c_double), ("kappa", ctypes.c_double)]
+                ("nt", ctypes.c_int32), ("sigma", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("kernel", ctypes.c_int32), ("nu", ctypes.c_double)]
+
+
+# kernel families of the designated kernel function K (R23)
+KERNELS = {"gauss": 0, "exp": 1, "pow": 2}
 
 
 def _load():
@@ -69,6 +74,9 @@ def _acq(acq) -> _Acq:
     a.c, a.t0, a.dt = float(acq["c"]), float(acq["t0"]), float(acq["dt"])
     a.nt = int(acq["nt"])
     a.sigma, a.kappa = float(acq["sigma"]), float(acq["kappa"])
+    k = acq.get("kernel", "gauss")
+    a.kernel = KERNELS[k] if isinstance(k, str) else int(k)
+    a.nu = float(acq.get("nu", 0.0))
     return a
 
 

@@ -17,9 +17,15 @@
  *   element position x_fe = R_f * tmpl_e + t_f, poses[f] = R row-major, t
  *   sample j at time t_j = t0 + j*dt                                           (R5)
  *   r = |x_fe - y_k|,  D = r - c*t_j
- *   traces[f,e,j] = sum_k p0[k] * D/(2r) * exp(-D^2/(2 sigma^2)) * [|D| <= kappa*sigma]
+ *   traces[f,e,j] = sum_k p0[k] * D/(2r) * K(|D|) * [|D| <= kappa*sigma]
  *                                                   (Eq. gpu_forward_model P:341-345,
  *                                                    cutoff R4 / S:141; kappa <= 0 => dense)
+ *   K = "the designated kernel function"; sigma is its scale s (R23):
+ *     kernel 0  Gaussian     K(D) = exp(-D^2 / 2 s^2)      (Eq. gaussian_far_field)
+ *     kernel 1  exponential  K(D) = exp(-|D| / s)          (Eq. exponential_solution, P:313-316,
+ *                                                           outgoing term, far field P:325-329)
+ *     kernel 2  power law    K(D) = (D^2 + s^2)^(-nu)      (Eq. power_law_solution, P:318-322,
+ *                                                           outgoing term, nu > 1/2)
  */
 #include <math.h>
 #include <stdint.h>
@@ -36,6 +42,8 @@ typedef struct {
     double c, t0, dt;
     int32_t nt;
     double sigma, kappa; /* kappa <= 0 : dense (no cutoff), documentation/FD mode (R11) */
+    int32_t kernel;      /* 0 Gaussian, 1 exponential, 2 power law (R23) */
+    double nu;           /* power-law exponent (kernel 2 only) */
 } og_acq;
 
 /* ---------------------------------------------------------------------------
@@ -101,19 +109,36 @@ static int window(const og_acq *a, double r, int *jlo_out, int *jhi_out)
     return 1;
 }
 
-/* N-shaped kernel h(D)/(2r) = D/(2r) exp(-D^2/2 sigma^2)   (Eq. gaussian_far_field) */
+/* The designated kernel K(D) and D K'(D) / K(D), by family (R23). */
+static double kfun(const og_acq *a, double D)
+{
+    double s = a->sigma;
+    if (a->kernel == 1) return exp(-fabs(D) / s);
+    if (a->kernel == 2) return pow(D * D + s * s, -a->nu);
+    return exp(-D * D / (2.0 * s * s));
+}
+
+static double dlogk_times_D(const og_acq *a, double D)
+{
+    double s = a->sigma;
+    if (a->kernel == 1) return -fabs(D) / s;                      /* d/dD e^{-|D|/s} = -sgn(D)/s K */
+    if (a->kernel == 2) return -2.0 * a->nu * D * D / (D * D + s * s);
+    return -D * D / (s * s);
+}
+
+/* N-shaped kernel h(D)/(2r) = D/(2r) K(|D|)   (Eq. gpu_forward_model) */
 static double kern(const og_acq *a, double r, int j)
 {
     double D = r - a->c * (a->t0 + (double)j * a->dt);
-    return D / (2.0 * r) * exp(-D * D / (2.0 * a->sigma * a->sigma));
+    return D / (2.0 * r) * kfun(a, D);
 }
 
-/* d/dr [h(D)/(2r)] = exp(-D^2/2s^2)/(2r) * [(1 - D^2/s^2) - D/r] */
+/* d/dr [D K(D)/(2r)] = K(D)/(2r) * [(1 + D K'/K) - D/r];
+ * Gaussian: 1 + D K'/K = 1 - D^2/s^2 */
 static double dkern_dr(const og_acq *a, double r, int j)
 {
-    double s2 = a->sigma * a->sigma;
     double D = r - a->c * (a->t0 + (double)j * a->dt);
-    return exp(-D * D / (2.0 * s2)) / (2.0 * r) * ((1.0 - D * D / s2) - D / r);
+    return kfun(a, D) / (2.0 * r) * ((1.0 + dlogk_times_D(a, D)) - D / r);
 }
 
 /* ---------------------------------------------------------------------------
