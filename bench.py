@@ -32,13 +32,24 @@ OPS_FWD = 4.5
 OPS_ADJ = 8.5
 N_SM = 148
 LANES = 128
+# kernel families (f3): algorithmic ops per in-window update and the pipe that bounds them.
+#   exp: E = min(A K_i, B/K_i) -> 2 FMUL + 1 MIN + D + FFMA (+0.5 setup) forward; adjoint + pose adds
+#        g E, |D| and three sums (SE, SD, SX)
+#   pow: MUFU-bound: lg2 + ex2 per update forward, + ex2(-lg2 x) for the pose sum; 16 XU lanes/SM
+FAMILIES = {
+    "gauss": dict(fwd=OPS_FWD, adj=OPS_ADJ, lanes=LANES, unit="T FP32-lane-op/s", pipe="128 FP32 lanes"),
+    "exp": dict(fwd=5.5, adj=9.5, lanes=LANES, unit="T FP32-lane-op/s", pipe="128 FP32 lanes"),
+    "pow": dict(fwd=2.0, adj=3.0, lanes=16, unit="T MUFU-op/s", pipe="16 MUFU (XU) lanes"),
+}
 LAUNCHES_PER_STEP = 9  # euler_pose, check, forward(+loss), rowloss_sum, adjoint+pose, pose_reduce, euler_grad, adam, adam_pose
 
 
 def describe(w):
-    g = w.grid
+    g, a = w.grid, w.acq
+    k = a.get("kernel", "gauss")
+    kern = {"gauss": "Gaussian kernel, sigma", "exp": "exponential kernel, s", "pow": f"power-law kernel nu={a.get('nu')}, s"}[k]
     return (f"{w.name}: {g['nx']}x{g['ny']}x{g['nz']} voxels @{g['pitch']} mm, {w.F} frames, {w.E}-element array, "
-            f"{w.acq['nt']} samples @40 MHz, sigma={w.acq['sigma']} mm, kappa={w.acq['kappa']}, c=1.5 mm/us")
+            f"{a['nt']} samples @40 MHz, {kern}={a['sigma']} mm, kappa={a['kappa']}, c=1.5 mm/us")
 
 
 class ClockSampler:
@@ -132,6 +143,7 @@ def run_reference(args):
     import oracle
 
     w = gen.workload(args.config)
+    w.acq = gen.family_acq(w.acq, args.kernel, args.nu)
     p0 = gen.phantom(w)
     poses = w.poses_true()
     # size the per-step sample once (about 10-20 s of CPU work)
@@ -165,7 +177,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": describe(w), "sample": sample},
+            "config": {"workload": describe(w), "kernel": args.kernel, "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -181,6 +193,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--frames", type=int, default=None, help="override the frame count (debug)")
+    ap.add_argument("--kernel", default="gauss", choices=sorted(FAMILIES),
+                    help="kernel family of K (f3): gauss (the paper's, default), exp, pow")
+    ap.add_argument("--nu", type=float, default=1.5, help="power-law exponent for --kernel pow")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -210,6 +225,7 @@ def main():
 
     # ---------------------------------------------------------------- workload (setup, untimed)
     w = gen.workload(args.config, frames=args.frames)
+    w.acq = gen.family_acq(w.acq, args.kernel, args.nu)
     p_true = gen.phantom(w).astype(np.float32)
     frames = shard_frames(w.F, world, rank)
     Fl = len(frames)
@@ -315,26 +331,28 @@ def main():
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
         peaks = json.load(fh)
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    peak = N_SM * LANES * f_max / 1e12
+    fam = FAMILIES[args.kernel]
+    ops_fwd, ops_adj, lanes = fam["fwd"], fam["adj"], fam["lanes"]
+    peak = N_SM * lanes * f_max / 1e12
     U_local_max = U / world  # frames are balanced; per-GPU roofline uses the per-rank share
-    adj_achieved = U_local_max * OPS_ADJ / (ams / 1e3) / 1e12 if ams > 0 else None
-    fwd_achieved = U_local_max * OPS_FWD / (fms / 1e3) / 1e12 if fms > 0 else None
+    adj_achieved = U_local_max * ops_adj / (ams / 1e3) / 1e12 if ams > 0 else None
+    fwd_achieved = U_local_max * ops_fwd / (fms / 1e3) / 1e12 if fms > 0 else None
     fwd_frac = fwd_achieved / peak if fwd_achieved else None
     adj_frac = adj_achieved / peak if adj_achieved else None
     f_meas = clocks["sm_mhz"] * 1e6 if clocks.get("sm_mhz") else None
     k_fwd = {"kernel": "k_forward (K1, forward + fused loss/cotangent)", "achieved": fwd_achieved, "frac": fwd_frac,
-             "ops_per_update": OPS_FWD, "ms_per_step": fms}
+             "ops_per_update": ops_fwd, "ms_per_step": fms}
     k_adj = {"kernel": "k_adjoint (K2, fused adjoint + pose gradient)", "achieved": adj_achieved, "frac": adj_frac,
-             "ops_per_update": OPS_ADJ, "ms_per_step": ams}
+             "ops_per_update": ops_adj, "ms_per_step": ams}
     dom, other = (k_fwd, k_adj) if fms >= ams else (k_adj, k_fwd)
     roofline = {"bound": "alu", "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
-                "unit": "T FP32-lane-op/s", "frac": dom["frac"], "traffic": None,
-                "peak_basis": f"148 SM x 128 FP32 lanes x sm_max {f_max / 1e6:.0f} MHz (MEASURED_PEAKS.json)",
+                "unit": fam["unit"], "frac": dom["frac"], "traffic": None,
+                "peak_basis": f"148 SM x {fam['pipe']} x sm_max {f_max / 1e6:.0f} MHz (MEASURED_PEAKS.json)",
                 "ops_per_update": dom["ops_per_update"], "kernel_ms_per_step": dom["ms_per_step"],
                 "kernel_share_of_step": dom["ms_per_step"] / ms if ms > 0 else None,
-                "frac_at_measured_clock": (dom["achieved"] * 1e12 / (N_SM * LANES * f_meas)) if (dom["achieved"] and f_meas) else None,
+                "frac_at_measured_clock": (dom["achieved"] * 1e12 / (N_SM * lanes * f_meas)) if (dom["achieved"] and f_meas) else None,
                 "other_kernel": other,
-                "step_frac": (U_local_max * (OPS_FWD + OPS_ADJ) / (ms / 1e3) / 1e12) / peak if ms > 0 else None,
+                "step_frac": (U_local_max * (ops_fwd + ops_adj) / (ms / 1e3) / 1e12) / peak if ms > 0 else None,
                 "traffic_note": "DRAM bytes per launch from ncu --set full on the C4 geometry with 16 frames "
                                 "(profiles/r1_ncu_c4_k_*.md): k_adjoint 89 MB read + 42 MB written, k_forward 257 MB "
                                 "read + 22 MB written; both are ALU-bound (>= 5e4 updates per DRAM byte)"}
@@ -346,7 +364,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "s_per_iteration": ms / 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded vascular phantom, freehand sweep; meas = forward at true poses)",
-        "config": {"workload": describe(w), "frames_per_rank": Fl, "updates_per_pass": U,
+        "config": {"workload": describe(w), "kernel": args.kernel, "frames_per_rank": Fl, "updates_per_pass": U,
                    "parallelism": f"frame-sharded x{world}, NCCL all-reduce of dL/dp0",
                    "l2": "inputs larger than L2 (meas + cotangent per step) and a 256 MiB L2 flush before every timed step"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,

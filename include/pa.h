@@ -7,8 +7,12 @@
  *
  * The operator (Eq. gpu_forward_model; Eq. 1):
  *
- *   traces[f][e][j] = sum_k p0[k] * D/(2r) * exp(-D^2 / (2 sigma^2)) * [|D| <= kappa*sigma]
+ *   traces[f][e][j] = sum_k p0[k] * D/(2r) * K(|D|) * [|D| <= kappa*sigma]
  *   r = |x_fe - y_k|,  D = r - c (t0 + j dt),  x_fe = R_f tmpl[e] + t_f  (Stage 4)
+ *   K = "the designated kernel function", scale s = sigma (pa_acq.kernel, R23):
+ *     PA_KERNEL_GAUSS  K = exp(-D^2 / (2 s^2))   [default]
+ *     PA_KERNEL_EXP    K = exp(-|D| / s)           (outgoing term of P:313-316)
+ *     PA_KERNEL_POW    K = (D^2 + s^2)^(-nu)       (outgoing term of P:318-322)
  *   y_k = origin + pitch * (i, j, l),  k = i + nx*(j + ny*l)    (x fastest, R7)
  *
  * Units: mm, µs, mm/µs.  Arithmetic: fp32 with fp64 per-tile anchors.
@@ -55,12 +59,24 @@ typedef struct {
     float pitch;
 } pa_grid;
 
+/* Kernel families of the designated kernel K (f3 of SURVEY §8; reading R23). */
+typedef enum {
+    PA_KERNEL_GAUSS = 0, /* exp(-D^2/2s^2): the paper's kernel (Eq. gaussian_far_field)    */
+    PA_KERNEL_EXP = 1,   /* exp(-|D|/s): far field of the exponential distribution  */
+    PA_KERNEL_POW = 2    /* (D^2+s^2)^-nu, nu in (1/2, 16]: far field of the power law     */
+} pa_kernel;
+
 /* Acquisition + kernel.  Sample j at t0 + j*dt (R5); speed of sound c;
- * Gaussian width sigma; window |D| <= kappa*sigma, kappa >= 4 (R4). */
+ * kernel scale sigma (the Gaussian width; s of the other families, R23); window
+ * |D| <= kappa*sigma, kappa >= 4 (R4; kappa <= 30 for PA_KERNEL_EXP so that the factored
+ * recurrence constants stay in fp32 range).  `kernel` is a pa_kernel; `nu` is read only for
+ * PA_KERNEL_POW.  Bad kernel / nu / kappa -> PA_EINVAL. */
 typedef struct {
     float c, t0, dt;
     int32_t nt;
     float sigma, kappa;
+    int32_t kernel;
+    float nu;
 } pa_acq;
 
 typedef struct pa_ctx pa_ctx;
@@ -88,7 +104,7 @@ pa_status pa_forward(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
 
 /*
  * a4 — adjoint back-projection, the exact transpose of pa_forward:
- *   grad_p0[k] = sum_f sum_e sum_j cot[f][e][j] * D/(2r) exp(-D^2/2sigma^2) [|D| <= kappa sigma]
+ *   grad_p0[k] = sum_f sum_e sum_j cot[f][e][j] * D/(2r) K(|D|) [|D| <= kappa sigma]
  *   cot [F][E][nt] cotangent dL/dtraces;  grad_p0 [nz][ny][nx] output (overwritten).
  */
 pa_status pa_adjoint(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
@@ -96,7 +112,7 @@ pa_status pa_adjoint(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
 
 /*
  * a5+a6 — pose gradient ("sensor spatial coordinates"; Stage 4 P:109-115):
- *   grad_elem[f][e] = sum_k p0[k] sum_j cot[f][e][j] d/dr[D/(2r) e^{-D^2/2s^2}] (x_fe - y_k)/r
+ *   grad_elem[f][e] = sum_k p0[k] sum_j cot[f][e][j] d/dr[D K(|D|)/(2r)] (x_fe - y_k)/r
  *                     (window indicator held constant, R11)
  *   grad_pose[f] = [ dL/dR_f (row-major 3x3) = sum_e grad_elem[f][e] tmpl[e]^T , dL/dt_f = sum_e grad_elem[f][e] ]
  *   grad_pose [F][12] output; grad_elem [F][E][3] output or NULL.

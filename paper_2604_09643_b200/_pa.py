@@ -34,7 +34,12 @@ class Grid(ctypes.Structure):
 
 class Acq(ctypes.Structure):
     _fields_ = [("c", ctypes.c_float), ("t0", ctypes.c_float), ("dt", ctypes.c_float), ("nt", ctypes.c_int32),
-                ("sigma", ctypes.c_float), ("kappa", ctypes.c_float)]
+                ("sigma", ctypes.c_float), ("kappa", ctypes.c_float), ("kernel", ctypes.c_int32),
+                ("nu", ctypes.c_float)]
+
+
+# pa_kernel: families of the designated kernel K (reading R23)
+KERNELS = {"gauss": 0, "exp": 1, "pow": 2}
 
 
 class StepCfg(ctypes.Structure):
@@ -102,6 +107,9 @@ def make_acq(acq: dict) -> Acq:
     a.c, a.t0, a.dt = float(acq["c"]), float(acq["t0"]), float(acq["dt"])
     a.nt = int(acq["nt"])
     a.sigma, a.kappa = float(acq["sigma"]), float(acq["kappa"])
+    k = acq.get("kernel", "gauss")
+    a.kernel = KERNELS[k] if isinstance(k, str) else int(k)
+    a.nu = float(acq.get("nu", 0.0))
     return a
 
 

@@ -49,6 +49,7 @@ struct Plan {
     FwdConst fc;
     AdjConst ac;
     int klass;
+    int fam;  // pa_kernel (KF_*)
 };
 
 pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &pl)
@@ -62,6 +63,12 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
         return fail(PA_EINVAL, "c, dt, nt, sigma must be positive");
     if (!std::isfinite(acq->t0)) return fail(PA_EINVAL, "t0 must be finite");
     if (!(acq->kappa >= 4.f)) return fail(PA_EINVAL, "kappa must be >= 4 (got %g)", (double)acq->kappa);
+    if (acq->kernel < PA_KERNEL_GAUSS || acq->kernel > PA_KERNEL_POW)
+        return fail(PA_EINVAL, "kernel must be PA_KERNEL_GAUSS, _EXP or _POW (got %d)", (int)acq->kernel);
+    if (acq->kernel == PA_KERNEL_EXP && !(acq->kappa <= 30.f))
+        return fail(PA_EINVAL, "kappa must be <= 30 for PA_KERNEL_EXP (got %g)", (double)acq->kappa);
+    if (acq->kernel == PA_KERNEL_POW && !(acq->nu > 0.5f && acq->nu <= 16.f))
+        return fail(PA_EINVAL, "nu must be in (1/2, 16] for PA_KERNEL_POW (got %g)", (double)acq->nu);
     if (E < 1) return fail(PA_ESHAPE, "E must be >= 1");
     if (F < 0) return fail(PA_ESHAPE, "F must be >= 0");
     Geo &g = pl.g;
@@ -100,6 +107,9 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     g.s2 = (float)(sig * sig);
     g.inv_s2 = (float)(1.0 / (sig * sig));
     g.rt = (float)g.rt_d;
+    g.ls = (float)(1.4426950408889634 / sig);
+    g.nu = acq->kernel == PA_KERNEL_POW ? acq->nu : 0.0f;
+    pl.fam = acq->kernel;
 
     const double K2 = 2.0 * g.ksig_d / a;
     const int wmin = (int)std::floor(K2);
@@ -120,17 +130,30 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
         g.mF = ((c.lmin + c.omax) / 2) & ~1;  // == FwdMid<LMIN,OMAX>::m
         g.mA = (c.lmin + 1) / 2;  // == AdjMid<LMIN>::m
         const double be = a * a / (2.0 * sig * sig);
+        const double as = a / sig;  // exponential family: K_i = exp((i - m) a / s)
         for (int k = 0; k < 64; ++k) {
             const double k0 = 2 * k - g.mF, k1 = 2 * k + 1 - g.mF;
-            pl.fc.C2[k] = make_float2((float)std::exp(-k0 * k0 * be), (float)std::exp(-k1 * k1 * be));
+            if (pl.fam == PA_KERNEL_EXP) {
+                pl.fc.C2[k] = make_float2((float)std::exp(k0 * as), (float)std::exp(k1 * as));
+                pl.fc.X2[k] = make_float2((float)std::exp(-k0 * as), (float)std::exp(-k1 * as));
+            } else {
+                pl.fc.C2[k] = make_float2((float)std::exp(-k0 * k0 * be), (float)std::exp(-k1 * k1 * be));
+                pl.fc.X2[k] = make_float2(0.0f, 0.0f);
+            }
             pl.fc.I2[k] = make_float2((float)(-2 * k), (float)(-2 * k - 1));
         }
         for (int i = 0; i < 128; ++i) {
             const double ka = i - g.mA;
-            const double ca = std::exp(-ka * ka * be);
-            pl.ac.C0[i] = (float)ca;
-            pl.ac.C1[i] = (float)(ca * ka);
-            pl.ac.C2[i] = (float)(ca * ka * ka);
+            if (pl.fam == PA_KERNEL_EXP) {
+                pl.ac.C0[i] = (float)std::exp(ka * as);
+                pl.ac.C1[i] = (float)std::exp(-ka * as);
+                pl.ac.C2[i] = 0.0f;
+            } else {
+                const double ca = std::exp(-ka * ka * be);
+                pl.ac.C0[i] = (float)ca;
+                pl.ac.C1[i] = (float)(ca * ka);
+                pl.ac.C2[i] = (float)(ca * ka * ka);
+            }
         }
     }
     if (pl.klass < 0)
@@ -498,27 +521,38 @@ pa_status check_degenerate(pa_ctx *ctx, const Plan &pl, const float *poses, cons
 }
 
 // ---------------------------------------------------------------- launchers per class
-template <int LMIN, int OMAX, int SPAN>
+template <int LMIN, int OMAX, int SPAN, int FAM>
 pa_status launch_forward_t(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
                            const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
 {
     using C = FwdCfg<LMIN, OMAX, SPAN>;
     const size_t smem = (size_t)FWD_WARPS * C::warp_floats(pl.g.nt) * sizeof(float);
     if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "nt=%d too long for the forward kernel's shared memory", pl.g.nt);
-    auto kern = k_forward<LMIN, OMAX, SPAN>;
+    auto kern = k_forward<LMIN, OMAX, SPAN, FAM>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<pl.g.F * pl.g.E, FWD_WARPS * 32, smem, st>>>(pl.g, pl.fc, poses, tmpl, p0, out, mode, meas, mask, rowloss);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
 
+template <int FAM>
+pa_status launch_forward_f(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
+                           const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
+{
+    switch (pl.klass) {
+    case 0: return launch_forward_t<53, 11, 58, FAM>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    case 1: return launch_forward_t<26, 6, 30, FAM>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    default: return launch_forward_t<106, 21, 114, FAM>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    }
+}
+
 pa_status launch_forward(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
                          const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
 {
-    switch (pl.klass) {
-    case 0: return launch_forward_t<53, 11, 58>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    case 1: return launch_forward_t<26, 6, 30>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    default: return launch_forward_t<106, 21, 114>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    switch (pl.fam) {
+    case KF_EXP: return launch_forward_f<KF_EXP>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    case KF_POW: return launch_forward_f<KF_POW>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    default: return launch_forward_f<KF_GAUSS>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
     }
 }
 
@@ -527,11 +561,11 @@ struct AdjLaunch {
     size_t smem = 0;
 };
 
-template <int LMIN, int SEG, bool POSE, bool ADJ>
+template <int LMIN, int SEG, bool POSE, bool ADJ, int FAM>
 pa_status launch_adjoint_t(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
                            const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
 {
-    auto kern = k_adjoint<LMIN, SEG, POSE, ADJ>;
+    auto kern = k_adjoint<LMIN, SEG, POSE, ADJ, FAM>;
     const int E = pl.g.E, F = pl.g.F;
     int Fc = POSE ? 64 : F;
     size_t smem = AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float);
@@ -563,14 +597,25 @@ pa_status launch_adjoint_t(pa_ctx *ctx, const Plan &pl, const float *poses, cons
     return PA_OK;
 }
 
+template <bool POSE, bool ADJ, int FAM>
+pa_status launch_adjoint_f(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
+                           const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
+{
+    switch (pl.klass) {
+    case 0: return launch_adjoint_t<53, 128, POSE, ADJ, FAM>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    case 1: return launch_adjoint_t<26, 64, POSE, ADJ, FAM>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    default: return launch_adjoint_t<106, 256, POSE, ADJ, FAM>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    }
+}
+
 template <bool POSE, bool ADJ>
 pa_status launch_adjoint(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
                          const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
 {
-    switch (pl.klass) {
-    case 0: return launch_adjoint_t<53, 128, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    case 1: return launch_adjoint_t<26, 64, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    default: return launch_adjoint_t<106, 256, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    switch (pl.fam) {
+    case KF_EXP: return launch_adjoint_f<POSE, ADJ, KF_EXP>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    case KF_POW: return launch_adjoint_f<POSE, ADJ, KF_POW>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    default: return launch_adjoint_f<POSE, ADJ, KF_GAUSS>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
     }
 }
 
@@ -640,7 +685,7 @@ extern "C" {
 
 const char *pa_last_error(void) { return g_err.c_str(); }
 
-const char *pa_version(void) { return "libpa 0.1 (sm_100a, fp32 + fp64 anchors)"; }
+const char *pa_version(void) { return "libpa 0.2 (sm_100a, fp32 + fp64 anchors; Gaussian/exponential/power-law kernels)"; }
 
 pa_status pa_create(pa_ctx **out, int device)
 {

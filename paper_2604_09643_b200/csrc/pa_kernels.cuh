@@ -41,19 +41,26 @@ struct Geo {
     float k2, two_a_k2, a2_k2;  // log2(e)/(2 s^2), 2a*k2, a^2*k2
     float s2, inv_s2, rt;
     int mF, mA;                 // recurrence centres (forward cluster window / adjoint pair window)
+    float ls, nu;               // exponential: log2(e)/s; power law: nu   (kernel families, R23)
 };
+
+// Kernel families of the designated kernel K(D) (R23): template parameter FAM.
+enum { KF_GAUSS = 0, KF_EXP = 1, KF_POW = 2 };
 
 // Step-index constants of the factored Gaussian (DESIGN.md §6 "recurrence"):
 //   exp(-D_i^2/2s^2) = u_i * C_i,  D_i = D_m - (i - m) a,  C_i = exp(-(i-m)^2 a^2 / 2s^2),
 //   u_i = u_0 p^i,  p = exp(a D_m / s^2),  u_0 = exp(-(D_m^2 + 2 m a D_m) / 2s^2).
+// Exponential family: exp(-|D_i|/s) = min(A K_i, B / K_i) with K_i = exp((i - m) a / s),
+// A = exp(-D_m/s), B = exp(D_m/s) (one of the two is the value, the other its reciprocal).
 struct FwdConst {
-    float2 C2[64];   // (C_2k, C_2k+1) about the cluster-window centre mF
+    float2 C2[64];   // Gaussian: (C_2k, C_2k+1) about the cluster-window centre mF; exp: (K_2k, K_2k+1)
     float2 I2[64];   // (-2k, -2k-1): step indices for packed D_i = D_J - i a
+    float2 X2[64];   // exp: (1/K_2k, 1/K_2k+1)
 };
 struct AdjConst {
-    float C0[128];  // C_i about the pair-window centre mA
-    float C1[128];  // C_i (i - mA)
-    float C2[128];  // C_i (i - mA)^2
+    float C0[128];  // Gaussian: C_i about the pair-window centre mA;  exp: K_i
+    float C1[128];  // Gaussian: C_i (i - mA);                           exp: 1/K_i
+    float C2[128];  // Gaussian: C_i (i - mA)^2
 };
 
 struct Anc {
@@ -68,6 +75,13 @@ __device__ __forceinline__ float ex2(float x)
 {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float lg2(float x)
+{
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 
@@ -219,7 +233,42 @@ struct FwdMid {
     static constexpr int m = ((LMIN + OMAX) / 2) & ~1;  // even: packed (i, i+1) pairs stay register-pair aligned
 };
 
-template <int LMIN, int OMAX, int SPAN>
+// K(D) evaluated directly (slow paths)
+template <int FAM>
+__device__ __forceinline__ float fam_direct(const Geo &g, float D)
+{
+    if constexpr (FAM == KF_GAUSS) return ex2(-D * D * g.k2);
+    else if constexpr (FAM == KF_EXP) return ex2(-fabsf(D) * g.ls);
+    else return ex2(-g.nu * lg2(__fmaf_rn(D, D, g.s2)));
+}
+
+// Kernel-family values at step i for the generic (non-Gaussian) forward path: packed (i, i+1)
+// and scalar.  A, B: exp family per-voxel factors (c folded in); c: amplitude (power law).
+template <int FAM>
+__device__ __forceinline__ float2 fam_val2(const Geo &g, const FwdConst &fc, int i2, float2 D, float A, float B)
+{
+    if constexpr (FAM == KF_EXP) {
+        const float2 t1 = __fmul2_rn(make_float2(A, A), fc.C2[i2]);
+        const float2 t2 = __fmul2_rn(make_float2(B, B), fc.X2[i2]);
+        return make_float2(fminf(t1.x, t2.x), fminf(t1.y, t2.y));
+    } else {
+        const float2 x = __ffma2_rn(D, D, make_float2(g.s2, g.s2));
+        return make_float2(A * ex2(-g.nu * lg2(x.x)), A * ex2(-g.nu * lg2(x.y)));
+    }
+}
+template <int FAM>
+__device__ __forceinline__ float fam_val1(const Geo &g, const FwdConst &fc, int i, float D, float A, float B)
+{
+    if constexpr (FAM == KF_EXP) {
+        const float K = (i & 1) ? fc.C2[i >> 1].y : fc.C2[i >> 1].x;
+        const float Ki = (i & 1) ? fc.X2[i >> 1].y : fc.X2[i >> 1].x;
+        return fminf(A * K, B * Ki);
+    } else {
+        return A * ex2(-g.nu * lg2(__fmaf_rn(D, D, g.s2)));
+    }
+}
+
+template <int LMIN, int OMAX, int SPAN, int FAM>
 __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <= 64) ? 3 : 2) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
                                                             const float *__restrict__ tmpl,
                                                             const float *__restrict__ p0, float *__restrict__ out,
@@ -340,78 +389,131 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
                 oLq[q] = o + pv.L;
                 DJ[q] = __fmaf_rn(jj, g.af, __fadd_rn(pv.drel, A.CA));
                 const float Dm = DJ[q] - mfa;  // D at the centre step M
-                // u_M = E(D_m) (C_M = 1); p = exp(a D_m / s^2); walk up with p, down with 1/p
-                um[q] = c * ex2(-g.k2 * Dm * Dm);
-                const float l = 2.0f * g.k2 * g.af * Dm;
-                pq[q] = ex2(l);
-                qq[q] = ex2(-l);
-                p2[q] = make_float2(ex2(2.0f * l), 0.0f);
-                q2[q] = make_float2(ex2(-2.0f * l), 0.0f);
                 DJ2[q] = make_float2(DJ[q], DJ[q]);
-                u2[q] = make_float2(um[q], um[q] * pq[q]);
-            }
-            // -- upward, packed
-#pragma unroll
-            for (int i = M; i < UPE; i += 2) {
-#pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
-                    acc2[i >> 1] = __ffma2_rn(u2[q], D, acc2[i >> 1]);
-                    u2[q] = __fmul2_rn(u2[q], make_float2(p2[q].x, p2[q].x));
+                if constexpr (FAM == KF_GAUSS) {
+                    // u_M = E(D_m) (C_M = 1); p = exp(a D_m / s^2); walk up with p, down with 1/p
+                    um[q] = c * ex2(-g.k2 * Dm * Dm);
+                    const float l = 2.0f * g.k2 * g.af * Dm;
+                    pq[q] = ex2(l);
+                    qq[q] = ex2(-l);
+                    p2[q] = make_float2(ex2(2.0f * l), 0.0f);
+                    q2[q] = make_float2(ex2(-2.0f * l), 0.0f);
+                    u2[q] = make_float2(um[q], um[q] * pq[q]);
+                } else if constexpr (FAM == KF_EXP) {
+                    // A = c exp(-D_m/s), B = c exp(D_m/s) (exponent clamped: c = 0 rows stay 0)
+                    const float l = fminf(fmaxf(g.ls * Dm, -100.0f), 100.0f);
+                    um[q] = c * ex2(-l);
+                    pq[q] = c * ex2(l);
+                } else {
+                    um[q] = c;
+                    pq[q] = 0.0f;
                 }
             }
-            // -- upward tail, scalar (predicated on the window end); steps past every lane's
-            // window end are skipped with a warp-uniform exit
-            int mx = 0, mn = 0x7fffffff;
+            if constexpr (FAM == KF_GAUSS) {
+                // -- upward, packed
 #pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                mx = max(mx, oLq[q]);
-                mn = min(mn, oq[q]);
-            }
-            const int tail_end = (int)__reduce_max_sync(0xffffffffu, (unsigned)mx);
-            float us[NV];
+                for (int i = M; i < UPE; i += 2) {
 #pragma unroll
-            for (int q = 0; q < NV; ++q) us[q] = u2[q].x;
-#pragma unroll
-            for (int i = UPE; i < R; ++i) {
-                if (i >= tail_end) break;
-#pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    const float D = __fmaf_rn(-(float)i, g.af, DJ[q]);
-                    if (i < LMIN || i < oLq[q]) ACC(i) = __fmaf_rn(us[q], D, ACC(i));
-                    us[q] *= pq[q];
+                    for (int q = 0; q < NV; ++q) {
+                        const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
+                        acc2[i >> 1] = __ffma2_rn(u2[q], D, acc2[i >> 1]);
+                        u2[q] = __fmul2_rn(u2[q], make_float2(p2[q].x, p2[q].x));
+                    }
                 }
-            }
-            // -- downward, packed on pairs (i, i+1), i = M-2, M-4, ..., DNE
-#pragma unroll
-            for (int q = 0; q < NV; ++q) u2[q] = make_float2(um[q] * q2[q].x, um[q] * qq[q]);
-#pragma unroll
-            for (int i = M - 2; i >= DNE; i -= 2) {
+                // -- upward tail, scalar (predicated on the window end); steps past every lane's
+                // window end are skipped with a warp-uniform exit
+                int mx = 0, mn = 0x7fffffff;
 #pragma unroll
                 for (int q = 0; q < NV; ++q) {
-                    const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
-                    acc2[i >> 1] = __ffma2_rn(u2[q], D, acc2[i >> 1]);
-                    u2[q] = __fmul2_rn(u2[q], make_float2(q2[q].x, q2[q].x));
+                    mx = max(mx, oLq[q]);
+                    mn = min(mn, oq[q]);
                 }
-            }
-            // -- downward head, scalar (predicated on the window start); steps before every
-            // lane's window start are skipped with a warp-uniform exit
-            const int head_beg = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+                const int tail_end = (int)__reduce_max_sync(0xffffffffu, (unsigned)mx);
+                float us[NV];
 #pragma unroll
-            for (int q = 0; q < NV; ++q) us[q] = u2[q].y;
+                for (int q = 0; q < NV; ++q) us[q] = u2[q].x;
 #pragma unroll
-            for (int i = DNE - 1; i >= 0; --i) {
-                if (i < head_beg) break;
+                for (int i = UPE; i < R; ++i) {
+                    if (i >= tail_end) break;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const float D = __fmaf_rn(-(float)i, g.af, DJ[q]);
+                        if (i < LMIN || i < oLq[q]) ACC(i) = __fmaf_rn(us[q], D, ACC(i));
+                        us[q] *= pq[q];
+                    }
+                }
+                // -- downward, packed on pairs (i, i+1), i = M-2, M-4, ..., DNE
+#pragma unroll
+                for (int q = 0; q < NV; ++q) u2[q] = make_float2(um[q] * q2[q].x, um[q] * qq[q]);
+#pragma unroll
+                for (int i = M - 2; i >= DNE; i -= 2) {
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
+                        acc2[i >> 1] = __ffma2_rn(u2[q], D, acc2[i >> 1]);
+                        u2[q] = __fmul2_rn(u2[q], make_float2(q2[q].x, q2[q].x));
+                    }
+                }
+                // -- downward head, scalar (predicated on the window start); steps before every
+                // lane's window start are skipped with a warp-uniform exit
+                const int head_beg = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+#pragma unroll
+                for (int q = 0; q < NV; ++q) us[q] = u2[q].y;
+#pragma unroll
+                for (int i = DNE - 1; i >= 0; --i) {
+                    if (i < head_beg) break;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const float D = __fmaf_rn(-(float)i, g.af, DJ[q]);
+                        if (i >= OMAX - 1 || i >= oq[q]) ACC(i) = __fmaf_rn(us[q], D, ACC(i));
+                        us[q] *= qq[q];
+                    }
+                }
+            } else {
+                // exponential / power law: no recurrence state; packed where every voxel of the
+                // pass is in-window, scalar and predicated at the edges (warp-uniform exits)
+#pragma unroll
+                for (int i = DNE; i + 1 < UPE; i += 2) {
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
+                        acc2[i >> 1] = __ffma2_rn(fam_val2<FAM>(g, fc, i >> 1, D, um[q], pq[q]), D, acc2[i >> 1]);
+                    }
+                }
+                int mx = 0, mn = 0x7fffffff;
 #pragma unroll
                 for (int q = 0; q < NV; ++q) {
-                    const float D = __fmaf_rn(-(float)i, g.af, DJ[q]);
-                    if (i >= OMAX - 1 || i >= oq[q]) ACC(i) = __fmaf_rn(us[q], D, ACC(i));
-                    us[q] *= qq[q];
+                    mx = max(mx, oLq[q]);
+                    mn = min(mn, oq[q]);
+                }
+                const int tail_end = (int)__reduce_max_sync(0xffffffffu, (unsigned)mx);
+                const int head_beg = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+#pragma unroll
+                for (int i = UPE; i < R; ++i) {
+                    if (i >= tail_end) break;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const float D = __fmaf_rn(-(float)i, g.af, DJ[q]);
+                        const float Ev = fam_val1<FAM>(g, fc, i, D, um[q], pq[q]);
+                        if (i < LMIN || i < oLq[q]) ACC(i) = __fmaf_rn(Ev, D, ACC(i));
+                    }
+                }
+#pragma unroll
+                for (int i = DNE - 1; i >= 0; --i) {
+                    if (i < head_beg) break;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const float D = __fmaf_rn(-(float)i, g.af, DJ[q]);
+                        const float Ev = fam_val1<FAM>(g, fc, i, D, um[q], pq[q]);
+                        if (i >= OMAX - 1 || i >= oq[q]) ACC(i) = __fmaf_rn(Ev, D, ACC(i));
+                    }
                 }
             }
         }
+        if constexpr (FAM == KF_GAUSS) {
 #pragma unroll
-        for (int k = 0; k < R2; ++k) acc2[k] = __fmul2_rn(acc2[k], fc.C2[k]);  // acc'_i C_i -> samples
+            for (int k = 0; k < R2; ++k) acc2[k] = __fmul2_rn(acc2[k], fc.C2[k]);
+        }  // acc'_i C_i -> samples
 
         // ---- flush, in two half-warp phases: lanes (16 ph .. 16 ph + 15) write C_i acc'_i into
         // column (J - Jmin + i), row lane%16, of the column-major buffer (zero between uses);
@@ -474,7 +576,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
                         for (int i = 0; i < pv.L; ++i) {
                             const int j = pv.jlo + i;
                             const float D = __fmaf_rn(-(float)(j - A.JA), g.af, __fadd_rn(pv.drel, A.CA));
-                            if (j >= 0 && j < g.nt) trw[C::PADL + j] += cv * D * ex2(-D * D * g.k2);
+                            if (j >= 0 && j < g.nt) trw[C::PADL + j] += cv * D * fam_direct<FAM>(g, D);
                         }
                     }
                 }
@@ -579,7 +681,7 @@ struct AncS {  // anchor as stored in shared memory (12 words)
     int JA, cull, jseg;
 };
 
-template <int LMIN, int SEG, bool POSE, bool ADJ>
+template <int LMIN, int SEG, bool POSE, bool ADJ, int FAM>
 __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, const float *__restrict__ poses,
                                                            const float *__restrict__ tmpl,
                                                            const float *__restrict__ p0,
@@ -671,46 +773,105 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                         constexpr int MA = AdjMid<LMIN>::m;
                         const float Dma = __fmaf_rn(-(float)(pa.jlo - sa.JA), g.af, __fadd_rn(pa.drel, sa.CA)) - (float)MA * g.af;
                         const float Dmb = __fmaf_rn(-(float)(pb.jlo - sb.JA), g.af, __fadd_rn(pb.drel, sb.CA)) - (float)MA * g.af;
-                        // centre-out: u_MA = E(D_m); up with p = exp(a D_m/s^2), down with 1/p
-                        const float2 um = make_float2(ex2(-g.k2 * Dma * Dma), ex2(-g.k2 * Dmb * Dmb));
-                        const float la = 2.0f * g.k2 * g.af * Dma, lb = 2.0f * g.k2 * g.af * Dmb;
-                        const float2 pu = make_float2(ex2(la), ex2(lb)), pd = make_float2(ex2(-la), ex2(-lb));
-                        float2 S0 = make_float2(0.f, 0.f), S1 = S0, S2 = S0;  // sum g E k^n, k = i - MA
-                        float2 u = um;
+                        // A1 = sum g D K (adjoint);  A2 = sum g (K + D K') (pose, d/dr of D K)
+                        float A1a, A1b, A2a = 0.0f, A2b = 0.0f;
+                        if constexpr (FAM == KF_GAUSS) {
+                            // centre-out: u_MA = E(D_m); up with p = exp(a D_m/s^2), down with 1/p
+                            const float2 um = make_float2(ex2(-g.k2 * Dma * Dma), ex2(-g.k2 * Dmb * Dmb));
+                            const float la = 2.0f * g.k2 * g.af * Dma, lb = 2.0f * g.k2 * g.af * Dmb;
+                            const float2 pu = make_float2(ex2(la), ex2(lb)), pd = make_float2(ex2(-la), ex2(-lb));
+                            float2 S0 = make_float2(0.f, 0.f), S1 = S0, S2 = S0;  // sum g E k^n, k = i - MA
+                            float2 u = um;
 #pragma unroll
-                        for (int i = MA; i < LMAX; ++i) {
-                            float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), u);
-                            if (i >= LMIN) {
-                                t.x = i < pa.L ? t.x : 0.0f;
-                                t.y = i < pb.L ? t.y : 0.0f;
+                            for (int i = MA; i < LMAX; ++i) {
+                                float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), u);
+                                if (i >= LMIN) {
+                                    t.x = i < pa.L ? t.x : 0.0f;
+                                    t.y = i < pb.L ? t.y : 0.0f;
+                                }
+                                S0 = __ffma2_rn(t, make_float2(ac.C0[i], ac.C0[i]), S0);
+                                S1 = __ffma2_rn(t, make_float2(ac.C1[i], ac.C1[i]), S1);
+                                if (POSE) S2 = __ffma2_rn(t, make_float2(ac.C2[i], ac.C2[i]), S2);
+                                u = __fmul2_rn(u, pu);
                             }
-                            S0 = __ffma2_rn(t, make_float2(ac.C0[i], ac.C0[i]), S0);
-                            S1 = __ffma2_rn(t, make_float2(ac.C1[i], ac.C1[i]), S1);
-                            if (POSE) S2 = __ffma2_rn(t, make_float2(ac.C2[i], ac.C2[i]), S2);
-                            u = __fmul2_rn(u, pu);
-                        }
-                        u = __fmul2_rn(um, pd);
+                            u = __fmul2_rn(um, pd);
 #pragma unroll
-                        for (int i = MA - 1; i >= 0; --i) {
-                            const float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), u);
-                            S0 = __ffma2_rn(t, make_float2(ac.C0[i], ac.C0[i]), S0);
-                            S1 = __ffma2_rn(t, make_float2(ac.C1[i], ac.C1[i]), S1);
-                            if (POSE) S2 = __ffma2_rn(t, make_float2(ac.C2[i], ac.C2[i]), S2);
-                            u = __fmul2_rn(u, pd);
+                            for (int i = MA - 1; i >= 0; --i) {
+                                const float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), u);
+                                S0 = __ffma2_rn(t, make_float2(ac.C0[i], ac.C0[i]), S0);
+                                S1 = __ffma2_rn(t, make_float2(ac.C1[i], ac.C1[i]), S1);
+                                if (POSE) S2 = __ffma2_rn(t, make_float2(ac.C2[i], ac.C2[i]), S2);
+                                u = __fmul2_rn(u, pd);
+                            }
+                            // A1 = sum g D E = Dm S0 - a S1 ;  Bq = sum g E (D^2 - s^2)
+                            A1a = __fmaf_rn(-g.af, S1.x, Dma * S0.x);
+                            A1b = __fmaf_rn(-g.af, S1.y, Dmb * S0.y);
+                            float Bqa = 0.0f, Bqb = 0.0f;
+                            if (POSE) {
+                                Bqa = (Dma * Dma - g.s2) * S0.x - 2.0f * g.af * Dma * S1.x + g.af * g.af * S2.x;
+                                Bqb = (Dmb * Dmb - g.s2) * S0.y - 2.0f * g.af * Dmb * S1.y + g.af * g.af * S2.y;
+                                A2a = -Bqa * g.inv_s2;  // sum g (K + D K') = -Bq / s^2
+                                A2b = -Bqb * g.inv_s2;
+                            }
+                        } else {
+                            // exponential: K_i = min(A C0_i, B C1_i); power law: K = 2^(-nu lg2(D^2+s^2)).
+                            // SX: exp sum t|D|, power law sum t/(D^2+s^2)
+                            const float2 Dm2 = make_float2(Dma, Dmb), af2 = make_float2(g.af, g.af);
+                            float2 Ae = make_float2(0.f, 0.f), Be = Ae;
+                            if constexpr (FAM == KF_EXP) {
+                                const float la = fminf(fmaxf(g.ls * Dma, -100.0f), 100.0f);
+                                const float lb = fminf(fmaxf(g.ls * Dmb, -100.0f), 100.0f);
+                                Ae = make_float2(ex2(-la), ex2(-lb));
+                                Be = make_float2(ex2(la), ex2(lb));
+                            }
+                            float2 SE = make_float2(0.f, 0.f), SD = SE, SX = SE;
+#pragma unroll
+                            for (int i = 0; i < LMAX; ++i) {
+                                const float2 D = __ffma2_rn(make_float2((float)(MA - i), (float)(MA - i)), af2, Dm2);
+                                float2 Kv;
+                                float2 lx;
+                                if constexpr (FAM == KF_EXP) {
+                                    const float2 t1 = __fmul2_rn(Ae, make_float2(ac.C0[i], ac.C0[i]));
+                                    const float2 t2 = __fmul2_rn(Be, make_float2(ac.C1[i], ac.C1[i]));
+                                    Kv = make_float2(fminf(t1.x, t2.x), fminf(t1.y, t2.y));
+                                } else {
+                                    const float2 x = __ffma2_rn(D, D, make_float2(g.s2, g.s2));
+                                    lx = make_float2(lg2(x.x), lg2(x.y));
+                                    Kv = make_float2(ex2(-g.nu * lx.x), ex2(-g.nu * lx.y));
+                                }
+                                float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), Kv);
+                                if (i >= LMIN) {
+                                    t.x = i < pa.L ? t.x : 0.0f;
+                                    t.y = i < pb.L ? t.y : 0.0f;
+                                }
+                                SE = __fadd2_rn(SE, t);
+                                SD = __ffma2_rn(t, D, SD);
+                                if (POSE) {
+                                    if constexpr (FAM == KF_EXP)
+                                        SX = __ffma2_rn(t, make_float2(fabsf(D.x), fabsf(D.y)), SX);
+                                    else
+                                        SX = __ffma2_rn(t, make_float2(ex2(-lx.x), ex2(-lx.y)), SX);
+                                }
+                            }
+                            A1a = SD.x;
+                            A1b = SD.y;
+                            if (POSE) {
+                                if constexpr (FAM == KF_EXP) {
+                                    const float inv_s = g.ls * 0.69314718f;  // K + D K' = K (1 - |D|/s)
+                                    A2a = SE.x - inv_s * SX.x;
+                                    A2b = SE.y - inv_s * SX.y;
+                                } else {  // K + D K' = K (1 - 2 nu D^2/x) = K ((1 - 2 nu) + 2 nu s^2 / x)
+                                    A2a = (1.0f - 2.0f * g.nu) * SE.x + 2.0f * g.nu * g.s2 * SX.x;
+                                    A2b = (1.0f - 2.0f * g.nu) * SE.y + 2.0f * g.nu * g.s2 * SX.y;
+                                }
+                            }
                         }
-                        // A1 = sum g D E = Dm S0 - a S1 ;  Bq = sum g E (D^2 - s^2)
-                        float A1a = __fmaf_rn(-g.af, S1.x, Dma * S0.x), A1b = __fmaf_rn(-g.af, S1.y, Dmb * S0.y);
-                        float Bqa = 0.0f, Bqb = 0.0f;
-                        if (POSE) {
-                            Bqa = (Dma * Dma - g.s2) * S0.x - 2.0f * g.af * Dma * S1.x + g.af * g.af * S2.x;
-                            Bqb = (Dmb * Dmb - g.s2) * S0.y - 2.0f * g.af * Dmb * S1.y + g.af * g.af * S2.y;
-                        }
-                        if (!va) A1a = Bqa = 0.0f;
-                        if (!vb) A1b = Bqb = 0.0f;
+                        if (!va) A1a = A2a = 0.0f;
+                        if (!vb) A1b = A2b = 0.0f;
                         if (ADJ) z = __fmaf_rn(A1b, 0.5f * pb.inv_r, __fmaf_rn(A1a, 0.5f * pa.inv_r, z));
                         if (POSE) {
-                            const float dLa = P * 0.5f * pa.inv_r * (-Bqa * g.inv_s2 - A1a * pa.inv_r);
-                            const float dLb = P * 0.5f * pb.inv_r * (-Bqb * g.inv_s2 - A1b * pb.inv_r);
+                            const float dLa = P * 0.5f * pa.inv_r * (A2a - A1a * pa.inv_r);
+                            const float dLb = P * 0.5f * pb.inv_r * (A2b - A1b * pb.inv_r);
                             const float sca = -dLa * pa.inv_r, scb = -dLb * pb.inv_r;  // x - y_k = -(d + delta)
                             G[q][0] = sca * (sa.dx + ex);
                             G[q][1] = sca * (sa.dy + ey);

@@ -93,8 +93,22 @@ def make_grid(n, pitch):
     return dict(nx=nx, ny=ny, nz=nz, origin=origin, pitch=pitch)
 
 
-def make_acq(nt, sigma, t0=0.0, kappa=KAPPA):
-    return dict(c=C_SOUND, t0=t0, dt=DT, nt=nt, sigma=sigma, kappa=kappa)
+def make_acq(nt, sigma, t0=0.0, kappa=KAPPA, kernel="gauss", nu=0.0):
+    """kernel: family of the designated kernel K (R23) — "gauss" | "exp" | "pow"."""
+    return dict(c=C_SOUND, t0=t0, dt=DT, nt=nt, sigma=sigma, kappa=kappa, kernel=kernel, nu=nu)
+
+
+def family_acq(acq: dict, kernel: str, nu: float = 1.5) -> dict:
+    """The same acquisition with another kernel family (f3, R23), keeping the window kappa s at
+    the Gaussian's 5 sigma: exponential s = sigma/2, kappa = 10 (tail e^-10); power law
+    s = sigma/4, kappa = 20 (tail 20^-2nu)."""
+    if kernel == "gauss":
+        return dict(acq)
+    if kernel == "exp":
+        return dict(acq, kernel="exp", nu=0.0, sigma=acq["sigma"] / 2.0, kappa=10.0)
+    if kernel == "pow":
+        return dict(acq, kernel="pow", nu=float(nu), sigma=acq["sigma"] / 4.0, kappa=20.0)
+    raise ValueError(f"unknown kernel family {kernel}")
 
 
 def _smooth_angles(F, rng, amp_rad, n_terms=3):
