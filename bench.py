@@ -345,17 +345,28 @@ def main():
     k_adj = {"kernel": "k_adjoint (K2, fused adjoint + pose gradient)", "achieved": adj_achieved, "frac": adj_frac,
              "ops_per_update": ops_adj, "ms_per_step": ams}
     dom, other = (k_fwd, k_adj) if fms >= ams else (k_adj, k_fwd)
+    # measured DRAM bytes per launch (ncu, default C4 command; profiles/r1_traffic_c4.json) — only for
+    # the workload it was measured on
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic_c4.json")) as fh:
+            tr = json.load(fh)
+        if args.config == "c4" and args.kernel == "gauss" and Fl == 400:
+            t = tr["k_forward" if dom is k_fwd else "k_adjoint"]
+            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+    except (OSError, KeyError, ValueError):
+        traffic = None
     roofline = {"bound": "alu", "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
-                "unit": fam["unit"], "frac": dom["frac"], "traffic": None,
+                "unit": fam["unit"], "frac": dom["frac"], "traffic": traffic, "traffic_unit": "bytes/launch",
                 "peak_basis": f"148 SM x {fam['pipe']} x sm_max {f_max / 1e6:.0f} MHz (MEASURED_PEAKS.json)",
                 "ops_per_update": dom["ops_per_update"], "kernel_ms_per_step": dom["ms_per_step"],
                 "kernel_share_of_step": dom["ms_per_step"] / ms if ms > 0 else None,
                 "frac_at_measured_clock": (dom["achieved"] * 1e12 / (N_SM * lanes * f_meas)) if (dom["achieved"] and f_meas) else None,
                 "other_kernel": other,
                 "step_frac": (U_local_max * (ops_fwd + ops_adj) / (ms / 1e3) / 1e12) / peak if ms > 0 else None,
-                "traffic_note": "DRAM bytes per launch from ncu --set full on the C4 geometry with 16 frames "
-                                "(profiles/r1_ncu_c4_k_*.md): k_adjoint 89 MB read + 42 MB written, k_forward 257 MB "
-                                "read + 22 MB written; both are ALU-bound (>= 5e4 updates per DRAM byte)"}
+                "traffic_note": "DRAM read+write bytes per launch, ncu on the default C4 command (profiles/r1_traffic_c4.json, "
+                                "r1_launches_c4.md): k_forward 13.7 GB read + 0.8 GB written, k_adjoint 3.7 GB + 1.7 GB per "
+                                "~10.7 s launch = ~0.02% of HBM bandwidth; both kernels are FP32-issue-bound"}
     cpu = None
     if world == 1 and not args.no_cpu:
         v, cores, sample = cpu_oracle_sample(w, p_true.astype(np.float64), w.poses_true())

@@ -9,10 +9,13 @@ rows = list(csv.reader(open(sys.argv[1])))
 i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]
 h = rows[i]
 iN, iV, iU, iG = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit"), h.index("Grid Size")
+iM = h.index("Metric Name")
 scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
 agg = OrderedDict()
 tot = 0.0
 for r in rows[i + 1:]:
+    if r[iM] != "gpu__time_duration.sum":  # other metrics (e.g. DRAM bytes) in the same capture
+        continue
     name = re.sub(r"^void\s+", "", r[iN])
     name = re.sub(r"\(.*$", "", name).replace("<unnamed>::", "")
     v = float(r[iV].replace(",", "")) * scale[r[iU]]
