@@ -27,6 +27,9 @@ constexpr int TX = 8, TY = 8, TZ = 4;  // voxel tile (anchor unit) — 256 voxel
 #ifndef PA_FWD_NV
 #define PA_FWD_NV 4
 #endif
+#ifndef PA_ADJ_HORNER
+#define PA_ADJ_HORNER 1  // adjoint moments by Horner (1) or by the explicit recurrence (0)
+#endif
 constexpr int FWD_WARPS = 4;           // warps per forward CTA
 constexpr int ADJ_THREADS = 256;       // one thread per tile voxel
 
@@ -780,6 +783,45 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                             const float2 um = make_float2(ex2(-g.k2 * Dma * Dma), ex2(-g.k2 * Dmb * Dmb));
                             const float la = 2.0f * g.k2 * g.af * Dma, lb = 2.0f * g.k2 * g.af * Dmb;
                             const float2 pu = make_float2(ex2(la), ex2(lb)), pd = make_float2(ex2(-la), ex2(-lb));
+#if PA_ADJ_HORNER
+                            // Moments S_n = sum_i g_i E_i (i - MA)^n with E_i = um C_i x^|i-MA| (x = pu above
+                            // MA, pd below) are polynomials in x with coefficients c_k = g C: Horner with
+                            // synthetic-division derivatives, b = P(x), d1 = P'(x), d2 = P''(x)/2, from the
+                            // outermost step inwards (3 FFMA2 + 1 FMUL2 per step for two elements):
+                            //   sum c_k x^k = b, sum k c_k x^k = x d1, sum k^2 c_k x^k = x d1 + 2 x^2 d2.
+                            const float2 z2 = make_float2(0.f, 0.f);
+                            float2 bu = z2, d1u = z2, d2u = z2, bd = z2, d1d = z2, d2d = z2;
+#pragma unroll
+                            for (int i = LMAX - 1; i >= MA; --i) {
+                                float2 c = __fmul2_rn(make_float2(gsa[i], gsb[i]), make_float2(ac.C0[i], ac.C0[i]));
+                                if (i >= LMIN) {
+                                    c.x = i < pa.L ? c.x : 0.0f;
+                                    c.y = i < pb.L ? c.y : 0.0f;
+                                }
+                                if (POSE) d2u = __ffma2_rn(d2u, pu, d1u);
+                                d1u = __ffma2_rn(d1u, pu, bu);
+                                bu = __ffma2_rn(bu, pu, c);
+                            }
+#pragma unroll
+                            for (int i = 0; i <= MA; ++i) {  // k = MA - i; the k = 0 step (i = MA) adds 0
+                                const float2 c = i < MA ? __fmul2_rn(make_float2(gsa[i], gsb[i]),
+                                                                     make_float2(ac.C0[i], ac.C0[i]))
+                                                        : z2;
+                                if (POSE) d2d = __ffma2_rn(d2d, pd, d1d);
+                                d1d = __ffma2_rn(d1d, pd, bd);
+                                bd = __ffma2_rn(bd, pd, c);
+                            }
+                            const float2 xu1 = __fmul2_rn(pu, d1u), xd1 = __fmul2_rn(pd, d1d);
+                            const float2 S0 = __fmul2_rn(um, __fadd2_rn(bu, bd));
+                            const float2 S1 = __fmul2_rn(um, make_float2(xu1.x - xd1.x, xu1.y - xd1.y));
+                            float2 S2 = z2;
+                            if (POSE) {
+                                const float2 two = make_float2(2.f, 2.f);
+                                const float2 su = __ffma2_rn(__fmul2_rn(two, __fmul2_rn(pu, pu)), d2u, xu1);
+                                const float2 sd = __ffma2_rn(__fmul2_rn(two, __fmul2_rn(pd, pd)), d2d, xd1);
+                                S2 = __fmul2_rn(um, __fadd2_rn(su, sd));
+                            }
+#else
                             float2 S0 = make_float2(0.f, 0.f), S1 = S0, S2 = S0;  // sum g E k^n, k = i - MA
                             float2 u = um;
 #pragma unroll
@@ -803,6 +845,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                                 if (POSE) S2 = __ffma2_rn(t, make_float2(ac.C2[i], ac.C2[i]), S2);
                                 u = __fmul2_rn(u, pd);
                             }
+#endif
                             // A1 = sum g D E = Dm S0 - a S1 ;  Bq = sum g E (D^2 - s^2)
                             A1a = __fmaf_rn(-g.af, S1.x, Dma * S0.x);
                             A1b = __fmaf_rn(-g.af, S1.y, Dmb * S0.y);
