@@ -6,7 +6,9 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -48,9 +50,49 @@ struct Plan {
     Geo g;
     FwdConst fc;
     AdjConst ac;
+    TayConst tc;     // moment-filter adjoint constants (Gaussian)
+    bool tay_ok;     // Taylor remainder below the bound for this geometry
+    double tay_err;  // host bound on the remainder (relative to sum |terms|)
     int klass;
     int fam;  // pa_kernel (KF_*)
 };
+
+// Series order of the moment-filter adjoint per class (must equal TayCfg<LMIN>::M).
+inline int tay_order(int lmin) { return lmin <= 32 ? 7 : (lmin <= 64 ? 5 : 4); }
+
+// Moment-filter constants (K2a/K2b, pa_kernels.cuh) and the bound on the Taylor remainder of
+// e^{dl k}, |dl| <= (a/s)^2/2 (+2%), relative to sum_k C'_k |k|^n, n = 0..2.
+void make_tay(Plan &pl, int lmin, double a, double sig)
+{
+    const int MA = (lmin + 1) / 2, M = tay_order(lmin), NP = M + 3;
+    const double W = pl.g.ksig_d / a, as2 = a / (sig * sig);
+    const double lam0 = as2 * a * (W - MA - 0.5);
+    std::memset(&pl.tc, 0, sizeof pl.tc);
+    pl.tc.lam0 = (float)lam0;
+    pl.tc.lam_s = (float)as2;
+    const int kt = lmin - MA;
+    pl.tc.Ckt = (float)std::exp(-(double)kt * kt * a * a / (2.0 * sig * sig));
+    for (int m = 0; m < 8; ++m) pl.tc.inv[m] = (float)(1.0 / (m + 1));
+    const double dl = 0.5 * as2 * a * 1.02;
+    double fact = 1.0;
+    for (int i = 2; i <= M + 1; ++i) fact *= i;
+    double worst = 0.0;
+    for (int n = 0; n < 3; ++n) {
+        double num = 0.0, den = 0.0;
+        for (int t = 0; t <= lmin; ++t) {
+            const double k = t - MA;
+            const double cp = std::exp(-k * k * a * a / (2.0 * sig * sig)) * std::exp(lam0 * k);
+            const double x = dl * std::fabs(k);
+            num += cp * std::pow(std::fabs(k), n) * std::pow(x, M + 1) / fact * std::exp(x);
+            den += cp * std::pow(std::fabs(k), n);
+            if (t < lmin && n == 0)
+                for (int p = 0; p < NP; ++p) pl.tc.H[t * NP + p] = (float)(cp * std::pow(k, p));
+        }
+        worst = std::max(worst, num / den);
+    }
+    pl.tay_err = worst;
+    pl.tay_ok = lmin * NP <= 768 && worst <= 4e-7;
+}
 
 pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &pl)
 {
@@ -142,6 +184,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
             }
             pl.fc.I2[k] = make_float2((float)(-2 * k), (float)(-2 * k - 1));
         }
+        make_tay(pl, c.lmin, a, sig);
         for (int i = 0; i < 128; ++i) {
             const double ka = i - g.mA;
             if (pl.fam == PA_KERNEL_EXP) {
@@ -464,6 +507,8 @@ struct pa_ctx {
     int nsm = 148;
     void *ws = nullptr;
     size_t ws_bytes = 0;
+    void *fws = nullptr;  // moment filters of one frame chunk (adjoint K2a -> K2b)
+    size_t fws_bytes = 0;
     unsigned long long *dflag = nullptr;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     bool ev_fwd = false, ev_adj = false;
@@ -483,6 +528,20 @@ struct DevGuard {
         if (prev >= 0) cudaSetDevice(prev);
     }
 };
+
+pa_status fws_reserve(pa_ctx *ctx, size_t bytes)
+{
+    if (bytes <= ctx->fws_bytes) return PA_OK;
+    if (ctx->fws) cudaFree(ctx->fws);
+    ctx->fws = nullptr;
+    ctx->fws_bytes = 0;
+    if (cudaMalloc(&ctx->fws, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PA_ENOMEM, "filter workspace allocation of %zu bytes failed", bytes);
+    }
+    ctx->fws_bytes = bytes;
+    return PA_OK;
+}
 
 pa_status ws_reserve(pa_ctx *ctx, size_t bytes)
 {
@@ -561,10 +620,61 @@ struct AdjLaunch {
     size_t smem = 0;
 };
 
+// Moment-filter adjoint (Gaussian): per frame chunk, K2a (filters, L2-resident) then K2b.
+template <int LMIN, bool POSE, bool ADJ>
+pa_status launch_adjoint_tay(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
+                             const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
+{
+    using T = TayCfg<LMIN>;
+    const int E = pl.g.E, F = pl.g.F, NJ = pl.g.nt + LMIN;
+    const size_t per_frame = (size_t)E * NJ * T::NF * sizeof(float);
+    int Fc = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t(48) << 20) / per_frame));
+    auto smem_of = [&](int fc) {
+        return ((size_t)E * 12 + (size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
+    };
+    while (Fc > 1 && smem_of(Fc) > 113 * 1024) --Fc;
+    Fc = std::min(Fc, std::max(1, 65535 / E));  // K2a grid.y = Fc E
+    Fc = std::min(Fc, F > 0 ? F : 1);
+    const size_t smem = smem_of(Fc);
+    if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "E=%d too large for the adjoint kernel's shared memory", E);
+    auto kern = k_adjoint_tay<LMIN, POSE, ADJ>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
+    if (occ < 1) occ = 1;
+    int P = occ * ctx->nsm;
+    if (P > pl.g.ntiles) P = pl.g.ntiles;
+    L.P = P;
+    L.Fc = Fc;
+    L.smem = smem;
+    if (dry) return PA_OK;
+    pa_status s;
+    if ((s = fws_reserve(ctx, (size_t)Fc * per_frame))) return s;
+    float *Fg = static_cast<float *>(ctx->fws);
+    for (int f0 = 0; f0 < F; f0 += Fc) {
+        const int fn = std::min(Fc, F - f0);
+        k_adj_filter<LMIN><<<dim3((NJ + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.tc, cot, f0, fn, Fg);
+        CUDA_TRY(cudaGetLastError());
+        kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.tc, poses, tmpl, p0, cot, Fg, grad_p0, partial, f0, fn);
+        CUDA_TRY(cudaGetLastError());
+    }
+    return PA_OK;
+}
+
+inline bool adj_direct_forced()
+{
+    const char *e = std::getenv("PA_ADJ_DIRECT");
+    return e != nullptr && e[0] == '1';
+}
+
 template <int LMIN, int SEG, bool POSE, bool ADJ, int FAM>
 pa_status launch_adjoint_t(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
                            const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
 {
+    if constexpr (FAM == KF_GAUSS) {
+        if (pl.tay_ok && !adj_direct_forced())
+            return launch_adjoint_tay<LMIN, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    }
     auto kern = k_adjoint<LMIN, SEG, POSE, ADJ, FAM>;
     const int E = pl.g.E, F = pl.g.F;
     int Fc = POSE ? 64 : F;
@@ -713,6 +823,7 @@ void pa_destroy(pa_ctx *c)
     if (!c) return;
     DevGuard dg(c->device);
     if (c->ws) cudaFree(c->ws);
+    if (c->fws) cudaFree(c->fws);
     if (c->dflag) cudaFree(c->dflag);
     for (int i = 0; i < 3; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);

@@ -976,6 +976,231 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
     }
 }
 
+// ============================================================================================
+// K2 (Gaussian), moment-filter form.  Relative to the voxel's window centre m (index j_m =
+// jlo + MA), D_k = D_m - k a and
+//   E_k = exp(-D_k^2/2s^2) = u_m C_k e^{lam k},   u_m = e^{-D_m^2/2s^2}, C_k = e^{-k^2 a^2/2s^2},
+//   lam = a D_m / s^2.
+// By construction of the window (D at its first sample lies in (kappa s - a, kappa s]) D_m lies
+// within 1.5 samples of zero, so lam stays within +-(a/s)^2/2 of a per-class constant lam0.  With
+// dl = lam - lam0 and C'_k = C_k e^{lam0 k}:
+//   S_n = sum_k g[j_m + k] C_k k^n e^{lam k} = sum_{m=0..M} dl^m/m! F_{n+m}[j_m] (+ remainder),
+//   F_p[j] = sum_{k=-MA}^{LMIN-MA-1} g[j + k] C'_k k^p          (per (frame, element) row)
+// — the exact Taylor series of e^{dl k}, truncated at M where the remainder is below fp32
+// rounding (checked on the host for the actual geometry, else the direct kernel runs).  The
+// window's optional last sample (L = LMIN + 1, k = LMIN - MA) is added directly.  Then
+//   A1 = sum g E D = u_m (D_m S0 - a S1),  Bq = sum g E (D^2 - s^2) = u_m ((D_m^2-s^2) S0 - 2a D_m S1 + a^2 S2)
+// exactly as the direct kernel.  K2a computes F for a frame chunk (L2-resident); K2b replaces the
+// per-voxel L-sample walk by NF/4 128-bit loads and three M-term Horner evaluations.
+// ============================================================================================
+template <int LMIN>
+struct TayCfg {
+    static constexpr int M = LMIN <= 32 ? 7 : (LMIN <= 64 ? 5 : 4);  // series order per class
+    static constexpr int NP = M + 3;                                    // F_0 .. F_{M+2}
+    static constexpr int NF = (NP + 3) & ~3;                            // floats per j (16-B rows)
+};
+
+struct TayConst {
+    float H[768];      // H[t][p] = C'_k k^p, k = t - MA, t in [0, LMIN), p in [0, NP)
+    float lam0;        // series centre (natural units)
+    float lam_s;       // a / s^2: lam = lam_s D_m
+    float Ckt;         // C_k at the extra tap k_t = LMIN - MA
+    float inv[8];      // 1/(m+1)
+};
+
+template <int LMIN>
+__global__ void __launch_bounds__(256) k_adj_filter(Geo g, TayConst tc, const float *__restrict__ cot, int f0, int fn,
+                                                    float *__restrict__ Fg)
+{
+    using T = TayCfg<LMIN>;
+    __shared__ float s[256 + LMIN];
+    const int NJ = g.nt + LMIN;
+    const int row = blockIdx.y;  // chunk-local row (f - f0) E + e
+    const int jj0 = blockIdx.x * 256;
+    const float *gr = cot + ((size_t)f0 * g.E + row) * g.nt;
+    // j_m = jj + MA - LMIN; the taps k in [-MA, LMIN - MA) read samples jj - LMIN + t, t = k + MA
+    for (int t = threadIdx.x; t < 256 + LMIN; t += 256) {
+        const int j = jj0 - LMIN + t;
+        s[t] = (j >= 0 && j < g.nt) ? __ldg(gr + j) : 0.0f;
+    }
+    __syncthreads();
+    const int jj = jj0 + threadIdx.x;
+    if (jj >= NJ) return;
+    float acc[T::NF];
+#pragma unroll
+    for (int p = 0; p < T::NF; ++p) acc[p] = 0.0f;
+#pragma unroll
+    for (int t = 0; t < LMIN; ++t) {
+        const float v = s[threadIdx.x + t];
+#pragma unroll
+        for (int p = 0; p < T::NP; ++p) acc[p] = __fmaf_rn(v, tc.H[t * T::NP + p], acc[p]);
+    }
+    float4 *o = reinterpret_cast<float4 *>(Fg + ((size_t)row * NJ + jj) * T::NF);
+#pragma unroll
+    for (int q = 0; q < T::NF / 4; ++q) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+}
+
+template <int LMIN, bool POSE, bool ADJ>
+__global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay(Geo g, TayConst tc, const float *__restrict__ poses,
+                                                               const float *__restrict__ tmpl,
+                                                               const float *__restrict__ p0,
+                                                               const float *__restrict__ cot,
+                                                               const float *__restrict__ Fg,
+                                                               float *__restrict__ grad_p0,
+                                                               float *__restrict__ partial, int f0, int fn)
+{
+    using T = TayCfg<LMIN>;
+    constexpr int LMAX = LMIN + 1, MA = AdjMid<LMIN>::m, M = T::M, NF = T::NF, KT = LMIN - MA;
+    extern __shared__ float sm[];
+    const int E = g.E, F = g.F, NJ = g.nt + LMIN;
+    AncS *anc = reinterpret_cast<AncS *>(sm);
+    float *wred = reinterpret_cast<float *>(anc + E);  // [8][E][3]
+    float *gacc = wred + (ADJ_THREADS / 32) * E * 3;  // [fn][E][3]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+    const float ex = ((float)lx - 0.5f * (TX - 1)) * g.hf;
+    const float ey = ((float)ly - 0.5f * (TY - 1)) * g.hf;
+    const float ez = ((float)lz - 0.5f * (TZ - 1)) * g.hf;
+    const float e2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+
+    if (POSE) {
+        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS) gacc[q] = 0.0f;
+    }
+    for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+        const int tx = tile % g.ntx, ty = (tile / g.ntx) % g.nty, tz = tile / (g.ntx * g.nty);
+        const int ix = TX * tx + lx, iy = TY * ty + ly, iz = TZ * tz + lz;
+        const bool inside = ix < g.nx && iy < g.ny && iz < g.nz;
+        const size_t kidx = ((size_t)iz * g.ny + iy) * g.nx + ix;
+        const float P = (POSE && inside) ? __ldg(p0 + kidx) : 0.0f;
+        float z = 0.0f;
+        for (int fl = 0; fl < fn; ++fl) {
+            const int f = f0 + fl;
+            __syncthreads();  // previous frame's anchors / wred consumed
+            for (int e = tid; e < E; e += ADJ_THREADS) {
+                double x[3];
+                elem_pos(poses, tmpl, f, e, x);
+                const Anc A = make_anchor(g, x, tx, ty, tz);
+                AncS sa;
+                sa.dx2 = A.dx2; sa.dy2 = A.dy2; sa.dz2 = A.dz2;
+                sa.dx = A.dx; sa.dy = A.dy; sa.dz = A.dz;
+                sa.rho = A.rho; sa.rho2 = A.rho2; sa.CA = A.CA;
+                sa.JA = A.JA; sa.cull = A.cull; sa.jseg = 0;
+                anc[e] = sa;
+            }
+            __syncthreads();
+            const float *Frow = Fg + (size_t)fl * E * NJ * NF;
+            const float *crow = cot + (size_t)f * E * g.nt;
+#pragma unroll 1
+            for (int e0 = 0; e0 < E; e0 += 4) {
+                float G[4][3];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    G[q][0] = G[q][1] = G[q][2] = 0.0f;
+                    const int e = e0 + q;
+                    if (e >= E) continue;  // uniform
+                    const AncS sa = anc[e];
+                    if (sa.cull) continue;  // uniform
+                    Anc Aa;
+                    Aa.dx2 = sa.dx2; Aa.dy2 = sa.dy2; Aa.dz2 = sa.dz2; Aa.dx = sa.dx; Aa.dy = sa.dy; Aa.dz = sa.dz;
+                    Aa.rho = sa.rho; Aa.rho2 = sa.rho2; Aa.CA = sa.CA; Aa.JA = sa.JA; Aa.cull = 0;
+                    const Pair pa = pair<LMIN>(g, Aa, ex, ey, ez, e2);
+                    const bool va = inside && pa.jlo <= g.nt - 1 && pa.jlo + pa.L - 1 >= 0;
+                    const int jj = va ? pa.jlo + LMIN : 0;  // j_m - (MA - LMIN)
+                    const float4 *fp = reinterpret_cast<const float4 *>(Frow + ((size_t)e * NJ + jj) * NF);
+                    float Fv[NF];
+#pragma unroll
+                    for (int r = 0; r < NF / 4; ++r) {
+                        const float4 v = __ldg(fp + r);
+                        Fv[4 * r] = v.x;
+                        Fv[4 * r + 1] = v.y;
+                        Fv[4 * r + 2] = v.z;
+                        Fv[4 * r + 3] = v.w;
+                    }
+                    const float Dm = __fmaf_rn(-(float)(pa.jlo - sa.JA), g.af, __fadd_rn(pa.drel, sa.CA)) - (float)MA * g.af;
+                    const float dl = __fmaf_rn(tc.lam_s, Dm, -tc.lam0);
+                    float qm[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) qm[m] = dl * tc.inv[m];
+                    float S[3];
+#pragma unroll
+                    for (int n = 0; n < (POSE ? 3 : 2); ++n) {
+                        float t = Fv[n + M];
+#pragma unroll
+                        for (int m = M - 1; m >= 0; --m) t = __fmaf_rn(t, qm[m], Fv[n + m]);
+                        S[n] = t;
+                    }
+                    if (!POSE) S[2] = 0.0f;
+                    // the window's optional last sample (k = KT), added directly
+                    const int jx = pa.jlo + LMIN;
+                    const float gx = (va && pa.L == LMAX && jx >= 0 && jx < g.nt) ? __ldg(crow + (size_t)e * g.nt + jx) : 0.0f;
+                    const float w = gx * tc.Ckt * ex2(g.two_a_k2 * Dm * (float)KT);
+                    S[0] = __fmaf_rn(w, 1.0f, S[0]);
+                    S[1] = __fmaf_rn(w, (float)KT, S[1]);
+                    if (POSE) S[2] = __fmaf_rn(w, (float)(KT * KT), S[2]);
+                    const float um = ex2(-g.k2 * Dm * Dm);
+                    float A1 = um * __fmaf_rn(-g.af, S[1], Dm * S[0]);
+                    if (!va) A1 = 0.0f;
+                    if (ADJ) z = __fmaf_rn(A1, 0.5f * pa.inv_r, z);
+                    if (POSE) {
+                        float Bq = um * ((Dm * Dm - g.s2) * S[0] - 2.0f * g.af * Dm * S[1] + g.af * g.af * S[2]);
+                        if (!va) Bq = 0.0f;
+                        const float dL = P * 0.5f * pa.inv_r * (-Bq * g.inv_s2 - A1 * pa.inv_r);
+                        const float sc = -dL * pa.inv_r;  // x - y_k = -(d + delta)
+                        G[q][0] = sc * (sa.dx + ex);
+                        G[q][1] = sc * (sa.dy + ey);
+                        G[q][2] = sc * (sa.dz + ez);
+                    }
+                }
+                if (POSE) {
+                    // transposed warp reduction of 4 elements x 3 components (as k_adjoint)
+                    const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+                    float r6[6];
+#pragma unroll
+                    for (int j = 0; j < 6; ++j) {
+                        const float lo = G[j / 3][j % 3], hi = G[2 + j / 3][j % 3];
+                        const float snd = h16 ? lo : hi, kp = h16 ? hi : lo;
+                        r6[j] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+                    }
+                    float r3[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float lo = r6[c], hi = r6[3 + c];
+                        const float snd = h8 ? lo : hi, kp = h8 ? hi : lo;
+                        r3[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 4);
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 2);
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 1);
+                    }
+                    const int e = e0 + ((lane >> 3) & 3);
+                    if ((lane & 7) == 0 && e < E) {
+                        wred[(warp * E + e) * 3 + 0] = r3[0];
+                        wred[(warp * E + e) * 3 + 1] = r3[1];
+                        wred[(warp * E + e) * 3 + 2] = r3[2];
+                    }
+                }
+            }
+            if (POSE) {
+                __syncthreads();
+                for (int q = tid; q < E * 3; q += ADJ_THREADS) {
+                    float s = 0.0f;
+#pragma unroll
+                    for (int w = 0; w < ADJ_THREADS / 32; ++w) s += wred[w * E * 3 + q];
+                    gacc[fl * E * 3 + q] += s;
+                }
+            }
+        }
+        if (ADJ && inside) grad_p0[kidx] = (f0 == 0 ? 0.0f : grad_p0[kidx]) + z;
+    }
+    if (POSE) {
+        __syncthreads();
+        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS)
+            partial[((size_t)blockIdx.x * F + f0) * E * 3 + q] = gacc[q];
+    }
+}
+
 }  // namespace pa
 
 namespace pa {
