@@ -1040,6 +1040,86 @@ __global__ void __launch_bounds__(256) k_adj_filter(Geo g, TayConst tc, const fl
     for (int q = 0; q < T::NF / 4; ++q) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
 }
 
+// Stage A of the moment-filter adjoint for element e (clamped to E-1; valid = false when
+// e >= E, the element is culled for this tile, the voxel is outside the grid or its window
+// misses [0, nt)): the window, D_m and the NF filter values at j_m.
+template <int NF>
+struct TayA {
+    float Fv[NF];
+    float Dm, inv_r, dx, dy, dz;
+    int jx;     // the window's optional last sample (j_lo + LMIN), or -1
+    int e;
+    bool valid;
+};
+
+template <int LMIN>
+__device__ __forceinline__ TayA<TayCfg<LMIN>::NF> tay_stage_a(const Geo &g, const AncS *anc, int e, int E, bool inside,
+                                                              float ex, float ey, float ez, float e2,
+                                                              const float *__restrict__ Frow, int NJ)
+{
+    constexpr int NF = TayCfg<LMIN>::NF, MA = AdjMid<LMIN>::m;
+    TayA<NF> o;
+    const int ec = min(e, E - 1);
+    const AncS sa = anc[ec];
+    Anc A;
+    A.dx2 = sa.dx2; A.dy2 = sa.dy2; A.dz2 = sa.dz2; A.dx = sa.dx; A.dy = sa.dy; A.dz = sa.dz;
+    A.rho = sa.rho; A.rho2 = sa.rho2; A.CA = sa.CA; A.JA = sa.JA; A.cull = 0;
+    const Pair pa = pair<LMIN>(g, A, ex, ey, ez, e2);
+    o.valid = e < E && !sa.cull && inside && pa.jlo <= g.nt - 1 && pa.jlo + pa.L - 1 >= 0;
+    const int jj = o.valid ? pa.jlo + LMIN : 0;  // j_m - (MA - LMIN)
+    const float4 *fp = reinterpret_cast<const float4 *>(Frow + (size_t)ec * NJ * NF) + jj * (NF / 4);
+#pragma unroll
+    for (int r = 0; r < NF / 4; ++r) {
+        const float4 v = __ldg(fp + r);
+        o.Fv[4 * r] = v.x;
+        o.Fv[4 * r + 1] = v.y;
+        o.Fv[4 * r + 2] = v.z;
+        o.Fv[4 * r + 3] = v.w;
+    }
+    o.Dm = __fmaf_rn(-(float)(pa.jlo - sa.JA), g.af, __fadd_rn(pa.drel, sa.CA)) - (float)MA * g.af;
+    o.inv_r = pa.inv_r;
+    o.dx = sa.dx;
+    o.dy = sa.dy;
+    o.dz = sa.dz;
+    const int jx = pa.jlo + LMIN;
+    o.jx = (o.valid && pa.L == LMIN + 1 && jx >= 0 && jx < g.nt) ? jx : -1;
+    o.e = ec;
+    return o;
+}
+
+// Stage B: S_n = sum_m dl^m/m! F_{n+m} (+ the extra sample), A1 = sum g E D, Bq = sum g E (D^2 - s^2).
+template <int LMIN, bool POSE>
+__device__ __forceinline__ void tay_stage_b(const Geo &g, const TayConst &tc, const TayA<TayCfg<LMIN>::NF> &a,
+                                            const float *__restrict__ crow, float &A1, float &Bq)
+{
+    constexpr int M = TayCfg<LMIN>::M, MA = AdjMid<LMIN>::m, KT = LMIN - MA;
+    const float Dm = a.Dm;
+    const float dl = __fmaf_rn(tc.lam_s, Dm, -tc.lam0);
+    float qm[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) qm[m] = dl * tc.inv[m];
+    float S[3];
+#pragma unroll
+    for (int n = 0; n < (POSE ? 3 : 2); ++n) {
+        float t = a.Fv[n + M];
+#pragma unroll
+        for (int m = M - 1; m >= 0; --m) t = __fmaf_rn(t, qm[m], a.Fv[n + m]);
+        S[n] = t;
+    }
+    const float gx = a.jx >= 0 ? __ldg(crow + (size_t)a.e * g.nt + a.jx) : 0.0f;
+    const float w = gx * tc.Ckt * ex2(g.two_a_k2 * Dm * (float)KT);
+    S[0] += w;
+    S[1] = __fmaf_rn(w, (float)KT, S[1]);
+    const float um = ex2(-g.k2 * Dm * Dm);
+    A1 = a.valid ? um * __fmaf_rn(-g.af, S[1], Dm * S[0]) : 0.0f;
+    Bq = 0.0f;
+    if (POSE) {
+        S[2] = __fmaf_rn(w, (float)(KT * KT), S[2]);
+        const float b = um * ((Dm * Dm - g.s2) * S[0] - 2.0f * g.af * Dm * S[1] + g.af * g.af * S[2]);
+        Bq = a.valid ? b : 0.0f;
+    }
+}
+
 template <int LMIN, bool POSE, bool ADJ>
 __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay(Geo g, TayConst tc, const float *__restrict__ poses,
                                                                const float *__restrict__ tmpl,
@@ -1090,66 +1170,29 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay(Geo g, TayConst 
             __syncthreads();
             const float *Frow = Fg + (size_t)fl * E * NJ * NF;
             const float *crow = cot + (size_t)f * E * g.nt;
+            // two-stage software pipeline over elements: stage A (window, filter loads) of element
+            // e + 1 is issued before stage B (series, gradients) of element e; culled and
+            // out-of-range elements are predicated, not branched, so the loads can be hoisted
+            TayA<NF> cur = tay_stage_a<LMIN>(g, anc, min(0, E - 1), E, inside, ex, ey, ez, e2, Frow, NJ);
 #pragma unroll 1
             for (int e0 = 0; e0 < E; e0 += 4) {
                 float G[4][3];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    G[q][0] = G[q][1] = G[q][2] = 0.0f;
                     const int e = e0 + q;
-                    if (e >= E) continue;  // uniform
-                    const AncS sa = anc[e];
-                    if (sa.cull) continue;  // uniform
-                    Anc Aa;
-                    Aa.dx2 = sa.dx2; Aa.dy2 = sa.dy2; Aa.dz2 = sa.dz2; Aa.dx = sa.dx; Aa.dy = sa.dy; Aa.dz = sa.dz;
-                    Aa.rho = sa.rho; Aa.rho2 = sa.rho2; Aa.CA = sa.CA; Aa.JA = sa.JA; Aa.cull = 0;
-                    const Pair pa = pair<LMIN>(g, Aa, ex, ey, ez, e2);
-                    const bool va = inside && pa.jlo <= g.nt - 1 && pa.jlo + pa.L - 1 >= 0;
-                    const int jj = va ? pa.jlo + LMIN : 0;  // j_m - (MA - LMIN)
-                    const float4 *fp = reinterpret_cast<const float4 *>(Frow + ((size_t)e * NJ + jj) * NF);
-                    float Fv[NF];
-#pragma unroll
-                    for (int r = 0; r < NF / 4; ++r) {
-                        const float4 v = __ldg(fp + r);
-                        Fv[4 * r] = v.x;
-                        Fv[4 * r + 1] = v.y;
-                        Fv[4 * r + 2] = v.z;
-                        Fv[4 * r + 3] = v.w;
-                    }
-                    const float Dm = __fmaf_rn(-(float)(pa.jlo - sa.JA), g.af, __fadd_rn(pa.drel, sa.CA)) - (float)MA * g.af;
-                    const float dl = __fmaf_rn(tc.lam_s, Dm, -tc.lam0);
-                    float qm[M];
-#pragma unroll
-                    for (int m = 0; m < M; ++m) qm[m] = dl * tc.inv[m];
-                    float S[3];
-#pragma unroll
-                    for (int n = 0; n < (POSE ? 3 : 2); ++n) {
-                        float t = Fv[n + M];
-#pragma unroll
-                        for (int m = M - 1; m >= 0; --m) t = __fmaf_rn(t, qm[m], Fv[n + m]);
-                        S[n] = t;
-                    }
-                    if (!POSE) S[2] = 0.0f;
-                    // the window's optional last sample (k = KT), added directly
-                    const int jx = pa.jlo + LMIN;
-                    const float gx = (va && pa.L == LMAX && jx >= 0 && jx < g.nt) ? __ldg(crow + (size_t)e * g.nt + jx) : 0.0f;
-                    const float w = gx * tc.Ckt * ex2(g.two_a_k2 * Dm * (float)KT);
-                    S[0] = __fmaf_rn(w, 1.0f, S[0]);
-                    S[1] = __fmaf_rn(w, (float)KT, S[1]);
-                    if (POSE) S[2] = __fmaf_rn(w, (float)(KT * KT), S[2]);
-                    const float um = ex2(-g.k2 * Dm * Dm);
-                    float A1 = um * __fmaf_rn(-g.af, S[1], Dm * S[0]);
-                    if (!va) A1 = 0.0f;
-                    if (ADJ) z = __fmaf_rn(A1, 0.5f * pa.inv_r, z);
+                    const TayA<NF> nxt = tay_stage_a<LMIN>(g, anc, e + 1, E, inside, ex, ey, ez, e2, Frow, NJ);
+                    float A1, Bq;
+                    tay_stage_b<LMIN, POSE>(g, tc, cur, crow, A1, Bq);
+                    const float ir = cur.inv_r;
+                    if (ADJ) z = __fmaf_rn(A1, 0.5f * ir, z);
                     if (POSE) {
-                        float Bq = um * ((Dm * Dm - g.s2) * S[0] - 2.0f * g.af * Dm * S[1] + g.af * g.af * S[2]);
-                        if (!va) Bq = 0.0f;
-                        const float dL = P * 0.5f * pa.inv_r * (-Bq * g.inv_s2 - A1 * pa.inv_r);
-                        const float sc = -dL * pa.inv_r;  // x - y_k = -(d + delta)
-                        G[q][0] = sc * (sa.dx + ex);
-                        G[q][1] = sc * (sa.dy + ey);
-                        G[q][2] = sc * (sa.dz + ez);
+                        const float dL = P * 0.5f * ir * (-Bq * g.inv_s2 - A1 * ir);
+                        const float sc = -dL * ir;  // x - y_k = -(d + delta)
+                        G[q][0] = sc * (cur.dx + ex);
+                        G[q][1] = sc * (cur.dy + ey);
+                        G[q][2] = sc * (cur.dz + ez);
                     }
+                    cur = nxt;
                 }
                 if (POSE) {
                     // transposed warp reduction of 4 elements x 3 components (as k_adjoint)
