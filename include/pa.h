@@ -92,6 +92,10 @@ const char *pa_last_error(void);
 /* Library version string. */
 const char *pa_version(void);
 
+/* Running count of CUDA kernels this library has enqueued from the calling thread (every
+ * entry point, all streams).  Difference it around a region to count that region's launches. */
+long long pa_launch_count(void);
+
 /*
  * a2 — forward radiation (Eq. gpu_forward_model).
  *   tmpl   [E][3]      array template x^_e

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("PA_LIB_PATH", os.path.join(_HERE, "libpa.so"))
 PA_OK, PA_EINVAL, PA_ESHAPE, PA_EDEGENERATE, PA_ECUDA, PA_ENOMEM, PA_EUNSUPPORTED = range(7)
 _NAMES = {1: "PA_EINVAL", 2: "PA_ESHAPE", 3: "PA_EDEGENERATE", 4: "PA_ECUDA", 5: "PA_ENOMEM", 6: "PA_EUNSUPPORTED"}
 EXPORTS = ("pa_create", "pa_destroy", "pa_last_error", "pa_version", "pa_forward", "pa_adjoint", "pa_pose_grad",
-           "pa_adjoint_pose", "pa_count", "pa_loss", "pa_tgv", "pa_step", "pa_last_kernel_ms")
+           "pa_adjoint_pose", "pa_count", "pa_loss", "pa_tgv", "pa_step", "pa_last_kernel_ms", "pa_launch_count")
 
 
 class PAError(RuntimeError):
@@ -68,8 +68,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             lib.pa_last_error.restype = ctypes.c_char_p
             lib.pa_version.restype = ctypes.c_char_p
             for name in EXPORTS:
-                if name not in ("pa_last_error", "pa_version", "pa_destroy"):
+                if name not in ("pa_last_error", "pa_version", "pa_destroy", "pa_launch_count"):
                     getattr(lib, name).restype = st
+            lib.pa_launch_count.restype = ctypes.c_longlong
+            lib.pa_launch_count.argtypes = []
             lib.pa_create.argtypes = [ctypes.POINTER(vp), ctypes.c_int]
             lib.pa_destroy.argtypes = [vp]
             lib.pa_destroy.restype = None
@@ -269,6 +271,10 @@ class Context:
                                 ctypes.byref(c), cb, None, _f32(grad_p0), _f32(loss), _ptr(grad_euler),
                                 _ptr(row_loss), _ptr(tgv_w), _ptr(adam_w), _stream(stream)))
         return loss
+
+    def launch_count(self):
+        """Running count of kernels libpa enqueued from this thread (pa_launch_count)."""
+        return int(self.lib.pa_launch_count())
 
     def last_kernel_ms(self):
         fw, ad = ctypes.c_float(0), ctypes.c_float(0)

@@ -17,6 +17,7 @@ using namespace pa;
 namespace {
 
 thread_local std::string g_err;
+thread_local long long g_nlaunch = 0;  // kernels enqueued by this thread (pa_launch_count)
 
 pa_status fail(pa_status s, const char *fmt, ...)
 {
@@ -565,6 +566,7 @@ pa_status check_degenerate(pa_ctx *ctx, const Plan &pl, const float *poses, cons
     const unsigned long long init = ~0ull;
     CUDA_TRY(cudaMemcpyAsync(ctx->dflag, &init, sizeof init, cudaMemcpyHostToDevice, st));
     const int n = pl.g.F * pl.g.E;
+    ++g_nlaunch;
     k_check<<<(n + 127) / 128, 128, 0, st>>>(pl.g, poses, tmpl, ctx->dflag);
     CUDA_TRY(cudaGetLastError());
     unsigned long long best = 0;
@@ -589,6 +591,7 @@ pa_status launch_forward_t(const Plan &pl, const float *poses, const float *tmpl
     if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "nt=%d too long for the forward kernel's shared memory", pl.g.nt);
     auto kern = k_forward<LMIN, OMAX, SPAN, FAM>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ++g_nlaunch;
     kern<<<pl.g.F * pl.g.E, FWD_WARPS * 32, smem, st>>>(pl.g, pl.fc, poses, tmpl, p0, out, mode, meas, mask, rowloss);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
@@ -653,8 +656,10 @@ pa_status launch_adjoint_tay(pa_ctx *ctx, const Plan &pl, const float *poses, co
     float *Fg = static_cast<float *>(ctx->fws);
     for (int f0 = 0; f0 < F; f0 += Fc) {
         const int fn = std::min(Fc, F - f0);
+        ++g_nlaunch;
         k_adj_filter<LMIN><<<dim3((NJ + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.tc, cot, f0, fn, Fg);
         CUDA_TRY(cudaGetLastError());
+        ++g_nlaunch;
         kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.tc, poses, tmpl, p0, cot, Fg, grad_p0, partial, f0, fn);
         CUDA_TRY(cudaGetLastError());
     }
@@ -702,6 +707,7 @@ pa_status launch_adjoint_t(pa_ctx *ctx, const Plan &pl, const float *poses, cons
     L.Fc = Fc;
     L.smem = smem;
     if (dry) return PA_OK;
+    ++g_nlaunch;
     kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.ac, poses, tmpl, p0, cot, grad_p0, partial, Fc);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
@@ -758,6 +764,7 @@ pa_status adjoint_pose_core(pa_ctx *ctx, const Plan &pl, const float *tmpl, cons
     if (s) return s;
     CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
     ctx->ev_adj = true;
+    ++g_nlaunch;
     k_pose_reduce<<<pl.g.F, 128, 0, st>>>(partial, L.P, pl.g.F, pl.g.E, tmpl, ge, grad_pose);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
@@ -775,8 +782,10 @@ pa_status launch_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const flo
     t.a0 = a0;
     t.eps = eps;
     dim3 gd((t.nx + TGV_BX - 1) / TGV_BX, (t.ny + TGV_BY - 1) / TGV_BY, (t.nz + TGV_ZS - 1) / TGV_ZS);
+    ++g_nlaunch;
     k_tgv<<<gd, TGV_BX * TGV_BY, 0, st>>>(t, P, w, gP, gw, part);
     CUDA_TRY(cudaGetLastError());
+    ++g_nlaunch;
     k_sum_parts<<<1, 256, 0, st>>>(part, (long long)gd.x * gd.y * gd.z, scale, accumulate, value);
     CUDA_TRY(cudaGetLastError());
     (void)ctx;
@@ -794,6 +803,8 @@ inline size_t tgv_parts(const pa_grid *g)
 extern "C" {
 
 const char *pa_last_error(void) { return g_err.c_str(); }
+
+long long pa_launch_count(void) { return g_nlaunch; }
 
 const char *pa_version(void) { return "libpa 0.2 (sm_100a, fp32 + fp64 anchors; Gaussian/exponential/power-law kernels)"; }
 
@@ -925,6 +936,7 @@ pa_status pa_count(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const fl
     cudaStream_t st = (cudaStream_t)stream;
     if ((s = ws_reserve(ctx, sizeof(long long) * (size_t)F * E))) return s;
     long long *d = static_cast<long long *>(ctx->ws);
+    ++g_nlaunch;
     k_count<<<F * E, 256, 0, st>>>(pl.g, (double)acq->c, (double)acq->t0, (double)acq->dt, (double)acq->kappa,
                                    (double)acq->sigma, poses, tmpl, d);
     CUDA_TRY(cudaGetLastError());
@@ -956,10 +968,12 @@ pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, con
     if ((s = ws_reserve(ctx, sizeof(double) * (size_t)(rows + 1)))) return s;
     double *rl = static_cast<double *>(ctx->ws);
     if (rows > 0) {
+        ++g_nlaunch;
         k_loss_rows<<<(unsigned)rows, 128, 0, st>>>(kind, y, S, row_mask, nt, cot, rl);
         CUDA_TRY(cudaGetLastError());
     }
     if (row_loss && !aligned4(row_loss)) return fail(PA_ESHAPE, "misaligned row_loss");
+    ++g_nlaunch;
     k_rowloss_sum<<<1, 256, 0, st>>>(rl, rows, loss, row_loss);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
@@ -1038,6 +1052,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     double *tg_parts = use_tgv ? reinterpret_cast<double *>(ws + o_tp) : nullptr;
 
     if (F > 0) {
+        ++g_nlaunch;
         k_euler_pose<<<(F + 127) / 128, 128, 0, st>>>(euler_t, F, poses, dR);
         CUDA_TRY(cudaGetLastError());
         if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
@@ -1047,10 +1062,12 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
                                 st)))
             return s;
         ctx->ev_fwd = true;
+        ++g_nlaunch;
         k_rowloss_sum<<<1, 256, 0, st>>>(rl, (long long)F * E, loss, row_loss);
         CUDA_TRY(cudaGetLastError());
         // a4 + a5 + a6 (records ev[1], ev[2])
         if ((s = adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, gpose, nullptr, true, st, ws, off))) return s;
+        ++g_nlaunch;
         k_euler_grad<<<(F + 127) / 128, 128, 0, st>>>(gpose, dR, F, geul);
         CUDA_TRY(cudaGetLastError());
     } else {
@@ -1068,6 +1085,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
         if ((s = launch_tgv(ctx, grid, p0, tgv_w, cfg->tgv_alpha1, cfg->tgv_alpha0, cfg->tgv_eps, tg_p, tg_w, tg_parts,
                             loss + 1, cfg->tgv_lambda, 1, st)))
             return s;
+        ++g_nlaunch;
         k_axpy<<<ctx->nsm * 8, 256, 0, st>>>(grad_p0, tg_p, cfg->tgv_lambda, nvox);
         CUDA_TRY(cudaGetLastError());
     }
@@ -1075,18 +1093,22 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     const double bc1 = 1.0 - std::pow((double)cfg->beta1, cfg->step), bc2 = 1.0 - std::pow((double)cfg->beta2, cfg->step);
     if (cfg->update_p0) {
         int blocks = ctx->nsm * 8;
+        ++g_nlaunch;
         k_adam<<<blocks, 256, 0, st>>>(p0, adam_p0, adam_p0 + nvox, grad_p0, nvox, cfg->lr_p0, cfg->beta1, cfg->beta2,
                                       cfg->eps, (float)bc1, (float)bc2, 1);
         CUDA_TRY(cudaGetLastError());
     }
     if (use_tgv && cfg->update_p0) {  // Adam on the TGV auxiliary field w with lambda * dTGV/dw
         int blocks = ctx->nsm * 8;
+        ++g_nlaunch;
         k_axpy<<<blocks, 256, 0, st>>>(tg_w, tg_w, cfg->tgv_lambda - 1.0f, 3 * nvox);  // tg_w *= lambda
+        ++g_nlaunch;
         k_adam<<<blocks, 256, 0, st>>>(tgv_w, adam_w, adam_w + 3 * nvox, tg_w, 3 * nvox, cfg->lr_p0, cfg->beta1,
                                        cfg->beta2, cfg->eps, (float)bc1, (float)bc2, 0);
         CUDA_TRY(cudaGetLastError());
     }
     if (cfg->update_pose && F > 0) {
+        ++g_nlaunch;
         k_adam_pose<<<(6 * F + 127) / 128, 128, 0, st>>>(euler_t, adam_pose, adam_pose + 6 * F, geul, F, cfg->lr_rot,
                                                          cfg->lr_trans, cfg->beta1, cfg->beta2, cfg->eps, (float)bc1,
                                                          (float)bc2);

@@ -1130,7 +1130,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay(Geo g, TayConst 
                                                                float *__restrict__ partial, int f0, int fn)
 {
     using T = TayCfg<LMIN>;
-    constexpr int LMAX = LMIN + 1, MA = AdjMid<LMIN>::m, M = T::M, NF = T::NF, KT = LMIN - MA;
+    constexpr int NF = T::NF;
     extern __shared__ float sm[];
     const int E = g.E, F = g.F, NJ = g.nt + LMIN;
     AncS *anc = reinterpret_cast<AncS *>(sm);
