@@ -54,6 +54,10 @@ struct Plan {
     TayConst tc;     // moment-filter adjoint constants (Gaussian)
     bool tay_ok;     // Taylor remainder below the bound for this geometry
     double tay_err;  // host bound on the remainder (relative to sum |terms|)
+    DepConst dc;     // deposit-form forward constants (Gaussian)
+    bool dep_ok;     // factorisation error below the bound for this geometry
+    int dep_nw;      // K1d warps per CTA (8: two CTAs per SM; 16: one)
+    double dep_err;  // measured error of the factorisation (relative to max |G|)
     int klass;
     int fam;  // pa_kernel (KF_*)
 };
@@ -93,6 +97,176 @@ void make_tay(Plan &pl, int lmin, double a, double sig)
     }
     pl.tay_err = worst;
     pl.tay_ok = lmin * NP <= 768 && worst <= 4e-7;
+}
+
+// Separable factorisation of the forward pulse for the deposit-form forward K1d (pa_kernels.cuh):
+//   G(t, k) = D_k exp(-D_k^2/2s^2),  D_k = Dc + Dw t - k a,  t in [-1, 1],  k in [-MA, LMIN-MA),
+// ~= sum_{m<R} phi_m(t) psi_m(k).  Chebyshev interpolation of degree 9 in t on 64 nodes, SVD of the
+// (coefficient x tap) matrix by one-sided Jacobi (fp64), phi_m converted to monomials and reduced
+// to 4 coefficients of its parity; the optional last tap (k = LMIN - MA) as a cubic in t.  The
+// error of exactly what the kernel evaluates is measured on a fine grid; > 1e-7 of max|G| (or a
+// geometry outside the class) keeps the direct kernel K1.
+void make_dep(Plan &pl, int lmin, double a, double sig)
+{
+    constexpr int N = 64, DG = 10;  // nodes, Chebyshev coefficients (degree 9)
+    const int R = lmin <= 32 ? 6 : 5;  // == DepRank<LMIN>::R
+    const int MA = (lmin + 1) / 2, KT = lmin - MA, K = lmin;
+    const double ks = pl.g.ksig_d;
+    const double Dlo = ks - (MA + 1) * a, Dhi = ks - MA * a;
+    const double Dc = 0.5 * (Dlo + Dhi), Dw = 0.5 * a * 1.02;
+    DepConst &dc = pl.dc;
+    std::memset(&dc, 0, sizeof dc);
+    pl.dep_ok = false;
+    pl.dep_err = 1.0;
+    pl.dep_nw = 0;
+    if (lmin > 128) return;
+    // warps per CTA: 8 (two CTAs per SM) when two row accumulators fit in shared memory, else 16
+    {
+        const int CS = (R + 2) | 1, CF = R + 1;
+        const size_t sm = (size_t)(CS + CF) * (pl.g.nt + lmin) * 4;
+        const size_t st8 = 8 * 32 * 8 + 4 * (32 + CS) + 64, st16 = 16 * 32 * 8 + 4 * (32 + CS) + 64;  // static smem
+        if (2 * (sm + st8 + 1024) <= 228 * 1024) pl.dep_nw = 8;
+        else if (sm + st16 <= 227 * 1024) pl.dep_nw = 16;
+        else return;
+    }
+    const int NB = pl.dep_nw == 8 ? 19 : 18, NB0 = NB + 10;  // == DepCfg<LMIN, NW>::NB, NB0
+    auto G = [&](double t, int q) {  // tap q in [0, K): k = q - MA
+        const double D = Dc + Dw * t - (double)(q - MA) * a;
+        return D * std::exp(-D * D / (2.0 * sig * sig));
+    };
+    auto GX = [&](double t) {
+        const double D = Dc + Dw * t - (double)KT * a;
+        return D * std::exp(-D * D / (2.0 * sig * sig));
+    };
+    double tn[N];
+    for (int i = 0; i < N; ++i) tn[i] = std::cos(M_PI * (i + 0.5) / N);
+    auto cheb = [](int p, double t) { return std::cos(p * std::acos(std::max(-1.0, std::min(1.0, t)))); };
+    // A = B^T: rows = taps (K), columns = scaled Chebyshev coefficients (DG); w_0 = sqrt(2)
+    std::vector<double> A((size_t)K * DG), V((size_t)DG * DG, 0.0);
+    for (int q = 0; q < K; ++q)
+        for (int p = 0; p < DG; ++p) {
+            double sum = 0.0;
+            for (int i = 0; i < N; ++i) sum += G(tn[i], q) * cheb(p, tn[i]);
+            sum *= (p == 0 ? 1.0 : 2.0) / N;
+            A[(size_t)q * DG + p] = sum * (p == 0 ? std::sqrt(2.0) : 1.0);
+        }
+    for (int p = 0; p < DG; ++p) V[p * DG + p] = 1.0;
+    for (int sweep = 0; sweep < 60; ++sweep) {  // one-sided Jacobi: orthogonalise the columns of A
+        double off = 0.0;
+        for (int p = 0; p < DG; ++p)
+            for (int r = p + 1; r < DG; ++r) {
+                double al = 0, be = 0, ga = 0;
+                for (int q = 0; q < K; ++q) {
+                    const double x = A[(size_t)q * DG + p], y = A[(size_t)q * DG + r];
+                    al += x * x;
+                    be += y * y;
+                    ga += x * y;
+                }
+                if (std::fabs(ga) <= 1e-300 || std::fabs(ga) <= 1e-17 * std::sqrt(al * be)) continue;
+                off = std::max(off, std::fabs(ga) / std::sqrt(al * be));
+                const double ze = (be - al) / (2.0 * ga);
+                const double tt = (ze >= 0 ? 1.0 : -1.0) / (std::fabs(ze) + std::sqrt(1.0 + ze * ze));
+                const double c = 1.0 / std::sqrt(1.0 + tt * tt), sn = c * tt;
+                for (int q = 0; q < K; ++q) {
+                    const double x = A[(size_t)q * DG + p], y = A[(size_t)q * DG + r];
+                    A[(size_t)q * DG + p] = c * x - sn * y;
+                    A[(size_t)q * DG + r] = sn * x + c * y;
+                }
+                for (int q = 0; q < DG; ++q) {
+                    const double x = V[q * DG + p], y = V[q * DG + r];
+                    V[q * DG + p] = c * x - sn * y;
+                    V[q * DG + r] = sn * x + c * y;
+                }
+            }
+        if (off < 1e-15) break;
+    }
+    // singular values, order by size
+    std::vector<double> sv(DG);
+    std::vector<int> ord(DG);
+    for (int p = 0; p < DG; ++p) {
+        double sum = 0;
+        for (int q = 0; q < K; ++q) sum += A[(size_t)q * DG + p] * A[(size_t)q * DG + p];
+        sv[p] = std::sqrt(sum);
+        ord[p] = p;
+    }
+    std::sort(ord.begin(), ord.end(), [&](int x, int y) { return sv[x] > sv[y]; });
+    // monomial coefficients of T_p
+    double Tm[DG][DG] = {};
+    Tm[0][0] = 1.0;
+    Tm[1][1] = 1.0;
+    for (int p = 2; p < DG; ++p)
+        for (int i = 0; i < DG; ++i) Tm[p][i] = (i > 0 ? 2.0 * Tm[p - 1][i - 1] : 0.0) - Tm[p - 2][i];
+    // B = V S U^T  =>  G(t, q) ~ sum_c phi_c(t) psi_c(q),  phi_c = sum_p V[p][c] / w_p T_p,  psi_c = A[:, c] (= U s)
+    double mono[DEP_MAXR][DG] = {}, psi[DEP_MAXR][128] = {};
+    for (int m = 0; m < R; ++m) {
+        const int c = ord[m];
+        for (int p = 0; p < DG; ++p) {
+            const double cp = V[p * DG + c] * (p == 0 ? 1.0 / std::sqrt(2.0) : 1.0);
+            for (int i = 0; i < DG; ++i) mono[m][i] += cp * Tm[p][i];
+        }
+        for (int q = 0; q < K; ++q) psi[m][q] = A[(size_t)q * DG + c];
+    }
+    // reduce each phi_m to its parity (m % 2) and 4 coefficients
+    double cfd[DEP_MAXR + 1][4] = {};
+    for (int m = 0; m < R; ++m)
+        for (int r = 0; r < 4; ++r) {
+            const int i = 2 * r + (m & 1);
+            cfd[m][r] = i < DG ? mono[m][i] : 0.0;
+        }
+    auto phi = [&](int m, double t) {
+        const double s2 = t * t;
+        double v = ((cfd[m][3] * s2 + cfd[m][2]) * s2 + cfd[m][1]) * s2 + cfd[m][0];
+        return (m & 1) ? v * t : v;
+    };
+    // X: cubic fit of GX (Chebyshev, degree 3)
+    {
+        double cx[4] = {};
+        for (int p = 0; p < 4; ++p) {
+            double sum = 0.0;
+            for (int i = 0; i < N; ++i) sum += GX(tn[i]) * cheb(p, tn[i]);
+            cx[p] = sum * (p == 0 ? 1.0 : 2.0) / N;
+        }
+        for (int p = 0; p < 4; ++p)
+            for (int i = 0; i < 4; ++i) cfd[R][i] += cx[p] * Tm[p][i];
+    }
+    auto phix = [&](double t) { return ((cfd[R][3] * t + cfd[R][2]) * t + cfd[R][1]) * t + cfd[R][0]; };
+    // error of the truncated factorisation on a fine grid, relative to max |G|
+    double gmax = 0.0, err = 0.0, pmaxv[DEP_MAXR + 1] = {};
+    for (int it = 0; it <= 2000; ++it) {
+        const double t = -1.0 + 2.0 * it / 2000.0;
+        double ph[DEP_MAXR];
+        for (int m = 0; m < R; ++m) {
+            ph[m] = phi(m, t);
+            pmaxv[m] = std::max(pmaxv[m], std::fabs(ph[m]));
+        }
+        for (int q = 0; q < K; ++q) {
+            const double gv = G(t, q);
+            double ap = 0.0;
+            for (int m = 0; m < R; ++m) ap += ph[m] * psi[m][q];
+            gmax = std::max(gmax, std::fabs(gv));
+            err = std::max(err, std::fabs(gv - ap));
+        }
+        const double xv = phix(t);
+        pmaxv[R] = std::max(pmaxv[R], std::fabs(xv));
+        err = std::max(err, std::fabs(GX(t) - xv));
+    }
+    pl.dep_err = err / gmax;
+    // fixed-point scales: |c| <= 1 (P / Pmax, r_lo / r), |n| <= 2^NB (channel 0: 2^NB0)
+    for (int m = 0; m <= R; ++m) {
+        const double S = std::ldexp(1.0, m == 0 ? NB0 : NB) / (pmaxv[m] * (1.0 + 1e-3) + 1e-300);
+        for (int r = 0; r < 4; ++r) dc.cf[m][r] = (float)(cfd[m][r] * S);
+        dc.dec[m] = (float)(0.5 / S);
+    }
+    // psi[m][q-1] = psi_m(k = OFF - q), tap index OFF - q + MA = LMIN - q
+    for (int m = 0; m < R; ++m)
+        for (int q = 1; q <= lmin; ++q) dc.psi[m][q - 1] = (float)psi[m][lmin - q];
+    // t = (D_m - Dc)/Dw with D_m = drel + CA - clo a - MA a
+    dc.tA = (float)(1.0 / Dw);
+    dc.tB = (float)(a / Dw);
+    dc.tC = (float)((-MA * a - Dc) / Dw);
+    // r_lo(pos) = c t0 + j_m a + (ks - (MA+1) a) - 0.05 a, j_m = pos - OFF
+    dc.W0 = (float)(pl.g.c * pl.g.t0 + ks - (MA + 1) * a - 0.05 * a - (double)KT * a);
+    pl.dep_ok = pl.dep_err <= 1e-7;
 }
 
 pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &pl)
@@ -186,6 +360,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
             pl.fc.I2[k] = make_float2((float)(-2 * k), (float)(-2 * k - 1));
         }
         make_tay(pl, c.lmin, a, sig);
+        make_dep(pl, c.lmin, a, sig);
         for (int i = 0; i < 128; ++i) {
             const double ka = i - g.mA;
             if (pl.fam == PA_KERNEL_EXP) {
@@ -597,6 +772,44 @@ pa_status launch_forward_t(const Plan &pl, const float *poses, const float *tmpl
     return PA_OK;
 }
 
+inline bool fwd_direct_forced()
+{
+    const char *e = std::getenv("PA_FWD_DIRECT");
+    return e != nullptr && e[0] == '1';
+}
+
+// Deposit-form forward (Gaussian): |p0| max (the fixed-point normalisation), then K1d.
+template <int LMIN, int NW>
+pa_status launch_forward_dep(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
+                             float *out, int mode, const float *meas, const uint8_t *mask, double *rowloss,
+                             cudaStream_t st)
+{
+    const size_t smem = DepCfg<LMIN, NW>::smem_bytes(pl.g.nt);
+    auto kern = k_fwd_dep<LMIN, NW>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    unsigned *pm = reinterpret_cast<unsigned *>(ctx->dflag + 1);
+    CUDA_TRY(cudaMemsetAsync(pm, 0, sizeof(unsigned), st));
+    const long long nvox = (long long)pl.g.nx * pl.g.ny * pl.g.nz;
+    ++g_nlaunch;
+    k_absmax<<<ctx->nsm * 4, 256, 0, st>>>(p0, nvox, pm);
+    CUDA_TRY(cudaGetLastError());
+    ++g_nlaunch;
+    kern<<<pl.g.F * pl.g.E, NW * 32, smem, st>>>(pl.g, pl.dc, poses, tmpl, p0, pm, out, mode, meas, mask, rowloss);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+template <int LMIN>
+pa_status launch_forward_dep_c(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
+                               float *out, int mode, const float *meas, const uint8_t *mask, double *rowloss,
+                               cudaStream_t st)
+{
+    if (pl.dep_nw == 8) return launch_forward_dep<LMIN, 8>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    return launch_forward_dep<LMIN, 16>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+}
+
+inline bool use_dep(const Plan &pl) { return pl.fam == KF_GAUSS && pl.dep_ok && pl.dep_nw > 0 && !fwd_direct_forced(); }
+
 template <int FAM>
 pa_status launch_forward_f(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
                            const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
@@ -608,9 +821,16 @@ pa_status launch_forward_f(const Plan &pl, const float *poses, const float *tmpl
     }
 }
 
-pa_status launch_forward(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
-                         const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
+pa_status launch_forward(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out,
+                         int mode, const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
 {
+    if (use_dep(pl)) {
+        switch (pl.klass) {
+        case 0: return launch_forward_dep_c<53>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+        case 1: return launch_forward_dep_c<26>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+        default: return launch_forward_dep_c<106>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+        }
+    }
     switch (pl.fam) {
     case KF_EXP: return launch_forward_f<KF_EXP>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
     case KF_POW: return launch_forward_f<KF_POW>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
@@ -854,7 +1074,7 @@ pa_status pa_forward(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
     cudaStream_t st = (cudaStream_t)stream;
     if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
     CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
-    if ((s = launch_forward(pl, poses, tmpl, p0, traces, FWD_TRACE, nullptr, nullptr, nullptr, st))) return s;
+    if ((s = launch_forward(ctx, pl, poses, tmpl, p0, traces, FWD_TRACE, nullptr, nullptr, nullptr, st))) return s;
     CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
     ctx->ev_fwd = true;
     return PA_OK;
@@ -1058,7 +1278,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
         if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
         // a2 + a3: forward with fused loss/cotangent epilogue
         CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
-        if ((s = launch_forward(pl, poses, tmpl, p0, cot, cfg->loss_kind == 0 ? FWD_MSE : FWD_NC, meas, row_mask, rl,
+        if ((s = launch_forward(ctx, pl, poses, tmpl, p0, cot, cfg->loss_kind == 0 ? FWD_MSE : FWD_NC, meas, row_mask, rl,
                                 st)))
             return s;
         ctx->ev_fwd = true;

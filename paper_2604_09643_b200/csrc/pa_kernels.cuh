@@ -16,6 +16,7 @@
 //     exact transposes of each other up to fp32 rounding (R17).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace pa {
@@ -1242,6 +1243,347 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay(Geo g, TayConst 
         for (int q = tid; q < fn * E * 3; q += ADJ_THREADS)
             partial[((size_t)blockIdx.x * F + f0) * E * 3 + q] = gacc[q];
     }
+}
+
+// ============================================================================================
+// K1d — forward radiation (a2 + fused a3), Gaussian, deposit form.
+//
+// Relative to the pair window centre j_m = jlo + MA, every main tap k in [-MA, LMIN-MA) is in
+// the window for every pair, and the term at sample j_m + k is
+//   c * G(D_m, k),  G(D_m, k) = D_k exp(-D_k^2/2s^2),  D_k = D_m - k a,  c = P/(2r),
+// with D_m confined by the window construction to an interval of width a.  On that interval G
+// has a separable approximation of rank R (host: Chebyshev fit + one-sided Jacobi SVD, error
+// checked on a fine grid):
+//   G(D_m, k) ~= sum_{m<R} phi_m(t) psi_m(k),   t = (D_m - Dc)/Dw in [-1, 1],
+// phi_m a polynomial of parity m (4 coefficients in t^2).  So a pair deposits R numbers
+// c phi_m(t) at ONE position pos = j_m + OFF of a per-row channel accumulator, plus the exact
+// optional last tap (L = LMIN + 1) in channel X, and the trace is, once per row,
+//   y[j] = sum_{q=1..LMIN} sum_m Q_m[j + q] psi_m(OFF - q) + Q_X[j].
+// Deposits are fixed-point integers (red.shared.add: integer addition is associative, so the
+// result is deterministic): per-position scale r_lo(pos) <= r removes 1/r, 1/Pmax normalises P,
+// and per-channel scales bound |n| <= 2^NB (channel 0 in two words, hi 2^10 + lo).  A round =
+// one 8x8x4 tile per warp; after each round the touched range is flushed into fp32 accumulators
+// in a fixed order.  Layout [pos][channel] with an odd stride: the R + 2 words of a deposit are
+// immediate offsets of one address, and 32 lanes at distinct positions hit distinct banks.
+// ============================================================================================
+constexpr int DEP_MAXR = 6;
+
+// rank per window class: the factorisation error is <= ~2e-8 (L_min 53), 5e-9 (26, rank 6),
+// 6e-10 (106) of max|G|
+template <int LMIN>
+struct DepRank {
+    static constexpr int R = LMIN <= 32 ? 6 : 5;
+};
+
+struct DepConst {
+    float psi[DEP_MAXR][128];  // psi[m][q-1] = psi_m(k = OFF - q), q in [1, LMIN]
+    float cf[DEP_MAXR + 1][4]; // phi_m(t) = t^(m%2) (cf0 + s cf1 + s^2 cf2 + s^3 cf3), s = t^2, scaled by S_m;
+                               // X (index R): cf0 + t cf1 + t^2 cf2 + t^3 cf3, scaled by S_X
+    float dec[DEP_MAXR + 1];   // 0.5 / S_m  (x Pmax / r_lo at decode)
+    float tA, tB;              // t = tA * bse - clo * tB + tC   (= (D_m - Dc) / Dw)
+    float tC;
+    float W0;                  // r_lo(pos) = max(r_min, pos * a + W0) <= r of every pair depositing at pos
+};
+
+template <int LMIN, int NW>
+struct DepCfg {
+    static constexpr int R = DepRank<LMIN>::R;
+    static constexpr int NQ = R + 2;              // int words per position: R channels, X, low word of channel 0
+    static constexpr int CS = NQ | 1;             // odd stride
+    static constexpr int CF = R + 1;              // fp32 words per position
+    static constexpr int NB = NW == 8 ? 19 : 18;  // a round adds <= 256 NW deposits per word
+    static constexpr int NB0 = NB + 10;           // channel 0: hi (<= 2^NB) * 2^10 + lo
+    static __host__ __device__ int njp(int nt) { return nt + LMIN; }
+    static __host__ __device__ size_t smem_bytes(int nt) { return (size_t)(CS + CF) * njp(nt) * 4; }
+};
+
+// Row epilogue shared by the forward kernels: y (shared memory, nt floats) -> trace, or the MSE / NC
+// cotangent and row loss (a3; Eq. 2, Eq. 3; mask Eq. 4).
+__device__ __forceinline__ void fwd_epilogue(const Geo &g, const float *y, int fe, float *__restrict__ out, int mode,
+                                             const float *__restrict__ meas, const uint8_t *__restrict__ row_mask,
+                                             double *__restrict__ rowloss, double *red)
+{
+    const int nt = g.nt;
+    const size_t rowoff = (size_t)fe * nt;
+    if (mode == FWD_TRACE) {
+        for (int j = threadIdx.x; j < nt; j += blockDim.x) out[rowoff + j] = y[j];
+        return;
+    }
+    const bool masked = row_mask != nullptr && row_mask[fe] == 0;
+    const float *S = meas + rowoff;
+    if (mode == FWD_MSE) {
+        double part = 0.0;
+        for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+            const float d = y[j] - __ldg(S + j);
+            part += (double)d * (double)d;
+            out[rowoff + j] = masked ? 0.0f : 2.0f * d;
+        }
+        const double tot = block_sum(part, red);
+        if (threadIdx.x == 0) rowloss[fe] = masked ? 0.0 : tot;
+        return;
+    }
+    double sy = 0.0, ss = 0.0;
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        sy += y[j];
+        ss += __ldg(S + j);
+    }
+    const double my = block_sum(sy, red) / nt, ms = block_sum(ss, red) / nt;
+    double cv = 0.0, vy = 0.0, vs = 0.0;
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        const double a = y[j] - my, b = (double)__ldg(S + j) - ms;
+        cv += a * b;
+        vy += a * a;
+        vs += b * b;
+    }
+    const double COV = block_sum(cv, red) / nt, VY = block_sum(vy, red) / nt, VS = block_sum(vs, red) / nt;
+    const double sdy = sqrt(VY), sds = sqrt(VS);
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+        const double gj = -(((double)__ldg(S + j) - ms) / (sdy * sds) - COV * (y[j] - my) / (sdy * sdy * sdy * sds)) / nt;
+        out[rowoff + j] = masked ? 0.0f : (float)gj;
+    }
+    if (threadIdx.x == 0) rowloss[fe] = masked ? 0.0 : -COV / (sdy * sds);
+}
+
+// ceil(x) for |x| < 2^22 on the FP32 pipe (round-to-nearest by the 1.5*2^23 shifter, then +1 when
+// below x): bit-identical to ceilf, without the FRND/F2I conversion unit.
+__device__ __forceinline__ float ceil_alu(float x, int &xi)
+{
+    const float sh = __fadd_rn(x, 12582912.0f);
+    float r = __fsub_rn(sh, 12582912.0f);
+    int ri = __float_as_int(sh) - 0x4B400000;
+    const bool up = r < x;
+    r = up ? __fadd_rn(r, 1.0f) : r;
+    xi = up ? ri + 1 : ri;
+    return r;
+}
+
+// Unpredicated shared-memory integer add (ATOMS.ADD, no return value) at addr + OFF: a predicated
+// red is turned into a branch per atomic by ptxas, so lanes without a deposit add 0 to a per-lane
+// dummy word instead.
+template <int OFF>
+__device__ __forceinline__ void red_s32(unsigned addr, int v)
+{
+    asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
+}
+
+template <int LMIN, int NW>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, DepConst dc, const float *__restrict__ poses,
+                                                                       const float *__restrict__ tmpl,
+                                                                       const float *__restrict__ p0,
+                                                                       const unsigned *__restrict__ pmax_bits,
+                                                                       float *__restrict__ out, int mode,
+                                                                       const float *__restrict__ meas,
+                                                                       const uint8_t *__restrict__ row_mask,
+                                                                       double *__restrict__ rowloss)
+{
+    using C = DepCfg<LMIN, NW>;
+    constexpr int R = C::R, CS = C::CS, CF = C::CF, NQ = C::NQ;
+    extern __shared__ int smi[];
+    const int NJ = C::njp(g.nt);
+    int *Qi = smi;                                         // [NJ][CS] fixed-point round accumulators
+    float *Qf = reinterpret_cast<float *>(smi + CS * NJ);  // [NJ][CF] fp32 row accumulators
+    __shared__ int rng[2][2];
+    __shared__ double red[NW * 32];
+    __shared__ int dummy[32 + DepCfg<LMIN, NW>::CS];  // target of lanes without a deposit (adds 0)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < (CS + CF) * NJ; i += blockDim.x) smi[i] = 0;
+    if (tid < 2) {
+        rng[tid][0] = 0x7fffffff;
+        rng[tid][1] = -1;
+    }
+    const int fe = blockIdx.x;
+    const int f = fe / g.E, e = fe - f * g.E;
+    double x[3];
+    elem_pos(poses, tmpl, f, e, x);
+    // r_min: distance from the element to the nearest voxel centre (nearest lattice point, clamped)
+    float rmin;
+    {
+        const double o[3] = {g.ox, g.oy, g.oz};
+        const int n[3] = {g.nx, g.ny, g.nz};
+        double d2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            double i = rint((x[q] - o[q]) / g.h);
+            i = i < 0.0 ? 0.0 : (i > n[q] - 1 ? (double)(n[q] - 1) : i);
+            const double d = x[q] - (o[q] + g.h * i);
+            d2 += d * d;
+        }
+        rmin = (float)(sqrt(d2) * (1.0 - 1e-6));
+    }
+    const float pm = __uint_as_float(__ldg(pmax_bits));
+    const float invP = pm > 0.0f ? 1.0f / pm : 0.0f;
+    const int cx = lane & 3, cy = (lane >> 2) & 3, cz = lane >> 4;
+    // rounds: NW tiles in a 2 x 2 x (NW/4) tile block, x fastest
+    constexpr int BZ = NW / 4;
+    const int nbx = (g.ntx + 1) >> 1, nby = (g.nty + 1) >> 1, nbz = (g.ntz + BZ - 1) / BZ;
+    const int nb = nbx * nby * nbz;
+    const int spanlo = (int)floorf((-g.rt - g.ksig) * g.inv_a) - 2, spanhi = (int)ceilf((g.rt - g.ksig) * g.inv_a) + 3;
+    const unsigned qbase = (unsigned)__cvta_generic_to_shared(Qi);
+    const unsigned dbase = (unsigned)__cvta_generic_to_shared(dummy) + 4u * lane;
+    __syncthreads();
+
+    auto tile_of = [&](int b, int &tx, int &ty, int &tz) {
+        const int bx = b % nbx, byz = b / nbx, by = byz % nby, bz = byz / nby;
+        tx = 2 * bx + (warp & 1);
+        ty = 2 * by + ((warp >> 1) & 1);
+        tz = BZ * bz + (warp >> 2);
+        return tx < g.ntx && ty < g.nty && tz < g.ntz;
+    };
+    const size_t sy = (size_t)g.nx, sz = (size_t)g.nx * g.ny;
+    // the lane's 2x2x2 voxel amplitudes of a tile (0 outside the grid)
+    auto load_p = [&](int tx, int ty, int tz, bool ok, float P[8]) {
+        const int ix0 = TX * tx + 2 * cx, iy0 = TY * ty + 2 * cy, iz0 = TZ * tz + 2 * cz;
+        const float *pb = p0 + ((size_t)iz0 * g.ny + iy0) * g.nx + ix0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+            const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
+            const bool in = ok && ix0 + vx < g.nx && iy0 + vy < g.ny && iz0 + vz < g.nz;
+            P[v] = in ? __ldg(pb + vx + vy * sy + vz * sz) : 0.0f;
+        }
+    };
+    int ntx_, nty_, ntz_;
+    bool nok = nb > 0 && tile_of(0, ntx_, nty_, ntz_);
+    float Pn[8];
+    load_p(ntx_, nty_, ntz_, nok, Pn);
+    for (int b = 0; b < nb; ++b) {
+        const int tx = ntx_, ty = nty_, tz = ntz_;
+        const bool tok = nok;
+        float P[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) P[v] = Pn[v];
+        // software pipeline: the next round's amplitudes are in flight during this round
+        nok = b + 1 < nb && tile_of(b + 1, ntx_, nty_, ntz_);
+        load_p(ntx_, nty_, ntz_, nok, Pn);
+        if (tok) {
+            const Anc A = make_anchor(g, x, tx, ty, tz);
+            if (!A.cull) {
+                const int base = A.JA + LMIN + (int)floorf(A.CA * g.inv_a);
+                if (lane == 0) {
+                    atomicMin(&rng[b & 1][0], max(base + spanlo, 0));
+                    atomicMax(&rng[b & 1][1], min(base + spanhi, NJ - 1));
+                }
+                const float ex0 = ((float)(2 * cx) - 0.5f * (TX - 1)) * g.hf;
+                const float ey0 = ((float)(2 * cy) - 0.5f * (TY - 1)) * g.hf;
+                const float ez0 = ((float)(2 * cz) - 0.5f * (TZ - 1)) * g.hf;
+                const float posA = (float)(A.JA + LMIN);
+                const float tCA = __fmaf_rn(A.CA, dc.tA, dc.tC);
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
+                    const float Pv = P[v];
+                    const float ex = ex0 + (float)vx * g.hf, ey = ey0 + (float)vy * g.hf, ez = ez0 + (float)vz * g.hf;
+                    const float e2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                    // the pair window, exactly as pair<LMIN>() (R17), with ceil/floor on the FP32 pipe
+                    const float num = __fmaf_rn(A.dx2, ex, __fmaf_rn(A.dy2, ey, __fmaf_rn(A.dz2, ez, e2)));
+                    const float r2 = __fadd_rn(A.rho2, num);
+                    const float inv_r = rsqrtf(r2);
+                    const float r = __fmul_rn(r2, inv_r);
+                    const float drel = __fdividef(num, __fadd_rn(r, A.rho));
+                    const float bse = __fadd_rn(drel, A.CA);
+                    const float xlo = __fmul_rn(__fsub_rn(bse, g.ksig), g.inv_a);
+                    const float xhi = __fmul_rn(__fadd_rn(bse, g.ksig), g.inv_a);
+                    int clo;
+                    const float clof = ceil_alu(xlo, clo);
+                    const bool Lx = xhi >= __fadd_rn(clof, (float)LMIN);  // floor(xhi) - clo + 1 >= LMIN + 1
+                    const int pos = A.JA + LMIN + clo;                    // j_m + OFF = jlo + LMIN
+                    const bool valid = Pv != 0.0f && pos >= 0 && pos < NJ;
+                    // t = (D_m - Dc)/Dw, D_m = bse - clo a - MA a
+                    const float t = __fmaf_rn(-clof, dc.tB, __fmaf_rn(drel, dc.tA, tCA));
+                    const float s = t * t;
+                    const float rlo = fmaxf(rmin, __fmaf_rn(__fadd_rn(clof, posA), g.af, dc.W0));
+                    const float ct = valid ? Pv * invP * rlo * inv_r : 0.0f;
+                    // c t^i s^k products shared by all channels
+                    const float c1 = ct * s, c2 = c1 * s, c3 = c2 * s;       // even channels
+                    const float o0 = ct * t, o1 = o0 * s, o2 = o1 * s, o3 = o2 * s;  // odd channels
+                    // ct = 0 (all words 0) for a lane without a deposit; it adds to its dummy words
+                    const unsigned sa = valid ? qbase + (unsigned)pos * (CS * 4) : dbase;
+                    auto chan = [&](auto mc) {
+                        constexpr int m = decltype(mc)::value;
+                        const float a0 = (m & 1) ? o0 : ct, a1 = (m & 1) ? o1 : c1, a2 = (m & 1) ? o2 : c2,
+                                    a3 = (m & 1) ? o3 : c3;
+                        const float xm = __fmaf_rn(a3, dc.cf[m][3], __fmaf_rn(a2, dc.cf[m][2], __fmaf_rn(a1, dc.cf[m][1], a0 * dc.cf[m][0])));
+                        if constexpr (m == 0) {
+                            // two words: |x| <= 2^NB0 = hi 2^10 + lo, quantum far below fp32 rounding
+                            const float hs = __fmaf_rn(xm, 1.0f / 1024.0f, 12582912.0f);
+                            const float hf = __fsub_rn(hs, 12582912.0f);
+                            const int nh = __float_as_int(hs) - 0x4B400000;
+                            const int nl = __float_as_int(__fadd_rn(__fmaf_rn(-hf, 1024.0f, xm), 12582912.0f)) - 0x4B400000;
+                            red_s32<0>(sa, nh);
+                            red_s32<4 * (R + 1)>(sa, nl);
+                        } else {
+                            red_s32<4 * m>(sa, __float_as_int(__fadd_rn(xm, 12582912.0f)) - 0x4B400000);
+                        }
+                    };
+                    chan(std::integral_constant<int, 0>{});
+                    chan(std::integral_constant<int, 1>{});
+                    chan(std::integral_constant<int, 2>{});
+                    chan(std::integral_constant<int, 3>{});
+                    chan(std::integral_constant<int, 4>{});
+                    if constexpr (R > 5) chan(std::integral_constant<int, 5>{});
+                    static_assert(R == 5 || R == 6, "rank 5 or 6");
+                    {  // X: the optional last tap (L = LMIN + 1), a cubic in t
+                        const float xm = __fmaf_rn(o1, dc.cf[R][3], __fmaf_rn(c1, dc.cf[R][2], __fmaf_rn(o0, dc.cf[R][1], ct * dc.cf[R][0])));
+                        const int n = __float_as_int(__fadd_rn(xm, 12582912.0f)) - 0x4B400000;
+                        red_s32<4 * R>(sa, Lx ? n : 0);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        {
+            const int lo = rng[b & 1][0], hi = rng[b & 1][1];  // lo > hi when every tile was culled
+            for (int p = (lo <= hi ? lo : hi + 1) + tid; p <= hi; p += blockDim.x) {
+                int *qi = Qi + p * CS;
+                float *qf = Qf + p * CF;
+                int n[NQ];
+#pragma unroll
+                for (int c = 0; c < NQ; ++c) n[c] = qi[c];
+                qf[0] += __fmaf_rn((float)n[0], 1024.0f, (float)n[R + 1]);
+#pragma unroll
+                for (int c = 1; c <= R; ++c) qf[c] += (float)n[c];
+#pragma unroll
+                for (int c = 0; c < NQ; ++c) qi[c] = 0;
+            }
+            if (tid < 1) {
+                rng[(b + 1) & 1][0] = 0x7fffffff;
+                rng[(b + 1) & 1][1] = -1;
+            }
+        }
+        __syncthreads();
+    }
+    // decode: Q_m[pos] = Qf * (0.5 / S_m) * Pmax / r_lo(pos)
+    for (int p = tid; p < NJ; p += blockDim.x) {
+        const float rr = pm / fmaxf(rmin, __fmaf_rn((float)p, g.af, dc.W0));
+#pragma unroll
+        for (int m = 0; m < CF; ++m) Qf[p * CF + m] *= dc.dec[m] * rr;
+    }
+    __syncthreads();
+    float *y = reinterpret_cast<float *>(Qi);  // the round accumulators are free now
+    for (int j = tid; j < g.nt; j += blockDim.x) {
+        float acc = Qf[j * CF + R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const float *qm = Qf + j * CF + m;
+            float am = 0.0f;
+#pragma unroll 8
+            for (int q = 1; q <= LMIN; ++q) am = __fmaf_rn(qm[q * CF], dc.psi[m][q - 1], am);
+            acc += am;
+        }
+        y[j] = acc;
+    }
+    __syncthreads();
+    fwd_epilogue(g, y, fe, out, mode, meas, row_mask, rowloss, red);
+}
+
+// max |p0| as float bits (non-negative floats order like unsigned integers): the 1/Pmax
+// normalisation of the fixed-point deposits of K1d.
+__global__ void k_absmax(const float *__restrict__ p, long long n, unsigned *__restrict__ out)
+{
+    unsigned m = 0u;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        m = max(m, __float_as_uint(fabsf(__ldg(p + i))));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 }  // namespace pa
