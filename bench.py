@@ -341,20 +341,24 @@ def main():
     fwd_frac = fwd_achieved / peak if fwd_achieved else None
     adj_frac = adj_achieved / peak if adj_achieved else None
     f_meas = clocks["sm_mhz"] * 1e6 if clocks.get("sm_mhz") else None
-    k_fwd = {"kernel": "k_forward (K1, forward + fused loss/cotangent)", "achieved": fwd_achieved, "frac": fwd_frac,
-             "ops_per_update": ops_fwd, "ms_per_step": fms}
-    k_adj = {"kernel": "k_adjoint (K2, fused adjoint + pose gradient)", "achieved": adj_achieved, "frac": adj_frac,
-             "ops_per_update": ops_adj, "ms_per_step": ams}
+    gauss = args.kernel == "gauss"
+    fwd_name = ("k_fwd_dep (K1d, deposit-form forward + fused loss/cotangent)" if gauss
+                else "k_forward (K1, direct forward + fused loss/cotangent)")
+    adj_name = ("k_adj_filter + k_adjoint_tay (K2a/K2b, moment-filter adjoint + pose gradient)" if gauss
+                else "k_adjoint (K2, direct adjoint + pose gradient)")
+    k_fwd = {"kernel": fwd_name, "achieved": fwd_achieved, "frac": fwd_frac, "ops_per_update": ops_fwd, "ms_per_step": fms}
+    k_adj = {"kernel": adj_name, "achieved": adj_achieved, "frac": adj_frac, "ops_per_update": ops_adj, "ms_per_step": ams}
     dom, other = (k_fwd, k_adj) if fms >= ams else (k_adj, k_fwd)
     # measured DRAM bytes per launch (ncu, default C4 command; profiles/r1_traffic_c4.json) — only for
     # the workload it was measured on
-    traffic = None
+    traffic, traffic_note = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "r1_traffic_c4.json")) as fh:
             tr = json.load(fh)
-        if args.config == "c4" and args.kernel == "gauss" and Fl == 400:
-            t = tr["k_forward" if dom is k_fwd else "k_adjoint"]
+        if args.config == "c4" and gauss and Fl == 400:
+            t = tr["forward" if dom is k_fwd else "adjoint"]
             traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+            traffic_note = tr.get("note")
     except (OSError, KeyError, ValueError):
         traffic = None
     roofline = {"bound": "alu", "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
@@ -365,9 +369,7 @@ def main():
                 "frac_at_measured_clock": (dom["achieved"] * 1e12 / (N_SM * lanes * f_meas)) if (dom["achieved"] and f_meas) else None,
                 "other_kernel": other,
                 "step_frac": (U_local_max * (ops_fwd + ops_adj) / (ms / 1e3) / 1e12) / peak if ms > 0 else None,
-                "traffic_note": "DRAM read+write bytes per launch, ncu on the default C4 command (profiles/r1_traffic_c4.json, "
-                                "r1_launches_c4.md): k_forward 13.7 GB read + 0.8 GB written, k_adjoint 3.7 GB + 1.7 GB per "
-                                "~10.7 s launch = ~0.02% of HBM bandwidth; both kernels are FP32-issue-bound"}
+                "traffic_note": traffic_note}
     cpu = None
     if world == 1 and not args.no_cpu:
         v, cores, sample = cpu_oracle_sample(w, p_true.astype(np.float64), w.poses_true())

@@ -129,7 +129,7 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
         else if (sm + st16 <= 227 * 1024) pl.dep_nw = 16;
         else return;
     }
-    const int NB = pl.dep_nw == 8 ? 19 : 18, NB0 = NB + 10;  // == DepCfg<LMIN, NW>::NB, NB0
+    const int NB = dep_nb(pl.dep_nw), NB0 = NB + 10;  // == DepCfg<LMIN, NW>::NB, NB0
     auto G = [&](double t, int q) {  // tap q in [0, K): k = q - MA
         const double D = Dc + Dw * t - (double)(q - MA) * a;
         return D * std::exp(-D * D / (2.0 * sig * sig));
@@ -254,7 +254,7 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     // fixed-point scales: |c| <= 1 (P / Pmax, r_lo / r), |n| <= 2^NB (channel 0: 2^NB0)
     for (int m = 0; m <= R; ++m) {
         const double S = std::ldexp(1.0, m == 0 ? NB0 : NB) / (pmaxv[m] * (1.0 + 1e-3) + 1e-300);
-        for (int r = 0; r < 4; ++r) dc.cf[m][r] = (float)(cfd[m][r] * S);
+        for (int r = 0; r < 4; ++r) dc.cf2[m][r] = make_float2((float)(cfd[m][r] * S), (float)(cfd[m][r] * S));
         dc.dec[m] = (float)(0.5 / S);
     }
     // psi[m][q-1] = psi_m(k = OFF - q), tap index OFF - q + MA = LMIN - q
@@ -874,14 +874,44 @@ pa_status launch_adjoint_tay(pa_ctx *ctx, const Plan &pl, const float *poses, co
     pa_status s;
     if ((s = fws_reserve(ctx, (size_t)Fc * per_frame))) return s;
     float *Fg = static_cast<float *>(ctx->fws);
+    // PA_DEBUG_CHUNKS=1: per-kernel device time of the chunk loop on stderr (diagnostic)
+    const char *dbg = std::getenv("PA_DEBUG_CHUNKS");
+    std::vector<cudaEvent_t> evs;
     for (int f0 = 0; f0 < F; f0 += Fc) {
         const int fn = std::min(Fc, F - f0);
+        if (dbg) {
+            evs.emplace_back();
+            cudaEventCreate(&evs.back());
+            cudaEventRecord(evs.back(), st);
+        }
         ++g_nlaunch;
         k_adj_filter<LMIN><<<dim3((NJ + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.tc, cot, f0, fn, Fg);
         CUDA_TRY(cudaGetLastError());
+        if (dbg) {
+            evs.emplace_back();
+            cudaEventCreate(&evs.back());
+            cudaEventRecord(evs.back(), st);
+        }
         ++g_nlaunch;
         kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.tc, poses, tmpl, p0, cot, Fg, grad_p0, partial, f0, fn);
         CUDA_TRY(cudaGetLastError());
+    }
+    if (dbg) {
+        evs.emplace_back();
+        cudaEventCreate(&evs.back());
+        cudaEventRecord(evs.back(), st);
+        cudaEventSynchronize(evs.back());
+        double ta = 0, tb = 0;
+        for (size_t i = 0; i + 2 < evs.size() + 1 && i + 1 < evs.size(); i += 2) {
+            float x = 0, y = 0;
+            cudaEventElapsedTime(&x, evs[i], evs[i + 1]);
+            if (i + 2 < evs.size()) cudaEventElapsedTime(&y, evs[i + 1], evs[i + 2]);
+            ta += x;
+            tb += y;
+        }
+        std::fprintf(stderr, "[pa] adjoint chunks=%zu Fc=%d P=%d smem=%zu: K2a %.3f ms, K2b %.3f ms\n", evs.size() / 2, Fc, P,
+                     smem, ta, tb);
+        for (auto e : evs) cudaEventDestroy(e);
     }
     return PA_OK;
 }

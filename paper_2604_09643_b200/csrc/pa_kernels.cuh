@@ -1277,13 +1277,20 @@ struct DepRank {
 
 struct DepConst {
     float psi[DEP_MAXR][128];  // psi[m][q-1] = psi_m(k = OFF - q), q in [1, LMIN]
-    float cf[DEP_MAXR + 1][4]; // phi_m(t) = t^(m%2) (cf0 + s cf1 + s^2 cf2 + s^3 cf3), s = t^2, scaled by S_m;
-                               // X (index R): cf0 + t cf1 + t^2 cf2 + t^3 cf3, scaled by S_X
+    float2 cf2[DEP_MAXR + 1][4]; // (c, c): phi_m(t) = t^(m%2) (c0 + s c1 + s^2 c2 + s^3 c3), s = t^2, scaled by S_m;
+                                 // X (index R): c0 + t c1 + t^2 c2 + t^3 c3, scaled by S_X
     float dec[DEP_MAXR + 1];   // 0.5 / S_m  (x Pmax / r_lo at decode)
     float tA, tB;              // t = tA * bse - clo * tB + tC   (= (D_m - Dc) / Dw)
     float tC;
     float W0;                  // r_lo(pos) = max(r_min, pos * a + W0) <= r of every pair depositing at pos
 };
+
+#ifndef PA_DEP_TPR
+#define PA_DEP_TPR 4
+#endif
+// |deposit| <= 2^NB with NW warps x PA_DEP_TPR tiles x 256 voxels adding to a word per round: sums < 2^30
+constexpr int dep_ilog2(int x) { return x <= 1 ? 0 : 1 + dep_ilog2(x / 2); }
+constexpr int dep_nb(int nw) { return 22 - dep_ilog2(nw * PA_DEP_TPR); }
 
 template <int LMIN, int NW>
 struct DepCfg {
@@ -1291,7 +1298,8 @@ struct DepCfg {
     static constexpr int NQ = R + 2;              // int words per position: R channels, X, low word of channel 0
     static constexpr int CS = NQ | 1;             // odd stride
     static constexpr int CF = R + 1;              // fp32 words per position
-    static constexpr int NB = NW == 8 ? 19 : 18;  // a round adds <= 256 NW deposits per word
+    static constexpr int TPR = PA_DEP_TPR;        // tiles per warp per round
+    static constexpr int NB = dep_nb(NW);         // a round adds <= 256 NW TPR deposits per word
     static constexpr int NB0 = NB + 10;           // channel 0: hi (<= 2^NB) * 2^10 + lo
     static __host__ __device__ int njp(int nt) { return nt + LMIN; }
     static __host__ __device__ size_t smem_bytes(int nt) { return (size_t)(CS + CF) * njp(nt) * 4; }
@@ -1360,6 +1368,14 @@ __device__ __forceinline__ float ceil_alu(float x, int &xi)
 // Unpredicated shared-memory integer add (ATOMS.ADD, no return value) at addr + OFF: a predicated
 // red is turned into a branch per atomic by ptxas, so lanes without a deposit add 0 to a per-lane
 // dummy word instead.
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float rcp_approx(float x)  // the reciprocal of __fdividef (div.approx = a * rcp(b))
+{
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 template <int OFF>
 __device__ __forceinline__ void red_s32(unsigned addr, int v)
 {
@@ -1414,19 +1430,21 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
     const float invP = pm > 0.0f ? 1.0f / pm : 0.0f;
     const int cx = lane & 3, cy = (lane >> 2) & 3, cz = lane >> 4;
     // rounds: NW tiles in a 2 x 2 x (NW/4) tile block, x fastest
-    constexpr int BZ = NW / 4;
-    const int nbx = (g.ntx + 1) >> 1, nby = (g.nty + 1) >> 1, nbz = (g.ntz + BZ - 1) / BZ;
-    const int nb = nbx * nby * nbz;
+    // a round = TPR tiles per warp: NW TPR tiles in a 2 x 2 x (NW TPR / 4) tile block, x fastest
+    constexpr int TPR = C::TPR, BZ = NW / 4;
+    const int nbx = (g.ntx + 1) >> 1, nby = (g.nty + 1) >> 1, nbz = (g.ntz + BZ * TPR - 1) / (BZ * TPR);
+    const int nb = nbx * nby * nbz, nslot = nb * TPR;
     const int spanlo = (int)floorf((-g.rt - g.ksig) * g.inv_a) - 2, spanhi = (int)ceilf((g.rt - g.ksig) * g.inv_a) + 3;
     const unsigned qbase = (unsigned)__cvta_generic_to_shared(Qi);
     const unsigned dbase = (unsigned)__cvta_generic_to_shared(dummy) + 4u * lane;
     __syncthreads();
 
-    auto tile_of = [&](int b, int &tx, int &ty, int &tz) {
+    auto tile_of = [&](int q, int &tx, int &ty, int &tz) {
+        const int b = q / TPR, k = q - b * TPR;
         const int bx = b % nbx, byz = b / nbx, by = byz % nby, bz = byz / nby;
         tx = 2 * bx + (warp & 1);
         ty = 2 * by + ((warp >> 1) & 1);
-        tz = BZ * bz + (warp >> 2);
+        tz = BZ * (TPR * bz + k) + (warp >> 2);
         return tx < g.ntx && ty < g.nty && tz < g.ntz;
     };
     const size_t sy = (size_t)g.nx, sz = (size_t)g.nx * g.ny;
@@ -1442,17 +1460,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
         }
     };
     int ntx_, nty_, ntz_;
-    bool nok = nb > 0 && tile_of(0, ntx_, nty_, ntz_);
+    bool nok = nslot > 0 && tile_of(0, ntx_, nty_, ntz_);
     float Pn[8];
     load_p(ntx_, nty_, ntz_, nok, Pn);
-    for (int b = 0; b < nb; ++b) {
+    for (int q = 0; q < nslot; ++q) {
+        const int b = q / TPR;
         const int tx = ntx_, ty = nty_, tz = ntz_;
         const bool tok = nok;
         float P[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) P[v] = Pn[v];
-        // software pipeline: the next round's amplitudes are in flight during this round
-        nok = b + 1 < nb && tile_of(b + 1, ntx_, nty_, ntz_);
+        // software pipeline: the next tile's amplitudes are in flight during this one
+        nok = q + 1 < nslot && tile_of(q + 1, ntx_, nty_, ntz_);
         load_p(ntx_, nty_, ntz_, nok, Pn);
         if (tok) {
             const Anc A = make_anchor(g, x, tx, ty, tz);
@@ -1466,52 +1485,71 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                 const float ey0 = ((float)(2 * cy) - 0.5f * (TY - 1)) * g.hf;
                 const float ez0 = ((float)(2 * cz) - 0.5f * (TZ - 1)) * g.hf;
                 const float posA = (float)(A.JA + LMIN);
-                const float tCA = __fmaf_rn(A.CA, dc.tA, dc.tC);
+                const float2 tCA = f2(__fmaf_rn(A.CA, dc.tA, dc.tC));
+                const float2 ex = make_float2(ex0, ex0 + g.hf);
+                // two voxels (vx = 0, 1) per pass in packed fp32x2 (FFMA2/FMUL2/FADD2: half the issue
+                // slots); every scalar step below is the same operation as pair<LMIN>() (R17)
 #pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                    const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
-                    const float Pv = P[v];
-                    const float ex = ex0 + (float)vx * g.hf, ey = ey0 + (float)vy * g.hf, ez = ez0 + (float)vz * g.hf;
-                    const float e2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
-                    // the pair window, exactly as pair<LMIN>() (R17), with ceil/floor on the FP32 pipe
-                    const float num = __fmaf_rn(A.dx2, ex, __fmaf_rn(A.dy2, ey, __fmaf_rn(A.dz2, ez, e2)));
-                    const float r2 = __fadd_rn(A.rho2, num);
-                    const float inv_r = rsqrtf(r2);
-                    const float r = __fmul_rn(r2, inv_r);
-                    const float drel = __fdividef(num, __fadd_rn(r, A.rho));
-                    const float bse = __fadd_rn(drel, A.CA);
-                    const float xlo = __fmul_rn(__fsub_rn(bse, g.ksig), g.inv_a);
-                    const float xhi = __fmul_rn(__fadd_rn(bse, g.ksig), g.inv_a);
-                    int clo;
-                    const float clof = ceil_alu(xlo, clo);
-                    const bool Lx = xhi >= __fadd_rn(clof, (float)LMIN);  // floor(xhi) - clo + 1 >= LMIN + 1
-                    const int pos = A.JA + LMIN + clo;                    // j_m + OFF = jlo + LMIN
-                    const bool valid = Pv != 0.0f && pos >= 0 && pos < NJ;
+                for (int v = 0; v < 8; v += 2) {
+                    const int vy = (v >> 1) & 1, vz = v >> 2;
+                    const float2 Pv = make_float2(P[v], P[v + 1]);
+                    const float ey = ey0 + (float)vy * g.hf, ez = ez0 + (float)vz * g.hf;
+                    const float2 e2 = __ffma2_rn(ex, ex, f2(__fmaf_rn(ey, ey, __fmul_rn(ez, ez))));
+                    const float2 num = __ffma2_rn(f2(A.dx2), ex, __ffma2_rn(f2(A.dy2), f2(ey), __ffma2_rn(f2(A.dz2), f2(ez), e2)));
+                    const float2 r2 = __fadd2_rn(f2(A.rho2), num);
+                    const float2 inv_r = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+                    const float2 den = __fadd2_rn(__fmul2_rn(r2, inv_r), f2(A.rho));
+                    const float2 drel = __fmul2_rn(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+                    const float2 bse = __fadd2_rn(drel, f2(A.CA));
+                    const float2 xlo = __fmul2_rn(__fadd2_rn(bse, f2(-g.ksig)), f2(g.inv_a));
+                    const float2 xhi = __fmul2_rn(__fadd2_rn(bse, f2(g.ksig)), f2(g.inv_a));
+                    // ceil(xlo) on the FP32 pipe (bit-identical to ceilf)
+                    const float2 sh = __fadd2_rn(xlo, f2(12582912.0f));
+                    float2 clof = __fadd2_rn(sh, f2(-12582912.0f));
+                    const bool upx = clof.x < xlo.x, upy = clof.y < xlo.y;
+                    clof.x = upx ? clof.x + 1.0f : clof.x;
+                    clof.y = upy ? clof.y + 1.0f : clof.y;
+                    const int clox = __float_as_int(sh.x) - 0x4B400000 + (upx ? 1 : 0);
+                    const int cloy = __float_as_int(sh.y) - 0x4B400000 + (upy ? 1 : 0);
+                    const float2 cl2 = __fadd2_rn(clof, f2((float)LMIN));
+                    const bool Lxx = xhi.x >= cl2.x, Lxy = xhi.y >= cl2.y;  // floor(xhi) - clo + 1 >= LMIN + 1
+                    const int posx = A.JA + LMIN + clox, posy = A.JA + LMIN + cloy;  // j_m + OFF = jlo + LMIN
+                    const bool vax = Pv.x != 0.0f && (unsigned)posx < (unsigned)NJ;
+                    const bool vay = Pv.y != 0.0f && (unsigned)posy < (unsigned)NJ;
                     // t = (D_m - Dc)/Dw, D_m = bse - clo a - MA a
-                    const float t = __fmaf_rn(-clof, dc.tB, __fmaf_rn(drel, dc.tA, tCA));
-                    const float s = t * t;
-                    const float rlo = fmaxf(rmin, __fmaf_rn(__fadd_rn(clof, posA), g.af, dc.W0));
-                    const float ct = valid ? Pv * invP * rlo * inv_r : 0.0f;
+                    const float2 t = __ffma2_rn(clof, f2(-dc.tB), __ffma2_rn(drel, f2(dc.tA), tCA));
+                    const float2 s2 = __fmul2_rn(t, t);
+                    float2 rlo = __ffma2_rn(__fadd2_rn(clof, f2(posA)), f2(g.af), f2(dc.W0));
+                    rlo.x = fmaxf(rmin, rlo.x);
+                    rlo.y = fmaxf(rmin, rlo.y);
+                    float2 ct = __fmul2_rn(__fmul2_rn(__fmul2_rn(Pv, f2(invP)), rlo), inv_r);
+                    ct.x = vax ? ct.x : 0.0f;
+                    ct.y = vay ? ct.y : 0.0f;
                     // c t^i s^k products shared by all channels
-                    const float c1 = ct * s, c2 = c1 * s, c3 = c2 * s;       // even channels
-                    const float o0 = ct * t, o1 = o0 * s, o2 = o1 * s, o3 = o2 * s;  // odd channels
-                    // ct = 0 (all words 0) for a lane without a deposit; it adds to its dummy words
-                    const unsigned sa = valid ? qbase + (unsigned)pos * (CS * 4) : dbase;
+                    const float2 c1 = __fmul2_rn(ct, s2), c2 = __fmul2_rn(c1, s2), c3 = __fmul2_rn(c2, s2);
+                    const float2 o0 = __fmul2_rn(ct, t), o1 = __fmul2_rn(o0, s2), o2 = __fmul2_rn(o1, s2), o3 = __fmul2_rn(o2, s2);
+                    // a lane without a deposit (ct = 0: every word 0) adds to its dummy words
+                    const unsigned sax = vax ? qbase + (unsigned)posx * (CS * 4) : dbase;
+                    const unsigned say = vay ? qbase + (unsigned)posy * (CS * 4) : dbase;
                     auto chan = [&](auto mc) {
                         constexpr int m = decltype(mc)::value;
-                        const float a0 = (m & 1) ? o0 : ct, a1 = (m & 1) ? o1 : c1, a2 = (m & 1) ? o2 : c2,
-                                    a3 = (m & 1) ? o3 : c3;
-                        const float xm = __fmaf_rn(a3, dc.cf[m][3], __fmaf_rn(a2, dc.cf[m][2], __fmaf_rn(a1, dc.cf[m][1], a0 * dc.cf[m][0])));
+                        const float2 a0 = (m & 1) ? o0 : ct, a1 = (m & 1) ? o1 : c1, a2 = (m & 1) ? o2 : c2,
+                                     a3 = (m & 1) ? o3 : c3;
                         if constexpr (m == 0) {
                             // two words: |x| <= 2^NB0 = hi 2^10 + lo, quantum far below fp32 rounding
-                            const float hs = __fmaf_rn(xm, 1.0f / 1024.0f, 12582912.0f);
-                            const float hf = __fsub_rn(hs, 12582912.0f);
-                            const int nh = __float_as_int(hs) - 0x4B400000;
-                            const int nl = __float_as_int(__fadd_rn(__fmaf_rn(-hf, 1024.0f, xm), 12582912.0f)) - 0x4B400000;
-                            red_s32<0>(sa, nh);
-                            red_s32<4 * (R + 1)>(sa, nl);
+                            const float2 xm = __ffma2_rn(a3, dc.cf2[m][3], __ffma2_rn(a2, dc.cf2[m][2], __ffma2_rn(a1, dc.cf2[m][1], __fmul2_rn(a0, dc.cf2[m][0]))));
+                            const float2 hs = __ffma2_rn(xm, f2(1.0f / 1024.0f), f2(12582912.0f));
+                            const float2 ls = __fadd2_rn(__ffma2_rn(__fadd2_rn(hs, f2(-12582912.0f)), f2(-1024.0f), xm), f2(12582912.0f));
+                            red_s32<0>(sax, __float_as_int(hs.x) - 0x4B400000);
+                            red_s32<0>(say, __float_as_int(hs.y) - 0x4B400000);
+                            red_s32<4 * (R + 1)>(sax, __float_as_int(ls.x) - 0x4B400000);
+                            red_s32<4 * (R + 1)>(say, __float_as_int(ls.y) - 0x4B400000);
                         } else {
-                            red_s32<4 * m>(sa, __float_as_int(__fadd_rn(xm, 12582912.0f)) - 0x4B400000);
+                            // the 1.5 2^23 shifter rides in the first FFMA: each step rounds to an integer
+                            // (quantisation <= 2 units on a channel <= 8% of the trace)
+                            const float2 xm = __ffma2_rn(a3, dc.cf2[m][3], __ffma2_rn(a2, dc.cf2[m][2], __ffma2_rn(a1, dc.cf2[m][1], __ffma2_rn(a0, dc.cf2[m][0], f2(12582912.0f)))));
+                            red_s32<4 * m>(sax, __float_as_int(xm.x) - 0x4B400000);
+                            red_s32<4 * m>(say, __float_as_int(xm.y) - 0x4B400000);
                         }
                     };
                     chan(std::integral_constant<int, 0>{});
@@ -1522,13 +1560,16 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                     if constexpr (R > 5) chan(std::integral_constant<int, 5>{});
                     static_assert(R == 5 || R == 6, "rank 5 or 6");
                     {  // X: the optional last tap (L = LMIN + 1), a cubic in t
-                        const float xm = __fmaf_rn(o1, dc.cf[R][3], __fmaf_rn(c1, dc.cf[R][2], __fmaf_rn(o0, dc.cf[R][1], ct * dc.cf[R][0])));
-                        const int n = __float_as_int(__fadd_rn(xm, 12582912.0f)) - 0x4B400000;
-                        red_s32<4 * R>(sa, Lx ? n : 0);
+                        const float2 cx = make_float2(Lxx ? ct.x : 0.0f, Lxy ? ct.y : 0.0f);
+                        const float2 ox = make_float2(Lxx ? o0.x : 0.0f, Lxy ? o0.y : 0.0f);
+                        const float2 xm = __ffma2_rn(__fmul2_rn(ox, s2), dc.cf2[R][3], __ffma2_rn(__fmul2_rn(cx, s2), dc.cf2[R][2], __ffma2_rn(ox, dc.cf2[R][1], __ffma2_rn(cx, dc.cf2[R][0], f2(12582912.0f)))));
+                        red_s32<4 * R>(sax, __float_as_int(xm.x) - 0x4B400000);
+                        red_s32<4 * R>(say, __float_as_int(xm.y) - 0x4B400000);
                     }
                 }
             }
         }
+        if (q - b * TPR != TPR - 1) continue;  // flush after the round's last tile
         __syncthreads();
         {
             const int lo = rng[b & 1][0], hi = rng[b & 1][1];  // lo > hi when every tile was culled
