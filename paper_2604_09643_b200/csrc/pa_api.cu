@@ -852,21 +852,26 @@ pa_status launch_adjoint_tay(pa_ctx *ctx, const Plan &pl, const float *poses, co
     const int E = pl.g.E, F = pl.g.F, NJ = pl.g.nt + LMIN;
     const size_t per_frame = (size_t)E * NJ * T::NF * sizeof(float);
     int Fc = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t(48) << 20) / per_frame));
+    // K2c (two voxels per thread, packed) unless PA_ADJ_TAY1=1 selects K2b (one voxel per thread)
+    const char *t1 = std::getenv("PA_ADJ_TAY1");
+    const bool v2 = !(t1 != nullptr && t1[0] == '1');
+    const size_t nanc = v2 ? 2 : 1;  // anchor sets per CTA
     auto smem_of = [&](int fc) {
-        return ((size_t)E * 12 + (size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
+        return ((size_t)E * 12 * nanc + (size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
     };
     while (Fc > 1 && smem_of(Fc) > 113 * 1024) --Fc;
     Fc = std::min(Fc, std::max(1, 65535 / E));  // K2a grid.y = Fc E
     Fc = std::min(Fc, F > 0 ? F : 1);
     const size_t smem = smem_of(Fc);
     if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "E=%d too large for the adjoint kernel's shared memory", E);
-    auto kern = k_adjoint_tay<LMIN, POSE, ADJ>;
+    auto kern = v2 ? k_adjoint_tay2<LMIN, POSE, ADJ> : k_adjoint_tay<LMIN, POSE, ADJ>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
     if (occ < 1) occ = 1;
     int P = occ * ctx->nsm;
-    if (P > pl.g.ntiles) P = pl.g.ntiles;
+    const int nwork = v2 ? pl.g.ntx * pl.g.nty * ((pl.g.ntz + 1) / 2) : pl.g.ntiles;  // tile pairs / tiles
+    if (P > nwork) P = nwork;
     L.P = P;
     L.Fc = Fc;
     L.smem = smem;

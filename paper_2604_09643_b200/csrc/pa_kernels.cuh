@@ -1616,6 +1616,252 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
     fwd_epilogue(g, y, fe, out, mode, meas, row_mask, rowloss, red);
 }
 
+// ============================================================================================
+// K2c — the moment-filter adjoint (a4 + a5) with two voxels per thread in packed fp32x2.
+//
+// Same arithmetic as K2b (k_adjoint_tay) per (voxel, element): the window of pair<LMIN>() (every
+// step bit-identical, ceil on the FP32 pipe), the Taylor moments S_n = sum_m dl^m/m! F_{n+m}[j_m]
+// from the L2-resident per-row filters, the exact optional last tap, A1 = u_m (D_m S0 - a S1)
+// and Bq = u_m ((D_m^2 - s^2) S0 - 2 a D_m S1 + a^2 S2).  A thread owns voxels z and z + 2 of an
+// 8x8x4 anchor tile (a CTA = two tiles stacked in z, 128 threads each), so the geometry, the
+// series and the gradient terms of the two voxels run as FFMA2/FMUL2/FADD2, the anchor is read
+// once for both, and their element-gradient terms are summed before the warp reduction.
+// ============================================================================================
+template <int NF>
+struct Tay2A {
+    float2 Fv[NF];  // filter values of voxel (.x) and voxel (.y)
+    float2 Dm, inv_r, dz;
+    float dx, dy;
+    float2 gx;  // cotangent at the optional last tap (0 if absent)
+    bool va, vb;
+};
+
+template <int LMIN>
+__device__ __forceinline__ Tay2A<TayCfg<LMIN>::NF> tay2_stage_a(const Geo &g, const AncS *anc, int e, int E, bool ina,
+                                                                bool inb, float ex, float ey, float2 ez, float2 e2,
+                                                                const float *__restrict__ Frow,
+                                                                const float *__restrict__ crow, int NJ)
+{
+    constexpr int NF = TayCfg<LMIN>::NF, MA = AdjMid<LMIN>::m;
+    Tay2A<NF> o;
+    const int ec = min(e, E - 1);
+    const AncS sa = anc[ec];
+    const float2 num = __ffma2_rn(f2(sa.dx2), f2(ex), __ffma2_rn(f2(sa.dy2), f2(ey), __ffma2_rn(f2(sa.dz2), ez, e2)));
+    const float2 r2 = __fadd2_rn(f2(sa.rho2), num);
+    const float2 inv_r = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+    const float2 den = __fadd2_rn(__fmul2_rn(r2, inv_r), f2(sa.rho));
+    const float2 drel = __fmul2_rn(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+    const float2 bse = __fadd2_rn(drel, f2(sa.CA));
+    const float2 xlo = __fmul2_rn(__fadd2_rn(bse, f2(-g.ksig)), f2(g.inv_a));
+    const float2 xhi = __fmul2_rn(__fadd2_rn(bse, f2(g.ksig)), f2(g.inv_a));
+    const float2 sh = __fadd2_rn(xlo, f2(12582912.0f));
+    float2 clof = __fadd2_rn(sh, f2(-12582912.0f));
+    const bool upx = clof.x < xlo.x, upy = clof.y < xlo.y;
+    clof.x = upx ? clof.x + 1.0f : clof.x;
+    clof.y = upy ? clof.y + 1.0f : clof.y;
+    const int jla = sa.JA + __float_as_int(sh.x) - 0x4B400000 + (upx ? 1 : 0);
+    const int jlb = sa.JA + __float_as_int(sh.y) - 0x4B400000 + (upy ? 1 : 0);
+    const float2 cl2 = __fadd2_rn(clof, f2((float)LMIN));
+    const bool Lxa = xhi.x >= cl2.x, Lxb = xhi.y >= cl2.y;  // L = LMIN + 1
+    const bool ok = e < E && !sa.cull;
+    o.va = ok && ina && jla <= g.nt - 1 && jla + LMIN + (Lxa ? 0 : -1) >= 0;
+    o.vb = ok && inb && jlb <= g.nt - 1 && jlb + LMIN + (Lxb ? 0 : -1) >= 0;
+    const int jja = o.va ? jla + LMIN : 0, jjb = o.vb ? jlb + LMIN : 0;  // j_m - (MA - LMIN)
+    const float4 *fa = reinterpret_cast<const float4 *>(Frow + (size_t)ec * NJ * NF) + jja * (NF / 4);
+    const float4 *fb = reinterpret_cast<const float4 *>(Frow + (size_t)ec * NJ * NF) + jjb * (NF / 4);
+#pragma unroll
+    for (int r = 0; r < NF / 4; ++r) {
+        const float4 u = __ldg(fa + r), w = __ldg(fb + r);
+        o.Fv[4 * r] = make_float2(u.x, w.x);
+        o.Fv[4 * r + 1] = make_float2(u.y, w.y);
+        o.Fv[4 * r + 2] = make_float2(u.z, w.z);
+        o.Fv[4 * r + 3] = make_float2(u.w, w.w);
+    }
+    o.Dm = __fadd2_rn(__ffma2_rn(clof, f2(-g.af), bse), f2(-(float)MA * g.af));
+    o.inv_r = inv_r;
+    o.dx = sa.dx;
+    o.dy = sa.dy;
+    o.dz = __fadd2_rn(f2(sa.dz), ez);
+    const int jxa = jla + LMIN, jxb = jlb + LMIN;
+    const bool xa = o.va && Lxa && jxa >= 0 && jxa < g.nt, xb = o.vb && Lxb && jxb >= 0 && jxb < g.nt;
+    const float *cr = crow + (size_t)ec * g.nt;
+    o.gx = make_float2(xa ? __ldg(cr + jxa) : 0.0f, xb ? __ldg(cr + jxb) : 0.0f);
+    return o;
+}
+
+template <int LMIN, bool POSE>
+__device__ __forceinline__ void tay2_stage_b(const Geo &g, const TayConst &tc, const Tay2A<TayCfg<LMIN>::NF> &a,
+                                             float2 &A1, float2 &Bq)
+{
+    constexpr int M = TayCfg<LMIN>::M, MA = AdjMid<LMIN>::m, KT = LMIN - MA;
+    const float2 Dm = a.Dm;
+    const float2 dl = __ffma2_rn(f2(tc.lam_s), Dm, f2(-tc.lam0));
+    float2 qm[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) qm[m] = __fmul2_rn(dl, f2(tc.inv[m]));
+    float2 S[3];
+#pragma unroll
+    for (int n = 0; n < (POSE ? 3 : 2); ++n) {
+        float2 t = a.Fv[n + M];
+#pragma unroll
+        for (int m = M - 1; m >= 0; --m) t = __ffma2_rn(t, qm[m], a.Fv[n + m]);
+        S[n] = t;
+    }
+    const float2 ea = __fmul2_rn(Dm, f2(g.two_a_k2 * (float)KT));
+    const float2 w = __fmul2_rn(__fmul2_rn(a.gx, f2(tc.Ckt)), make_float2(ex2(ea.x), ex2(ea.y)));
+    S[0] = __fadd2_rn(S[0], w);
+    S[1] = __ffma2_rn(w, f2((float)KT), S[1]);
+    const float2 q = __fmul2_rn(Dm, Dm);
+    const float2 um = make_float2(ex2(-g.k2 * q.x), ex2(-g.k2 * q.y));
+    A1 = __fmul2_rn(um, __ffma2_rn(f2(-g.af), S[1], __fmul2_rn(Dm, S[0])));
+    if (!a.va) A1.x = 0.0f;
+    if (!a.vb) A1.y = 0.0f;
+    Bq = f2(0.0f);
+    if (POSE) {
+        S[2] = __ffma2_rn(w, f2((float)(KT * KT)), S[2]);
+        // (D^2 - s^2) S0 - 2 a D S1 + a^2 S2
+        const float2 b = __ffma2_rn(f2(g.af * g.af), S[2],
+                                    __ffma2_rn(__fmul2_rn(f2(-2.0f * g.af), Dm), S[1], __fmul2_rn(__fadd2_rn(q, f2(-g.s2)), S[0])));
+        Bq = __fmul2_rn(um, b);
+        if (!a.va) Bq.x = 0.0f;
+        if (!a.vb) Bq.y = 0.0f;
+    }
+}
+
+template <int LMIN, bool POSE, bool ADJ>
+__global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst tc, const float *__restrict__ poses,
+                                                                const float *__restrict__ tmpl,
+                                                                const float *__restrict__ p0,
+                                                                const float *__restrict__ cot,
+                                                                const float *__restrict__ Fg,
+                                                                float *__restrict__ grad_p0,
+                                                                float *__restrict__ partial, int f0, int fn)
+{
+    using T = TayCfg<LMIN>;
+    constexpr int NF = T::NF;
+    extern __shared__ float sm[];
+    const int E = g.E, F = g.F, NJ = g.nt + LMIN;
+    AncS *anc = reinterpret_cast<AncS *>(sm);             // [2][E]: the two tiles of the CTA
+    float *wred = reinterpret_cast<float *>(anc + 2 * E);  // [8][E][3]
+    float *gacc = wred + (ADJ_THREADS / 32) * E * 3;       // [fn][E][3]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int half = tid >> 7, u = tid & 127;
+    const int lx = u & 7, ly = (u >> 3) & 7, lzp = u >> 6;  // voxels (lx, ly, lzp) and (lx, ly, lzp + 2)
+    const float ex = ((float)lx - 0.5f * (TX - 1)) * g.hf;
+    const float ey = ((float)ly - 0.5f * (TY - 1)) * g.hf;
+    const float2 ez = make_float2(((float)lzp - 0.5f * (TZ - 1)) * g.hf, ((float)(lzp + 2) - 0.5f * (TZ - 1)) * g.hf);
+    // e2 exactly as pair(): fma(ex, ex, fma(ey, ey, ez * ez))
+    const float2 e2 = __ffma2_rn(f2(ex), f2(ex), __ffma2_rn(f2(ey), f2(ey), __fmul2_rn(ez, ez)));
+    const AncS *anch = anc + half * E;
+    const int ntzp = (g.ntz + 1) >> 1, ntp = g.ntx * g.nty * ntzp;
+
+    if (POSE) {
+        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS) gacc[q] = 0.0f;
+    }
+    for (int tp = blockIdx.x; tp < ntp; tp += gridDim.x) {
+        const int tx = tp % g.ntx, ty = (tp / g.ntx) % g.nty, tzp = tp / (g.ntx * g.nty);
+        const int tz = 2 * tzp + half;
+        const int ix = TX * tx + lx, iy = TY * ty + ly, iza = TZ * tz + lzp, izb = iza + 2;
+        const bool ina = ix < g.nx && iy < g.ny && iza < g.nz, inb = ix < g.nx && iy < g.ny && izb < g.nz;
+        const size_t ka = ((size_t)iza * g.ny + iy) * g.nx + ix, kb = ka + 2 * (size_t)g.nx * g.ny;
+        const float2 P = make_float2((POSE && ina) ? __ldg(p0 + ka) : 0.0f, (POSE && inb) ? __ldg(p0 + kb) : 0.0f);
+        float2 z = f2(0.0f);
+        for (int fl = 0; fl < fn; ++fl) {
+            const int f = f0 + fl;
+            __syncthreads();  // previous frame's anchors / wred consumed
+            for (int q = tid; q < 2 * E; q += ADJ_THREADS) {
+                const int hh = q / E, e = q - hh * E;
+                double x[3];
+                elem_pos(poses, tmpl, f, e, x);
+                const int tzh = 2 * tzp + hh;
+                const Anc A = make_anchor(g, x, tx, ty, tzh < g.ntz ? tzh : 0);
+                AncS sa;
+                sa.dx2 = A.dx2; sa.dy2 = A.dy2; sa.dz2 = A.dz2;
+                sa.dx = A.dx; sa.dy = A.dy; sa.dz = A.dz;
+                sa.rho = A.rho; sa.rho2 = A.rho2; sa.CA = A.CA;
+                sa.JA = A.JA; sa.cull = A.cull || tzh >= g.ntz; sa.jseg = 0;
+                anc[q] = sa;
+            }
+            __syncthreads();
+            const float *Frow = Fg + (size_t)fl * E * NJ * NF;
+            const float *crow = cot + (size_t)f * E * g.nt;
+            Tay2A<NF> cur = tay2_stage_a<LMIN>(g, anch, 0, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
+#pragma unroll 1
+            for (int e0 = 0; e0 < E; e0 += 4) {
+                float G[4][3];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int e = e0 + q;
+                    const Tay2A<NF> nxt = tay2_stage_a<LMIN>(g, anch, e + 1, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
+                    float2 A1, Bq;
+                    tay2_stage_b<LMIN, POSE>(g, tc, cur, A1, Bq);
+                    const float2 ir = cur.inv_r;
+                    const float2 hir = __fmul2_rn(f2(0.5f), ir);
+                    if (ADJ) z = __ffma2_rn(A1, hir, z);
+                    if (POSE) {
+                        // dL/dr = P/(2r) (-Bq/s^2 - A1/r);  G += -dL/dr (d + delta)/r   (x - y_k = -(d + delta))
+                        const float2 dL = __fmul2_rn(__fmul2_rn(P, hir), __ffma2_rn(f2(-g.inv_s2), Bq, __fmul2_rn(__fmul2_rn(f2(-1.0f), A1), ir)));
+                        const float2 sc = __fmul2_rn(__fmul2_rn(f2(-1.0f), dL), ir);
+                        const float sxy = sc.x + sc.y;  // both voxels share x and y
+                        G[q][0] = sxy * (cur.dx + ex);
+                        G[q][1] = sxy * (cur.dy + ey);
+                        G[q][2] = sc.x * cur.dz.x + sc.y * cur.dz.y;
+                    }
+                    cur = nxt;
+                }
+                if (POSE) {
+                    // transposed warp reduction of 4 elements x 3 components (as k_adjoint)
+                    const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+                    float r6[6];
+#pragma unroll
+                    for (int j = 0; j < 6; ++j) {
+                        const float lo = G[j / 3][j % 3], hi = G[2 + j / 3][j % 3];
+                        const float snd = h16 ? lo : hi, kp = h16 ? hi : lo;
+                        r6[j] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+                    }
+                    float r3[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float lo = r6[c], hi = r6[3 + c];
+                        const float snd = h8 ? lo : hi, kp = h8 ? hi : lo;
+                        r3[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 4);
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 2);
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 1);
+                    }
+                    const int e = e0 + ((lane >> 3) & 3);
+                    if ((lane & 7) == 0 && e < E) {
+                        wred[(warp * E + e) * 3 + 0] = r3[0];
+                        wred[(warp * E + e) * 3 + 1] = r3[1];
+                        wred[(warp * E + e) * 3 + 2] = r3[2];
+                    }
+                }
+            }
+            if (POSE) {
+                __syncthreads();
+                for (int q = tid; q < E * 3; q += ADJ_THREADS) {
+                    float s = 0.0f;
+#pragma unroll
+                    for (int w = 0; w < ADJ_THREADS / 32; ++w) s += wred[w * E * 3 + q];
+                    gacc[fl * E * 3 + q] += s;
+                }
+            }
+        }
+        if (ADJ) {
+            if (ina) grad_p0[ka] = (f0 == 0 ? 0.0f : grad_p0[ka]) + z.x;
+            if (inb) grad_p0[kb] = (f0 == 0 ? 0.0f : grad_p0[kb]) + z.y;
+        }
+    }
+    if (POSE) {
+        __syncthreads();
+        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS)
+            partial[((size_t)blockIdx.x * F + f0) * E * 3 + q] = gacc[q];
+    }
+}
+
 // max |p0| as float bits (non-negative floats order like unsigned integers): the 1/Pmax
 // normalisation of the fixed-point deposits of K1d.
 __global__ void k_absmax(const float *__restrict__ p, long long n, unsigned *__restrict__ out)
