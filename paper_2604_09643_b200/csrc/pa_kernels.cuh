@@ -1369,6 +1369,13 @@ __device__ __forceinline__ float ceil_alu(float x, int &xi)
 // red is turned into a branch per atomic by ptxas, so lanes without a deposit add 0 to a per-lane
 // dummy word instead.
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+// one 256-bit read-only global load (LDG.E.ENL2.256, sm_100): 8 consecutive floats, 32-B aligned
+__device__ __forceinline__ void ldg256(const float *p, float v[8])
+{
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p));
+}
 __device__ __forceinline__ float rcp_approx(float x)  // the reciprocal of __fdividef (div.approx = a * rcp(b))
 {
     float y;
@@ -1667,16 +1674,21 @@ __device__ __forceinline__ Tay2A<TayCfg<LMIN>::NF> tay2_stage_a(const Geo &g, co
     o.va = ok && ina && jla <= g.nt - 1 && jla + LMIN + (Lxa ? 0 : -1) >= 0;
     o.vb = ok && inb && jlb <= g.nt - 1 && jlb + LMIN + (Lxb ? 0 : -1) >= 0;
     const int jja = o.va ? jla + LMIN : 0, jjb = o.vb ? jlb + LMIN : 0;  // j_m - (MA - LMIN)
-    const float4 *fa = reinterpret_cast<const float4 *>(Frow + (size_t)ec * NJ * NF) + jja * (NF / 4);
-    const float4 *fb = reinterpret_cast<const float4 *>(Frow + (size_t)ec * NJ * NF) + jjb * (NF / 4);
+    float u[NF], w[NF];  // Frow: this element's filter row
+    if constexpr (NF == 8) {  // one 256-bit load per voxel (32-B records)
+        ldg256(Frow + jja * NF, u);
+        ldg256(Frow + jjb * NF, w);
+    } else {  // 48-B records: 128-bit loads
 #pragma unroll
-    for (int r = 0; r < NF / 4; ++r) {
-        const float4 u = __ldg(fa + r), w = __ldg(fb + r);
-        o.Fv[4 * r] = make_float2(u.x, w.x);
-        o.Fv[4 * r + 1] = make_float2(u.y, w.y);
-        o.Fv[4 * r + 2] = make_float2(u.z, w.z);
-        o.Fv[4 * r + 3] = make_float2(u.w, w.w);
+        for (int r = 0; r < NF / 4; ++r) {
+            const float4 u4 = __ldg(reinterpret_cast<const float4 *>(Frow + jja * NF) + r);
+            const float4 w4 = __ldg(reinterpret_cast<const float4 *>(Frow + jjb * NF) + r);
+            u[4 * r] = u4.x; u[4 * r + 1] = u4.y; u[4 * r + 2] = u4.z; u[4 * r + 3] = u4.w;
+            w[4 * r] = w4.x; w[4 * r + 1] = w4.y; w[4 * r + 2] = w4.z; w[4 * r + 3] = w4.w;
+        }
     }
+#pragma unroll
+    for (int r = 0; r < NF; ++r) o.Fv[r] = make_float2(u[r], w[r]);
     o.Dm = __fadd2_rn(__ffma2_rn(clof, f2(-g.af), bse), f2(-(float)MA * g.af));
     o.inv_r = inv_r;
     o.dx = sa.dx;
@@ -1684,8 +1696,7 @@ __device__ __forceinline__ Tay2A<TayCfg<LMIN>::NF> tay2_stage_a(const Geo &g, co
     o.dz = __fadd2_rn(f2(sa.dz), ez);
     const int jxa = jla + LMIN, jxb = jlb + LMIN;
     const bool xa = o.va && Lxa && jxa >= 0 && jxa < g.nt, xb = o.vb && Lxb && jxb >= 0 && jxb < g.nt;
-    const float *cr = crow + (size_t)ec * g.nt;
-    o.gx = make_float2(xa ? __ldg(cr + jxa) : 0.0f, xb ? __ldg(cr + jxb) : 0.0f);
+    o.gx = make_float2(xa ? __ldg(crow + jxa) : 0.0f, xb ? __ldg(crow + jxb) : 0.0f);  // crow: this element's row
     return o;
 }
 
@@ -1783,8 +1794,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
                 anc[q] = sa;
             }
             __syncthreads();
+            // per-element rows advanced incrementally (element e+1 of stage A; clamped to E-1)
             const float *Frow = Fg + (size_t)fl * E * NJ * NF;
             const float *crow = cot + (size_t)f * E * g.nt;
+            const size_t fstep = (size_t)NJ * NF;
             Tay2A<NF> cur = tay2_stage_a<LMIN>(g, anch, 0, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
 #pragma unroll 1
             for (int e0 = 0; e0 < E; e0 += 4) {
@@ -1792,6 +1805,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int e = e0 + q;
+                    if (e + 1 < E) {
+                        Frow += fstep;
+                        crow += g.nt;
+                    }
                     const Tay2A<NF> nxt = tay2_stage_a<LMIN>(g, anch, e + 1, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
                     float2 A1, Bq;
                     tay2_stage_b<LMIN, POSE>(g, tc, cur, A1, Bq);
