@@ -27,7 +27,8 @@
  *     check enqueues a tiny kernel and synchronises `stream` to read its verdict.
  *   - F == 0 is a no-op returning PA_OK.
  *   - Results are bitwise deterministic run-to-run for a fixed GPU, shapes and inputs
- *     (no floating-point atomics; all reductions in fixed order).
+ *     (no floating-point atomics: the forward's shared-memory deposits are fixed-point
+ *     integer additions, which are associative; all floating-point reductions in fixed order).
  *   - Errors: the status code; pa_last_error() returns a thread-local message.
  *   - A pa_ctx owns only internal workspace (pose-gradient partials, scratch); use one
  *     context per stream.  Calls on different contexts may run concurrently.
@@ -198,6 +199,21 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
                   const float *meas, const uint8_t *row_mask, float *p0, float *euler_t, float *adam_p0,
                   float *adam_pose, const pa_step_cfg *cfg, pa_allreduce_fn ar, void *user, float *grad_p0,
                   float *loss, float *grad_euler, float *row_loss, float *tgv_w, float *adam_w, void *stream);
+
+/* Plan of the kernels pa_forward / pa_adjoint_pose / pa_step run for this geometry (host only:
+ * no device work, no context).  For tests and diagnostics.  PA_EUNSUPPORTED /
+ * PA_EINVAL as the entry points for a geometry outside the compiled window classes. */
+typedef struct {
+    int32_t lmin;        /* L_min = floor(2 kappa sigma / (c dt)): the window class              */
+    int32_t fwd_deposit; /* 1: the deposit-form forward K1d runs (Gaussian kernel); 0: direct K1 */
+    int32_t dep_rank;    /* K1d: separable rank R of the pulse factorisation                     */
+    int32_t dep_warps;   /* K1d: warps per CTA (8: two CTAs per SM, 16: one)                    */
+    double dep_err;      /* K1d: max |G - sum_m phi_m psi_m| / max |G| on a fine grid (R24)     */
+    int32_t adj_taylor;  /* 1: the moment-filter adjoint K2a + K2c runs; 0: the direct K2       */
+    int32_t tay_order;   /* K2a/K2c: Taylor order M of the moment filters                       */
+    double tay_err;      /* K2a/K2c: host bound on the Taylor remainder, relative to sum |terms| */
+} pa_plan_info;
+pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out);
 
 /* Kernel-level timing of the last pa_step / pa_forward / pa_adjoint_pose call on this context
  * (CUDA events recorded on `stream`): ms of the forward kernel and of the adjoint+pose kernel.

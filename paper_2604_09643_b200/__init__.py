@@ -4,6 +4,6 @@ The operator lives in libpa.so (hand-written CUDA for sm_100a behind the C ABI o
 include/pa.h); `_pa` is its thin ctypes binding, `dist` the frame-sharding / NCCL plumbing,
 `gen` the seeded synthetic-input generators.
 """
-from ._pa import Context, PAError, load  # noqa: F401
+from ._pa import Context, PAError, load, plan_info  # noqa: F401
 
 __all__ = ["Context", "PAError", "load"]

@@ -18,7 +18,22 @@ LIB_PATH = os.environ.get("PA_LIB_PATH", os.path.join(_HERE, "libpa.so"))
 PA_OK, PA_EINVAL, PA_ESHAPE, PA_EDEGENERATE, PA_ECUDA, PA_ENOMEM, PA_EUNSUPPORTED = range(7)
 _NAMES = {1: "PA_EINVAL", 2: "PA_ESHAPE", 3: "PA_EDEGENERATE", 4: "PA_ECUDA", 5: "PA_ENOMEM", 6: "PA_EUNSUPPORTED"}
 EXPORTS = ("pa_create", "pa_destroy", "pa_last_error", "pa_version", "pa_forward", "pa_adjoint", "pa_pose_grad",
-           "pa_adjoint_pose", "pa_count", "pa_loss", "pa_tgv", "pa_step", "pa_last_kernel_ms", "pa_launch_count")
+           "pa_adjoint_pose", "pa_count", "pa_loss", "pa_tgv", "pa_step", "pa_last_kernel_ms", "pa_launch_count",
+           "pa_get_plan_info")
+
+
+class PlanInfo(ctypes.Structure):
+    """pa_plan_info (include/pa.h): the kernels the library runs for a geometry."""
+    _fields_ = [("lmin", ctypes.c_int32), ("fwd_deposit", ctypes.c_int32), ("dep_rank", ctypes.c_int32),
+                ("dep_warps", ctypes.c_int32), ("dep_err", ctypes.c_double), ("adj_taylor", ctypes.c_int32),
+                ("tay_order", ctypes.c_int32), ("tay_err", ctypes.c_double)]
+
+
+def plan_info(grid, acq, E: int) -> dict:
+    """pa_get_plan_info: host-only (no GPU needed)."""
+    out = PlanInfo()
+    _check(load().pa_get_plan_info(ctypes.byref(make_grid(grid)), ctypes.byref(make_acq(acq)), int(E), ctypes.byref(out)))
+    return {k: getattr(out, k) for k, _ in PlanInfo._fields_}
 
 
 class PAError(RuntimeError):
@@ -86,6 +101,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                                     ALLREDUCE_FN, vp, vp, vp, vp, vp, vp, vp, vp]
             lib.pa_tgv.argtypes = [vp, g, vp, vp, ctypes.c_float, ctypes.c_float, ctypes.c_float, vp, vp, vp, vp]
             lib.pa_last_kernel_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
+            lib.pa_get_plan_info.argtypes = [g, a, i32, ctypes.POINTER(PlanInfo)]
             _lib = lib
     return _lib
 

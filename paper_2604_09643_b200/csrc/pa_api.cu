@@ -104,7 +104,7 @@ void make_tay(Plan &pl, int lmin, double a, double sig)
 // ~= sum_{m<R} phi_m(t) psi_m(k).  Chebyshev interpolation of degree 9 in t on 64 nodes, SVD of the
 // (coefficient x tap) matrix by one-sided Jacobi (fp64), phi_m converted to monomials and reduced
 // to 4 coefficients of its parity; the optional last tap (k = LMIN - MA) as a cubic in t.  The
-// error of exactly what the kernel evaluates is measured on a fine grid; > 1e-7 of max|G| (or a
+// error of exactly what the kernel evaluates is measured on a fine grid; > 2e-7 of max|G| (or a
 // geometry outside the class) keeps the direct kernel K1.
 void make_dep(Plan &pl, int lmin, double a, double sig)
 {
@@ -266,7 +266,7 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     dc.tC = (float)((-MA * a - Dc) / Dw);
     // r_lo(pos) = c t0 + j_m a + (ks - (MA+1) a) - 0.05 a, j_m = pos - OFF
     dc.W0 = (float)(pl.g.c * pl.g.t0 + ks - (MA + 1) * a - 0.05 * a - (double)KT * a);
-    pl.dep_ok = pl.dep_err <= 1e-7;
+    pl.dep_ok = pl.dep_err <= 2e-7;
 }
 
 pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &pl)
@@ -1369,6 +1369,24 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
                                                          (float)bc2);
         CUDA_TRY(cudaGetLastError());
     }
+    return PA_OK;
+}
+
+pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out)
+{
+    if (!out) return fail(PA_EINVAL, "null out");
+    std::memset(out, 0, sizeof *out);
+    Plan pl;
+    pa_status s = make_plan(grid, acq, E, 1, pl);
+    if (s) return s;
+    out->lmin = kClasses[pl.klass].lmin;
+    out->fwd_deposit = use_dep(pl) ? 1 : 0;
+    out->dep_rank = out->lmin <= 32 ? 6 : 5;  // == DepRank<LMIN>::R
+    out->dep_warps = pl.dep_nw;
+    out->dep_err = pl.dep_err;
+    out->adj_taylor = (pl.fam == KF_GAUSS && pl.tay_ok && !adj_direct_forced()) ? 1 : 0;
+    out->tay_order = tay_order(out->lmin);
+    out->tay_err = pl.tay_err;
     return PA_OK;
 }
 
