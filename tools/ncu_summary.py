@@ -1,5 +1,5 @@
 """Markdown summary of one-kernel `ncu --set full` report: key metrics, stall mix, SASS opcode mix.
-usage: python tools/ncu_summary.py rep.ncu-rep [units_of_work] > summary.md"""
+usage: python tools/ncu_summary.py rep.ncu-rep [units_of_work] [kernel_regex] > summary.md"""
 import csv
 import io
 import re
@@ -9,6 +9,7 @@ from collections import Counter
 
 rep = sys.argv[1]
 units = float(sys.argv[2]) if len(sys.argv) > 2 else None
+kregex = sys.argv[3] if len(sys.argv) > 3 else None  # summarise the first launch whose name matches
 
 
 def ncu(*args):
@@ -16,7 +17,10 @@ def ncu(*args):
 
 
 raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
-h, u, v = raw[0], raw[1], raw[2]
+h, u = raw[0], raw[1]
+iK = h.index("Kernel Name")
+rows = [r for r in raw[2:] if len(r) == len(h) and (kregex is None or re.search(kregex, r[iK]))]
+v = rows[0]
 d, un = dict(zip(h, v)), dict(zip(h, u))
 keys = ["Kernel Name", "gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "launch__grid_size",
         "launch__block_size", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
@@ -45,10 +49,15 @@ for k, val in d.items():
 tot = sum(x for x, _ in st) or 1.0
 print("\n**Warp-state samples:** " + ", ".join(f"{n} {100 * x / tot:.1f}%" for x, n in sorted(st, reverse=True)[:9]))
 sass = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source", "sass"))))
-hh = sass[1]
+# one block per profiled launch: "Kernel Name" line, header, rows; take the first matching block
+starts = [i for i, r in enumerate(sass) if r and r[0] == "Kernel Name" and (kregex is None or re.search(kregex, r[1]))]
+b0 = starts[0]
+nxt = [i for i, r in enumerate(sass) if i > b0 and r and r[0] == "Kernel Name"]
+block = sass[b0 + 1:(nxt[0] if nxt else len(sass))]
+hh = block[0]
 iE, iS, iSrc = hh.index("Instructions Executed"), hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source")
 ops, stalls = Counter(), Counter()
-for r in sass[2:]:
+for r in block[1:]:
     src = re.sub(r"^@!?U?P\w+\s+", "", r[iSrc].strip())
     op = src.split(" ")[0].split(".")[0] if src else "?"
     ops[op] += int(r[iE])
