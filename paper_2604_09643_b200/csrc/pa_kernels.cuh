@@ -1446,28 +1446,41 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
     const unsigned dbase = (unsigned)__cvta_generic_to_shared(dummy) + 4u * lane;
     __syncthreads();
 
-    auto tile_of = [&](int q, int &tx, int &ty, int &tz) {
-        const int b = q / TPR, k = q - b * TPR;
-        const int bx = b % nbx, byz = b / nbx, by = byz % nby, bz = byz / nby;
-        tx = 2 * bx + (warp & 1);
-        ty = 2 * by + ((warp >> 1) & 1);
-        tz = BZ * (TPR * bz + k) + (warp >> 2);
+    // the next tile of this warp, advanced incrementally (slot q: round b = q / TPR, k = q % TPR;
+    // rounds run over 2 x 2 x (BZ TPR) tile blocks, x fastest) — no integer division per tile
+    int nk = 0, nbx_ = 0, nby_ = 0, nbz_ = 0;
+    auto next_tile = [&](int &tx, int &ty, int &tz) {
+        tx = 2 * nbx_ + (warp & 1);
+        ty = 2 * nby_ + ((warp >> 1) & 1);
+        tz = BZ * (TPR * nbz_ + nk) + (warp >> 2);
+        if (++nk == TPR) {
+            nk = 0;
+            if (++nbx_ == nbx) {
+                nbx_ = 0;
+                if (++nby_ == nby) {
+                    nby_ = 0;
+                    ++nbz_;
+                }
+            }
+        }
         return tx < g.ntx && ty < g.nty && tz < g.ntz;
     };
-    const size_t sy = (size_t)g.nx, sz = (size_t)g.nx * g.ny;
+    const int sy = g.nx, sz = g.nx * g.ny;  // < 2^31 voxels per volume
     // the lane's 2x2x2 voxel amplitudes of a tile (0 outside the grid)
     auto load_p = [&](int tx, int ty, int tz, bool ok, float P[8]) {
         const int ix0 = TX * tx + 2 * cx, iy0 = TY * ty + 2 * cy, iz0 = TZ * tz + 2 * cz;
-        const float *pb = p0 + ((size_t)iz0 * g.ny + iy0) * g.nx + ix0;
+        const bool okx = ix0 + 1 < g.nx, oky = iy0 + 1 < g.ny, okz = iz0 + 1 < g.nz;
+        const bool ok0 = ok && ix0 < g.nx && iy0 < g.ny && iz0 < g.nz;
+        const float *pb = p0 + (ok0 ? (iz0 * sz + iy0 * sy + ix0) : 0);
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
             const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
-            const bool in = ok && ix0 + vx < g.nx && iy0 + vy < g.ny && iz0 + vz < g.nz;
-            P[v] = in ? __ldg(pb + vx + vy * sy + vz * sz) : 0.0f;
+            const bool in = ok0 && (!vx || okx) && (!vy || oky) && (!vz || okz);
+            P[v] = in ? __ldg(pb + (vx + vy * sy + vz * sz)) : 0.0f;
         }
     };
     int ntx_, nty_, ntz_;
-    bool nok = nslot > 0 && tile_of(0, ntx_, nty_, ntz_);
+    bool nok = nslot > 0 && next_tile(ntx_, nty_, ntz_);
     float Pn[8];
     load_p(ntx_, nty_, ntz_, nok, Pn);
     for (int q = 0; q < nslot; ++q) {
@@ -1478,7 +1491,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
 #pragma unroll
         for (int v = 0; v < 8; ++v) P[v] = Pn[v];
         // software pipeline: the next tile's amplitudes are in flight during this one
-        nok = q + 1 < nslot && tile_of(q + 1, ntx_, nty_, ntz_);
+        nok = q + 1 < nslot && next_tile(ntx_, nty_, ntz_);
         load_p(ntx_, nty_, ntz_, nok, Pn);
         if (tok) {
             const Anc A = make_anchor(g, x, tx, ty, tz);
