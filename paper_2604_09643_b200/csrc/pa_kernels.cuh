@@ -1616,7 +1616,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
     for (int p = tid; p < NJ; p += blockDim.x) {
         const float rr = pm / fmaxf(rmin, __fmaf_rn((float)p, g.af, dc.W0));
 #pragma unroll
-        for (int m = 0; m < CF; ++m) Qf[p * CF + m] *= dc.dec[m] * rr;
+        for (int m = 0; m < CF; ++m) Qf[p * CF + m] = (Qf[p * CF + m] * dc.dec[m]) * rr;  // no denormal intermediate for tiny Pmax
     }
     __syncthreads();
     float *y = reinterpret_cast<float *>(Qi);  // the round accumulators are free now
