@@ -1649,7 +1649,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
 // ============================================================================================
 template <int NF>
 struct Tay2A {
-    float2 Fv[NF];  // filter values of voxel (.x) and voxel (.y)
+    float Fa[NF], Fb[NF];  // filter values of voxel a (.x) and voxel b (.y), straight from the loads
     float2 Dm, inv_r, dz;
     float dx, dy;
     float2 gx;  // cotangent at the optional last tap (0 if absent)
@@ -1687,21 +1687,19 @@ __device__ __forceinline__ Tay2A<TayCfg<LMIN>::NF> tay2_stage_a(const Geo &g, co
     o.va = ok && ina && jla <= g.nt - 1 && jla + LMIN + (Lxa ? 0 : -1) >= 0;
     o.vb = ok && inb && jlb <= g.nt - 1 && jlb + LMIN + (Lxb ? 0 : -1) >= 0;
     const int jja = o.va ? jla + LMIN : 0, jjb = o.vb ? jlb + LMIN : 0;  // j_m - (MA - LMIN)
-    float u[NF], w[NF];  // Frow: this element's filter row
+    // Frow: this element's filter row
     if constexpr (NF == 8) {  // one 256-bit load per voxel (32-B records)
-        ldg256(Frow + jja * NF, u);
-        ldg256(Frow + jjb * NF, w);
+        ldg256(Frow + jja * NF, o.Fa);
+        ldg256(Frow + jjb * NF, o.Fb);
     } else {  // 48-B records: 128-bit loads
 #pragma unroll
         for (int r = 0; r < NF / 4; ++r) {
             const float4 u4 = __ldg(reinterpret_cast<const float4 *>(Frow + jja * NF) + r);
             const float4 w4 = __ldg(reinterpret_cast<const float4 *>(Frow + jjb * NF) + r);
-            u[4 * r] = u4.x; u[4 * r + 1] = u4.y; u[4 * r + 2] = u4.z; u[4 * r + 3] = u4.w;
-            w[4 * r] = w4.x; w[4 * r + 1] = w4.y; w[4 * r + 2] = w4.z; w[4 * r + 3] = w4.w;
+            o.Fa[4 * r] = u4.x; o.Fa[4 * r + 1] = u4.y; o.Fa[4 * r + 2] = u4.z; o.Fa[4 * r + 3] = u4.w;
+            o.Fb[4 * r] = w4.x; o.Fb[4 * r + 1] = w4.y; o.Fb[4 * r + 2] = w4.z; o.Fb[4 * r + 3] = w4.w;
         }
     }
-#pragma unroll
-    for (int r = 0; r < NF; ++r) o.Fv[r] = make_float2(u[r], w[r]);
     o.Dm = __fadd2_rn(__ffma2_rn(clof, f2(-g.af), bse), f2(-(float)MA * g.af));
     o.inv_r = inv_r;
     o.dx = sa.dx;
@@ -1723,13 +1721,18 @@ __device__ __forceinline__ void tay2_stage_b(const Geo &g, const TayConst &tc, c
     float2 qm[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) qm[m] = __fmul2_rn(dl, f2(tc.inv[m]));
+    // the series in scalar FFMAs straight on the loaded registers (packing the two voxels' filter
+    // values would cost a register move per value)
     float2 S[3];
 #pragma unroll
     for (int n = 0; n < (POSE ? 3 : 2); ++n) {
-        float2 t = a.Fv[n + M];
+        float ta = a.Fa[n + M], tb = a.Fb[n + M];
 #pragma unroll
-        for (int m = M - 1; m >= 0; --m) t = __ffma2_rn(t, qm[m], a.Fv[n + m]);
-        S[n] = t;
+        for (int m = M - 1; m >= 0; --m) {
+            ta = __fmaf_rn(ta, qm[m].x, a.Fa[n + m]);
+            tb = __fmaf_rn(tb, qm[m].y, a.Fb[n + m]);
+        }
+        S[n] = make_float2(ta, tb);
     }
     const float2 ea = __fmul2_rn(Dm, f2(g.two_a_k2 * (float)KT));
     const float2 w = __fmul2_rn(__fmul2_rn(a.gx, f2(tc.Ckt)), make_float2(ex2(ea.x), ex2(ea.y)));
