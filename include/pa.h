@@ -15,7 +15,11 @@
  *     PA_KERNEL_POW    K = (D^2 + s^2)^(-nu)       (outgoing term of P:318-322)
  *   y_k = origin + pitch * (i, j, l),  k = i + nx*(j + ny*l)    (x fastest, R7)
  *
- * Units: mm, µs, mm/µs.  Arithmetic: fp32 with fp64 per-tile anchors.
+ * Units: mm, µs, mm/µs.  Arithmetic: fp32 with fp64 per-tile anchors.  For the
+ * Gaussian kernel the forward and the adjoint evaluate the sum through approximations below fp32
+ * accumulation level (a rank-R separable pulse basis with fixed-point deposits; Taylor moment
+ * filters — reading R24); pa_get_plan_info reports the orders and measured errors for a geometry,
+ * and geometries outside the bounds run the direct kernels.
  *
  * Conventions for every entry point
  *   - Array arguments are caller-owned DEVICE pointers (cudaMalloc / torch), fp32,

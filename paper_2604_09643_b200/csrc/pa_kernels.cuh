@@ -1288,6 +1288,9 @@ struct DepConst {
 #ifndef PA_DEP_TPR
 #define PA_DEP_TPR 4
 #endif
+#ifndef PA_DEP_XPRED
+#define PA_DEP_XPRED 0  // 1: the last-tap deposit only by the lanes that have it (a branch)
+#endif
 // |deposit| <= 2^NB with NW warps x PA_DEP_TPR tiles x 256 voxels adding to a word per round: sums < 2^30
 constexpr int dep_ilog2(int x) { return x <= 1 ? 0 : 1 + dep_ilog2(x / 2); }
 constexpr int dep_nb(int nw) { return 22 - dep_ilog2(nw * PA_DEP_TPR); }
@@ -1583,8 +1586,14 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                         const float2 cx = make_float2(Lxx ? ct.x : 0.0f, Lxy ? ct.y : 0.0f);
                         const float2 ox = make_float2(Lxx ? o0.x : 0.0f, Lxy ? o0.y : 0.0f);
                         const float2 xm = __ffma2_rn(__fmul2_rn(ox, s2), dc.cf2[R][3], __ffma2_rn(__fmul2_rn(cx, s2), dc.cf2[R][2], __ffma2_rn(ox, dc.cf2[R][1], __ffma2_rn(cx, dc.cf2[R][0], f2(12582912.0f)))));
+#if PA_DEP_XPRED
+                        // only the lanes whose window has the last tap take part (branch)
+                        if (vax && Lxx) red_s32<4 * R>(sax, __float_as_int(xm.x) - 0x4B400000);
+                        if (vay && Lxy) red_s32<4 * R>(say, __float_as_int(xm.y) - 0x4B400000);
+#else
                         red_s32<4 * R>(sax, __float_as_int(xm.x) - 0x4B400000);
                         red_s32<4 * R>(say, __float_as_int(xm.y) - 0x4B400000);
+#endif
                     }
                 }
             }
