@@ -213,9 +213,11 @@ typedef struct {
     int32_t dep_rank;    /* K1d: separable rank R of the pulse factorisation                     */
     int32_t dep_warps;   /* K1d: warps per CTA (8: two CTAs per SM, 16: one)                    */
     double dep_err;      /* K1d: max |G - sum_m phi_m psi_m| / max |G| on a fine grid (R24)     */
-    int32_t adj_taylor;  /* 1: the moment-filter adjoint K2a + K2c runs; 0: the direct K2       */
+    int32_t adj_taylor;  /* 1: the moment-filter adjoint K2a + K2c is available; 0: direct K2     */
     int32_t tay_order;   /* K2a/K2c: Taylor order M of the moment filters                       */
     double tay_err;      /* K2a/K2c: host bound on the Taylor remainder, relative to sum |terms| */
+    int32_t adj_svd;     /* 1: the adjoint runs in the forward's basis (K2s, opt-in PA_ADJ_SVD=1) */
+    double svd_derr;     /* K2s: max error of d/dt of the factorisation (pose moment), relative  */
 } pa_plan_info;
 pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out);
 

@@ -26,7 +26,8 @@ class PlanInfo(ctypes.Structure):
     """pa_plan_info (include/pa.h): the kernels the library runs for a geometry."""
     _fields_ = [("lmin", ctypes.c_int32), ("fwd_deposit", ctypes.c_int32), ("dep_rank", ctypes.c_int32),
                 ("dep_warps", ctypes.c_int32), ("dep_err", ctypes.c_double), ("adj_taylor", ctypes.c_int32),
-                ("tay_order", ctypes.c_int32), ("tay_err", ctypes.c_double)]
+                ("tay_order", ctypes.c_int32), ("tay_err", ctypes.c_double), ("adj_svd", ctypes.c_int32),
+                ("svd_derr", ctypes.c_double)]
 
 
 def plan_info(grid, acq, E: int) -> dict:

@@ -55,6 +55,8 @@ struct Plan {
     bool tay_ok;     // Taylor remainder below the bound for this geometry
     double tay_err;  // host bound on the remainder (relative to sum |terms|)
     DepConst dc;     // deposit-form forward constants (Gaussian)
+    SvdConst sv;     // the same factorisation for the adjoint K2s (unscaled)
+    double svd_derr; // measured error of its t-derivative (the pose moment), relative to max |dG/dt|
     bool dep_ok;     // factorisation error below the bound for this geometry
     int dep_nw;      // K1d warps per CTA (8: two CTAs per SM; 16: one)
     double dep_err;  // measured error of the factorisation (relative to max |G|)
@@ -260,10 +262,46 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     // psi[m][q-1] = psi_m(k = OFF - q), tap index OFF - q + MA = LMIN - q
     for (int m = 0; m < R; ++m)
         for (int q = 1; q <= lmin; ++q) dc.psi[m][q - 1] = (float)psi[m][lmin - q];
+    // the adjoint K2s: the same basis, unscaled, and the error of the derivative d/dt (pose moment)
+    SvdConst &svc = pl.sv;
+    std::memset(&svc, 0, sizeof svc);
+    std::memcpy(svc.psi, dc.psi, sizeof svc.psi);
+    for (int m = 0; m <= R; ++m)
+        for (int r = 0; r < 4; ++r) svc.c[m][r] = (float)cfd[m][r];
+    {
+        auto dphi = [&](int m, double t) {  // d/dt of t^(m%2) sum_r c_r t^(2r)
+            double v = 0.0;
+            for (int r = 0; r < 4; ++r) {
+                const int i = 2 * r + (m & 1);
+                if (i > 0) v += cfd[m][r] * i * std::pow(t, i - 1);
+            }
+            return v;
+        };
+        auto dphix = [&](double t) { return (3.0 * cfd[R][3] * t + 2.0 * cfd[R][2]) * t + cfd[R][1]; };
+        const double hstep = 1e-4;
+        double dmax = 0.0, derr = 0.0;
+        for (int it = 0; it <= 2000; ++it) {
+            const double t = -1.0 + 2.0 * it / 2000.0;
+            for (int q = 0; q < K; ++q) {
+                const double dg = (G(t + hstep, q) - G(t - hstep, q)) / (2.0 * hstep);
+                double ap = 0.0;
+                for (int m = 0; m < R; ++m) ap += dphi(m, t) * psi[m][q];
+                dmax = std::max(dmax, std::fabs(dg));
+                derr = std::max(derr, std::fabs(dg - ap));
+            }
+            const double dgx = (GX(t + hstep) - GX(t - hstep)) / (2.0 * hstep);
+            derr = std::max(derr, std::fabs(dgx - dphix(t)));
+        }
+        pl.svd_derr = derr / dmax;
+    }
     // t = (D_m - Dc)/Dw with D_m = drel + CA - clo a - MA a
     dc.tA = (float)(1.0 / Dw);
     dc.tB = (float)(a / Dw);
     dc.tC = (float)((-MA * a - Dc) / Dw);
+    svc.tA = dc.tA;
+    svc.tB = dc.tB;
+    svc.tC = dc.tC;
+    svc.invDw = (float)(1.0 / Dw);
     // r_lo(pos) = c t0 + j_m a + (ks - (MA+1) a) - 0.05 a, j_m = pos - OFF
     dc.W0 = (float)(pl.g.c * pl.g.t0 + ks - (MA + 1) * a - 0.05 * a - (double)KT * a);
     pl.dep_ok = pl.dep_err <= 2e-7;
@@ -921,6 +959,62 @@ pa_status launch_adjoint_tay(pa_ctx *ctx, const Plan &pl, const float *poses, co
     return PA_OK;
 }
 
+// The adjoint in the forward's basis (K2s): per frame chunk, K2s-a (filter records, L2-resident) then K2s.
+template <int LMIN, bool POSE, bool ADJ>
+pa_status launch_adjoint_svd(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
+                             const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
+{
+    const int E = pl.g.E, F = pl.g.F, NJ = pl.g.nt + LMIN;
+    const size_t per_frame = (size_t)E * NJ * SVD_NF * sizeof(float);
+    int Fc = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t(48) << 20) / per_frame));
+    auto smem_of = [&](int fc) {
+        return ((size_t)E * 12 * 2 + (size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
+    };
+    while (Fc > 1 && smem_of(Fc) > 113 * 1024) --Fc;
+    Fc = std::min(Fc, std::max(1, 65535 / E));  // filter grid.y = Fc E
+    Fc = std::min(Fc, F > 0 ? F : 1);
+    const size_t smem = smem_of(Fc);
+    if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "E=%d too large for the adjoint kernel's shared memory", E);
+    auto kern = k_adjoint_svd<LMIN, POSE, ADJ>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
+    if (occ < 1) occ = 1;
+    int P = occ * ctx->nsm;
+    const int nwork = pl.g.ntx * pl.g.nty * ((pl.g.ntz + 1) / 2);  // tile pairs
+    if (P > nwork) P = nwork;
+    L.P = P;
+    L.Fc = Fc;
+    L.smem = smem;
+    if (dry) return PA_OK;
+    pa_status s;
+    if ((s = fws_reserve(ctx, (size_t)Fc * per_frame))) return s;
+    float *Fg = static_cast<float *>(ctx->fws);
+    for (int f0 = 0; f0 < F; f0 += Fc) {
+        const int fn = std::min(Fc, F - f0);
+        ++g_nlaunch;
+        k_adj_svd_filter<LMIN><<<dim3((NJ + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.sv, cot, f0, fn, Fg);
+        CUDA_TRY(cudaGetLastError());
+        ++g_nlaunch;
+        kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.sv, poses, tmpl, p0, Fg, grad_p0, partial, f0, fn);
+        CUDA_TRY(cudaGetLastError());
+    }
+    return PA_OK;
+}
+
+// K2s is opt-in (PA_ADJ_SVD=1): measured slower than K2c at C4 (150.5 vs 142.7 ms per 16 frames —
+// the polynomial evaluation costs more FFMAs than the Taylor series saves in exp/loads)
+inline bool adj_svd_selected()
+{
+    const char *e = std::getenv("PA_ADJ_SVD");
+    return e != nullptr && e[0] == '1';
+}
+
+inline bool use_adj_svd(const Plan &pl)
+{
+    return pl.fam == KF_GAUSS && pl.dep_ok && pl.svd_derr <= 1e-5 && adj_svd_selected();
+}
+
 inline bool adj_direct_forced()
 {
     const char *e = std::getenv("PA_ADJ_DIRECT");
@@ -932,8 +1026,12 @@ pa_status launch_adjoint_t(pa_ctx *ctx, const Plan &pl, const float *poses, cons
                            const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
 {
     if constexpr (FAM == KF_GAUSS) {
-        if (pl.tay_ok && !adj_direct_forced())
-            return launch_adjoint_tay<LMIN, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+        if (!adj_direct_forced()) {
+            if (use_adj_svd(pl))
+                return launch_adjoint_svd<LMIN, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+            if (pl.tay_ok)
+                return launch_adjoint_tay<LMIN, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+        }
     }
     auto kern = k_adjoint<LMIN, SEG, POSE, ADJ, FAM>;
     const int E = pl.g.E, F = pl.g.F;
@@ -1387,6 +1485,8 @@ pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa
     out->adj_taylor = (pl.fam == KF_GAUSS && pl.tay_ok && !adj_direct_forced()) ? 1 : 0;
     out->tay_order = tay_order(out->lmin);
     out->tay_err = pl.tay_err;
+    out->adj_svd = use_adj_svd(pl) ? 1 : 0;
+    out->svd_derr = pl.svd_derr;
     return PA_OK;
 }
 

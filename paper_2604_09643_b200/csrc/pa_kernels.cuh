@@ -1904,6 +1904,280 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
     }
 }
 
+// ============================================================================================
+// K2s — the adjoint (a4 + a5) in the basis of the forward's factorisation (R24): per (voxel,
+// element) pair with pos = j_m + OFF,
+//   A1 = sum_k g[j_m + k] G(t, k) ~= sum_m phi_m(t) F_m[pos] + [L = LMIN+1] g[pos] phi_X(t),
+//   F_m[pos] = sum_{q=1..LMIN} g[pos - q] psi_m(OFF - q)          (K2s-a, per row, L2-resident)
+// and the pose moment sum_k g (K + D K') = dA1/dD_m = (1/Dw) dA1/dt (the derivative of the same
+// smooth approximation; the window indicator held constant, R11).  The record of a position is
+// [F_0 .. F_{R-1}, g[pos], 0...] (8 floats, one 256-bit load).  With b_r = sum_{m even} F_m c_{m,r},
+// o_r = sum_{m odd} F_m c_{m,r}:  A1 = E(s) + t O(s),  dA1/dt = 2t E'(s) + O(s) + 2s O'(s),  s = t^2.
+// No exp, no Taylor series, no scattered load for the last tap; the window, geometry, tiling and
+// pose reduction are K2c's.
+// ============================================================================================
+struct SvdConst {
+    float psi[DEP_MAXR][128];   // as DepConst::psi
+    float c[DEP_MAXR + 1][4];   // unscaled phi_m coefficients (index R: the last-tap cubic in t)
+    float tA, tB, tC;           // t = (D_m - Dc)/Dw as in K1d
+    float invDw;                // dt/dD_m
+};
+constexpr int SVD_NF = 8;  // floats per position record
+
+template <int LMIN>
+__global__ void __launch_bounds__(256) k_adj_svd_filter(Geo g, SvdConst sc, const float *__restrict__ cot, int f0,
+                                                        int fn, float *__restrict__ Fg)
+{
+    constexpr int R = DepRank<LMIN>::R;
+    __shared__ float sg[256 + LMIN];
+    const int NJ = g.nt + LMIN;
+    const int row = blockIdx.y;  // chunk-local row (f - f0) E + e
+    const int p0 = blockIdx.x * 256;
+    const float *gr = cot + ((size_t)f0 * g.E + row) * g.nt;
+    // positions p0 .. p0+255 read samples p - q, q in [1, LMIN], and g[p]: samples [p0 - LMIN, p0 + 255]
+    for (int t = threadIdx.x; t < 256 + LMIN; t += 256) {
+        const int j = p0 - LMIN + t;
+        sg[t] = (j >= 0 && j < g.nt) ? __ldg(gr + j) : 0.0f;
+    }
+    __syncthreads();
+    const int pos = p0 + threadIdx.x;
+    if (pos >= NJ) return;
+    float acc[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) acc[m] = 0.0f;
+#pragma unroll 4
+    for (int q = 1; q <= LMIN; ++q) {
+        const float v = sg[threadIdx.x + LMIN - q];
+#pragma unroll
+        for (int m = 0; m < R; ++m) acc[m] = __fmaf_rn(v, sc.psi[m][q - 1], acc[m]);
+    }
+    float rec[SVD_NF];
+#pragma unroll
+    for (int r = 0; r < SVD_NF; ++r) rec[r] = 0.0f;
+#pragma unroll
+    for (int m = 0; m < R; ++m) rec[m] = acc[m];
+    rec[R] = sg[threadIdx.x + LMIN];  // g[pos]
+    float4 *o = reinterpret_cast<float4 *>(Fg + ((size_t)row * NJ + pos) * SVD_NF);
+    o[0] = make_float4(rec[0], rec[1], rec[2], rec[3]);
+    o[1] = make_float4(rec[4], rec[5], rec[6], rec[7]);
+}
+
+struct SvdA {
+    float Fa[SVD_NF], Fb[SVD_NF];  // records of voxel a (.x) and voxel b (.y)
+    float2 t, inv_r, dz;
+    float dx, dy;
+    bool va, vb, xa, xb;  // valid; last tap in-window
+};
+
+template <int LMIN>
+__device__ __forceinline__ SvdA svd_stage_a(const Geo &g, const SvdConst &sc, const AncS *anc, int e, int E, bool ina,
+                                            bool inb, float ex, float ey, float2 ez, float2 e2,
+                                            const float *__restrict__ Frow)
+{
+    SvdA o;
+    const int ec = min(e, E - 1);
+    const AncS sa = anc[ec];
+    const float2 num = __ffma2_rn(f2(sa.dx2), f2(ex), __ffma2_rn(f2(sa.dy2), f2(ey), __ffma2_rn(f2(sa.dz2), ez, e2)));
+    const float2 r2 = __fadd2_rn(f2(sa.rho2), num);
+    const float2 inv_r = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+    const float2 den = __fadd2_rn(__fmul2_rn(r2, inv_r), f2(sa.rho));
+    const float2 drel = __fmul2_rn(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+    const float2 bse = __fadd2_rn(drel, f2(sa.CA));
+    const float2 xlo = __fmul2_rn(__fadd2_rn(bse, f2(-g.ksig)), f2(g.inv_a));
+    const float2 xhi = __fmul2_rn(__fadd2_rn(bse, f2(g.ksig)), f2(g.inv_a));
+    const float2 sh = __fadd2_rn(xlo, f2(12582912.0f));
+    float2 clof = __fadd2_rn(sh, f2(-12582912.0f));
+    const bool upx = clof.x < xlo.x, upy = clof.y < xlo.y;
+    clof.x = upx ? clof.x + 1.0f : clof.x;
+    clof.y = upy ? clof.y + 1.0f : clof.y;
+    const int jla = sa.JA + __float_as_int(sh.x) - 0x4B400000 + (upx ? 1 : 0);
+    const int jlb = sa.JA + __float_as_int(sh.y) - 0x4B400000 + (upy ? 1 : 0);
+    const float2 cl2 = __fadd2_rn(clof, f2((float)LMIN));
+    const bool Lxa = xhi.x >= cl2.x, Lxb = xhi.y >= cl2.y;  // L = LMIN + 1
+    const bool ok = e < E && !sa.cull;
+    o.va = ok && ina && jla <= g.nt - 1 && jla + LMIN + (Lxa ? 0 : -1) >= 0;
+    o.vb = ok && inb && jlb <= g.nt - 1 && jlb + LMIN + (Lxb ? 0 : -1) >= 0;
+    o.xa = Lxa;
+    o.xb = Lxb;
+    const int pa = o.va ? jla + LMIN : 0, pb = o.vb ? jlb + LMIN : 0;  // pos = j_m + OFF
+    ldg256(Frow + pa * SVD_NF, o.Fa);
+    ldg256(Frow + pb * SVD_NF, o.Fb);
+    // t = (D_m - Dc)/Dw, D_m = bse - clo a - MA a  (as K1d)
+    o.t = __ffma2_rn(clof, f2(-sc.tB), __ffma2_rn(drel, f2(sc.tA), f2(__fmaf_rn(sa.CA, sc.tA, sc.tC))));
+    o.inv_r = inv_r;
+    o.dx = sa.dx;
+    o.dy = sa.dy;
+    o.dz = __fadd2_rn(f2(sa.dz), ez);
+    return o;
+}
+
+// A1 and dA1/dt of one voxel from its record
+template <int LMIN, bool POSE>
+__device__ __forceinline__ void svd_eval(const SvdConst &sc, const float F[SVD_NF], float t, bool lx, float &A1,
+                                         float &dA1)
+{
+    constexpr int R = DepRank<LMIN>::R;
+    const float s = t * t;
+    float e[4], o[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        e[r] = F[0] * sc.c[0][r];
+        o[r] = F[1] * sc.c[1][r];
+#pragma unroll
+        for (int m = 2; m < R; ++m) {
+            if (m & 1) o[r] = __fmaf_rn(F[m], sc.c[m][r], o[r]);
+            else e[r] = __fmaf_rn(F[m], sc.c[m][r], e[r]);
+        }
+    }
+    const float E0 = __fmaf_rn(__fmaf_rn(__fmaf_rn(e[3], s, e[2]), s, e[1]), s, e[0]);
+    const float O0 = __fmaf_rn(__fmaf_rn(__fmaf_rn(o[3], s, o[2]), s, o[1]), s, o[0]);
+    const float gx = lx ? F[R] : 0.0f;  // the last tap, in-window iff L = LMIN + 1
+    const float X0 = __fmaf_rn(__fmaf_rn(__fmaf_rn(sc.c[R][3], t, sc.c[R][2]), t, sc.c[R][1]), t, sc.c[R][0]);
+    A1 = __fmaf_rn(gx, X0, __fmaf_rn(t, O0, E0));
+    dA1 = 0.0f;
+    if (POSE) {
+        const float E1 = __fmaf_rn(__fmaf_rn(3.0f * e[3], s, 2.0f * e[2]), s, e[1]);  // E'(s)
+        const float O1 = __fmaf_rn(__fmaf_rn(3.0f * o[3], s, 2.0f * o[2]), s, o[1]);  // O'(s)
+        const float X1 = __fmaf_rn(__fmaf_rn(3.0f * sc.c[R][3], t, 2.0f * sc.c[R][2]), t, sc.c[R][1]);
+        const float d = __fmaf_rn(2.0f * s, O1, __fmaf_rn(2.0f * t, E1, O0));  // dA/dt = 2t E' + O + 2s O'
+        dA1 = __fmaf_rn(gx, X1, d) * sc.invDw;                                 // d/dD_m
+    }
+}
+
+template <int LMIN, bool POSE, bool ADJ>
+__global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_svd(Geo g, SvdConst sc, const float *__restrict__ poses,
+                                                               const float *__restrict__ tmpl,
+                                                               const float *__restrict__ p0,
+                                                               const float *__restrict__ Fg,
+                                                               float *__restrict__ grad_p0,
+                                                               float *__restrict__ partial, int f0, int fn)
+{
+    extern __shared__ float sm[];
+    const int E = g.E, F = g.F, NJ = g.nt + LMIN;
+    AncS *anc = reinterpret_cast<AncS *>(sm);             // [2][E]: the two tiles of the CTA
+    float *wred = reinterpret_cast<float *>(anc + 2 * E);  // [8][E][3]
+    float *gacc = wred + (ADJ_THREADS / 32) * E * 3;       // [fn][E][3]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int half = tid >> 7, u = tid & 127;
+    const int lx = u & 7, ly = (u >> 3) & 7, lzp = u >> 6;  // voxels (lx, ly, lzp) and (lx, ly, lzp + 2)
+    const float ex = ((float)lx - 0.5f * (TX - 1)) * g.hf;
+    const float ey = ((float)ly - 0.5f * (TY - 1)) * g.hf;
+    const float2 ez = make_float2(((float)lzp - 0.5f * (TZ - 1)) * g.hf, ((float)(lzp + 2) - 0.5f * (TZ - 1)) * g.hf);
+    const float2 e2 = __ffma2_rn(f2(ex), f2(ex), __ffma2_rn(f2(ey), f2(ey), __fmul2_rn(ez, ez)));
+    const AncS *anch = anc + half * E;
+    const int ntzp = (g.ntz + 1) >> 1, ntp = g.ntx * g.nty * ntzp;
+
+    if (POSE) {
+        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS) gacc[q] = 0.0f;
+    }
+    for (int tp = blockIdx.x; tp < ntp; tp += gridDim.x) {
+        const int tx = tp % g.ntx, ty = (tp / g.ntx) % g.nty, tzp = tp / (g.ntx * g.nty);
+        const int tz = 2 * tzp + half;
+        const int ix = TX * tx + lx, iy = TY * ty + ly, iza = TZ * tz + lzp, izb = iza + 2;
+        const bool ina = ix < g.nx && iy < g.ny && iza < g.nz, inb = ix < g.nx && iy < g.ny && izb < g.nz;
+        const size_t ka = ((size_t)iza * g.ny + iy) * g.nx + ix, kb = ka + 2 * (size_t)g.nx * g.ny;
+        const float2 P = make_float2((POSE && ina) ? __ldg(p0 + ka) : 0.0f, (POSE && inb) ? __ldg(p0 + kb) : 0.0f);
+        const float2 hP = __fmul2_rn(f2(0.5f), P);
+        float2 z = f2(0.0f);
+        for (int fl = 0; fl < fn; ++fl) {
+            const int f = f0 + fl;
+            __syncthreads();  // previous frame's anchors / wred consumed
+            for (int q = tid; q < 2 * E; q += ADJ_THREADS) {
+                const int hh = q / E, e = q - hh * E;
+                double x[3];
+                elem_pos(poses, tmpl, f, e, x);
+                const int tzh = 2 * tzp + hh;
+                const Anc A = make_anchor(g, x, tx, ty, tzh < g.ntz ? tzh : 0);
+                AncS sa;
+                sa.dx2 = A.dx2; sa.dy2 = A.dy2; sa.dz2 = A.dz2;
+                sa.dx = A.dx; sa.dy = A.dy; sa.dz = A.dz;
+                sa.rho = A.rho; sa.rho2 = A.rho2; sa.CA = A.CA;
+                sa.JA = A.JA; sa.cull = A.cull || tzh >= g.ntz; sa.jseg = 0;
+                anc[q] = sa;
+            }
+            __syncthreads();
+            const float *Frow = Fg + (size_t)fl * E * NJ * SVD_NF;
+            const size_t fstep = (size_t)NJ * SVD_NF;
+            SvdA cur = svd_stage_a<LMIN>(g, sc, anch, 0, E, ina, inb, ex, ey, ez, e2, Frow);
+#pragma unroll 1
+            for (int e0 = 0; e0 < E; e0 += 4) {
+                float G[4][3];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int e = e0 + q;
+                    if (e + 1 < E) Frow += fstep;
+                    const SvdA nxt = svd_stage_a<LMIN>(g, sc, anch, e + 1, E, ina, inb, ex, ey, ez, e2, Frow);
+                    float a1x, a1y, d1x = 0.0f, d1y = 0.0f;
+                    svd_eval<LMIN, POSE>(sc, cur.Fa, cur.t.x, cur.xa, a1x, d1x);
+                    svd_eval<LMIN, POSE>(sc, cur.Fb, cur.t.y, cur.xb, a1y, d1y);
+                    float2 A1 = make_float2(cur.va ? a1x : 0.0f, cur.vb ? a1y : 0.0f);
+                    const float2 ir = cur.inv_r;
+                    const float2 hir = __fmul2_rn(f2(0.5f), ir);
+                    if (ADJ) z = __ffma2_rn(A1, hir, z);
+                    if (POSE) {
+                        const float2 A2 = make_float2(cur.va ? d1x : 0.0f, cur.vb ? d1y : 0.0f);
+                        // dL/dr = P/(2r) (A2 - A1/r);  G += -dL/dr (d + delta)/r
+                        const float2 dL = __fmul2_rn(__fmul2_rn(hP, ir), __ffma2_rn(__fmul2_rn(f2(-1.0f), A1), ir, A2));
+                        const float2 scv = __fmul2_rn(__fmul2_rn(f2(-1.0f), dL), ir);
+                        const float sxy = scv.x + scv.y;  // both voxels share x and y
+                        G[q][0] = sxy * (cur.dx + ex);
+                        G[q][1] = sxy * (cur.dy + ey);
+                        G[q][2] = scv.x * cur.dz.x + scv.y * cur.dz.y;
+                    }
+                    cur = nxt;
+                }
+                if (POSE) {
+                    const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+                    float r6[6];
+#pragma unroll
+                    for (int j = 0; j < 6; ++j) {
+                        const float lo = G[j / 3][j % 3], hi = G[2 + j / 3][j % 3];
+                        const float snd = h16 ? lo : hi, kp = h16 ? hi : lo;
+                        r6[j] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+                    }
+                    float r3[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float lo = r6[c], hi = r6[3 + c];
+                        const float snd = h8 ? lo : hi, kp = h8 ? hi : lo;
+                        r3[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 4);
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 2);
+                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 1);
+                    }
+                    const int e = e0 + ((lane >> 3) & 3);
+                    if ((lane & 7) == 0 && e < E) {
+                        wred[(warp * E + e) * 3 + 0] = r3[0];
+                        wred[(warp * E + e) * 3 + 1] = r3[1];
+                        wred[(warp * E + e) * 3 + 2] = r3[2];
+                    }
+                }
+            }
+            if (POSE) {
+                __syncthreads();
+                for (int q = tid; q < E * 3; q += ADJ_THREADS) {
+                    float s = 0.0f;
+#pragma unroll
+                    for (int w = 0; w < ADJ_THREADS / 32; ++w) s += wred[w * E * 3 + q];
+                    gacc[fl * E * 3 + q] += s;
+                }
+            }
+        }
+        if (ADJ) {
+            if (ina) grad_p0[ka] = (f0 == 0 ? 0.0f : grad_p0[ka]) + z.x;
+            if (inb) grad_p0[kb] = (f0 == 0 ? 0.0f : grad_p0[kb]) + z.y;
+        }
+    }
+    if (POSE) {
+        __syncthreads();
+        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS)
+            partial[((size_t)blockIdx.x * F + f0) * E * 3 + q] = gacc[q];
+    }
+}
+
 // max |p0| as float bits (non-negative floats order like unsigned integers): the 1/Pmax
 // normalisation of the fixed-point deposits of K1d.
 __global__ void k_absmax(const float *__restrict__ p, long long n, unsigned *__restrict__ out)
