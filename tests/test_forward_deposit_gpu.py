@@ -88,3 +88,26 @@ def test_long_traces(ctx, nt, want_dep, want_warps, record_parity):
     r = rel(y, yo)
     record_parity(f"long_trace_{nt}", r, TOL_FA)
     assert r <= TOL_FA, r
+
+
+@pytest.mark.parametrize("variant", ["PA_ADJ_SVD", "PA_ADJ_TAY1", "PA_FWD_DIRECT", "PA_ADJ_DIRECT"])
+def test_alternative_kernels_parity(ctx, variant, monkeypatch, record_parity):
+    """The opt-in / fallback kernels selected by environment switches (K2s, K2b, direct K1, direct K2)
+    keep parity with the oracle on a ragged multi-tile case."""
+    monkeypatch.setenv(variant, "1")
+    grid = gen.make_grid((21, 19, 13), 0.2)
+    acq = gen.make_acq(301, 0.2, t0=1.3)
+    tmpl, poses = random_scene(14, grid, E=5, F=3)
+    p0 = gen.random_volume(grid, 8)
+    cot = gen.random_cotangent((3, 5, 301), 9)
+    g, a = grid32(grid), acq32(acq)
+    y = ctx.forward(g, a, T(tmpl), T(poses), T(p0)).cpu().numpy()
+    gz, gp, _ = ctx.adjoint_pose(g, a, T(tmpl), T(poses), T(p0), T(cot))
+    yo = oracle.forward(g, a, f64(tmpl), f64(poses), f64(p0))
+    zo = oracle.adjoint(g, a, f64(tmpl), f64(poses), f64(cot))
+    po, _ = oracle.pose_grad(g, a, f64(tmpl), f64(poses), f64(p0), f64(cot))
+    ef, ez, ep = rel(y, yo), rel(gz.cpu().numpy(), zo), rel(gp.cpu().numpy(), po)
+    record_parity(f"{variant}:forward", ef, TOL_FA)
+    record_parity(f"{variant}:adjoint", ez, TOL_FA)
+    record_parity(f"{variant}:pose", ep, 1e-3)
+    assert ef <= TOL_FA and ez <= TOL_FA and ep <= 1e-3, (ef, ez, ep)
