@@ -111,7 +111,7 @@ void make_tay(Plan &pl, int lmin, double a, double sig)
 void make_dep(Plan &pl, int lmin, double a, double sig)
 {
     constexpr int N = 64, DG = 10;  // nodes, Chebyshev coefficients (degree 9)
-    const int R = lmin <= 32 ? 6 : 5;  // == DepRank<LMIN>::R
+    const int R = lmin <= 32 ? PA_DEP_RANK_SHORT : 5;  // == DepRank<LMIN>::R
     const int MA = (lmin + 1) / 2, KT = lmin - MA, K = lmin;
     const double ks = pl.g.ksig_d;
     const double Dlo = ks - (MA + 1) * a, Dhi = ks - MA * a;
@@ -304,7 +304,10 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     svc.invDw = (float)(1.0 / Dw);
     // r_lo(pos) = c t0 + j_m a + (ks - (MA+1) a) - 0.05 a, j_m = pos - OFF
     dc.W0 = (float)(pl.g.c * pl.g.t0 + ks - (MA + 1) * a - 0.05 * a - (double)KT * a);
-    pl.dep_ok = pl.dep_err <= 2e-7;
+#ifndef PA_DEP_MAXERR
+#define PA_DEP_MAXERR 2e-7
+#endif
+    pl.dep_ok = pl.dep_err <= PA_DEP_MAXERR;
 }
 
 pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &pl)
@@ -1010,9 +1013,14 @@ inline bool adj_svd_selected()
     return e != nullptr && e[0] == '1';
 }
 
+// ... except for the short-window class (L_min <= 32), where the Taylor form needs M = 7 (48-B filter
+// records, three 128-bit loads) and K2s measured 5% faster (C5, 8 frames: 600 vs 633 ms)
 inline bool use_adj_svd(const Plan &pl)
 {
-    return pl.fam == KF_GAUSS && pl.dep_ok && pl.svd_derr <= 1e-5 && adj_svd_selected();
+    const char *t = std::getenv("PA_ADJ_TAYLOR");
+    const bool taylor = t != nullptr && t[0] == '1';
+    const bool pref = adj_svd_selected() || (kClasses[pl.klass].lmin <= 32 && !taylor);
+    return pl.fam == KF_GAUSS && pl.dep_ok && pl.svd_derr <= 1e-5 && pref;
 }
 
 inline bool adj_direct_forced()
@@ -1479,7 +1487,7 @@ pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa
     if (s) return s;
     out->lmin = kClasses[pl.klass].lmin;
     out->fwd_deposit = use_dep(pl) ? 1 : 0;
-    out->dep_rank = out->lmin <= 32 ? 6 : 5;  // == DepRank<LMIN>::R
+    out->dep_rank = out->lmin <= 32 ? PA_DEP_RANK_SHORT : 5;  // == DepRank<LMIN>::R
     out->dep_warps = pl.dep_nw;
     out->dep_err = pl.dep_err;
     out->adj_taylor = (pl.fam == KF_GAUSS && pl.tay_ok && !adj_direct_forced()) ? 1 : 0;

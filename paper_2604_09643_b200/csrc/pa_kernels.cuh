@@ -1270,9 +1270,12 @@ constexpr int DEP_MAXR = 6;
 
 // rank per window class: the factorisation error is <= ~2e-8 (L_min 53), 5e-9 (26, rank 6),
 // 6e-10 (106) of max|G|
+#ifndef PA_DEP_RANK_SHORT
+#define PA_DEP_RANK_SHORT 6  // rank for the short-window class (L_min <= 32)
+#endif
 template <int LMIN>
 struct DepRank {
-    static constexpr int R = LMIN <= 32 ? 6 : 5;
+    static constexpr int R = LMIN <= 32 ? PA_DEP_RANK_SHORT : 5;
 };
 
 struct DepConst {
