@@ -342,9 +342,13 @@ def main():
     adj_frac = adj_achieved / peak if adj_achieved else None
     f_meas = clocks["sm_mhz"] * 1e6 if clocks.get("sm_mhz") else None
     gauss = args.kernel == "gauss"
-    fwd_name = ("k_fwd_dep (K1d, deposit-form forward + fused loss/cotangent)" if gauss
+    # the kernels this geometry ran with (host-only plan query; env overrides included)
+    from paper_2604_09643_b200._pa import plan_info
+    plan = plan_info(w.grid, w.acq, w.E)
+    fwd_name = ("k_fwd_dep (K1d, deposit-form forward + fused loss/cotangent)" if plan["fwd_deposit"]
                 else "k_forward (K1, direct forward + fused loss/cotangent)")
-    adj_name = ("k_adj_filter + k_adjoint_tay (K2a/K2b, moment-filter adjoint + pose gradient)" if gauss
+    adj_name = ("k_adj_svd_filter + k_adjoint_svd (K2s, rank-R-basis adjoint + pose gradient)" if plan["adj_svd"]
+                else "k_adj_filter + k_adjoint_tay2 (K2a/K2c, moment-filter adjoint + pose gradient)" if plan["adj_taylor"]
                 else "k_adjoint (K2, direct adjoint + pose gradient)")
     k_fwd = {"kernel": fwd_name, "achieved": fwd_achieved, "frac": fwd_frac, "ops_per_update": ops_fwd, "ms_per_step": fms}
     k_adj = {"kernel": adj_name, "achieved": adj_achieved, "frac": adj_frac, "ops_per_update": ops_adj, "ms_per_step": ams}

@@ -27,7 +27,7 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("lmin", ctypes.c_int32), ("fwd_deposit", ctypes.c_int32), ("dep_rank", ctypes.c_int32),
                 ("dep_warps", ctypes.c_int32), ("dep_err", ctypes.c_double), ("adj_taylor", ctypes.c_int32),
                 ("tay_order", ctypes.c_int32), ("tay_err", ctypes.c_double), ("adj_svd", ctypes.c_int32),
-                ("svd_derr", ctypes.c_double)]
+                ("svd_derr", ctypes.c_double), ("dep_groups", ctypes.c_int32), ("dep_ring", ctypes.c_int32)]
 
 
 def plan_info(grid, acq, E: int) -> dict:

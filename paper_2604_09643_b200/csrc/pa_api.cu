@@ -59,6 +59,7 @@ struct Plan {
     double svd_derr; // measured error of its t-derivative (the pose moment), relative to max |dG/dt|
     bool dep_ok;     // factorisation error below the bound for this geometry
     int dep_nw;      // K1d warps per CTA (8: two CTAs per SM; 16: one)
+    int dep_g;       // K1d round-accumulator copies (lane l deposits into copy l % dep_g)
     double dep_err;  // measured error of the factorisation (relative to max |G|)
     int klass;
     int fam;  // pa_kernel (KF_*)
@@ -120,16 +121,52 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     std::memset(&dc, 0, sizeof dc);
     pl.dep_ok = false;
     pl.dep_err = 1.0;
+    pl.svd_derr = 1.0;  // not computed (K2s unavailable) unless the factorisation below succeeds
     pl.dep_nw = 0;
+    pl.dep_g = 1;
     if (lmin > 128) return;
-    // warps per CTA: 8 (two CTAs per SM) when two row accumulators fit in shared memory, else 16
+    // warps per CTA: 8 (two CTAs per SM) when two CTAs' accumulators fit in shared memory, else 16.
+    // The fixed-point round accumulator is a ring of nr positions (pos & (nr - 1)): nr >= the positions
+    // one round can touch = the window-base spread of its 2 x 2 x (NW/4 TPR) tile block (centre
+    // distance / a) + a tile's own spread (2 rt / a) + the margins of spanlo/spanhi; nr = NJ (no ring)
+    // when that is not smaller.  The ring also holds the final trace (nt floats).
     {
-        const int CS = (R + 2) | 1, CF = R + 1;
-        const size_t sm = (size_t)(CS + CF) * (pl.g.nt + lmin) * 4;
+        // accumulator copies: 2 when a tile spans few window positions (h / a < 4: many lanes of a
+        // deposit instruction share a position, and same-address atomics serialise), else 1 (the larger
+        // stride only adds bank conflicts and flush work); PA_DEP_GROUPS=1|2 overrides
+        pl.dep_g = pl.g.h / a < 4.0 ? 2 : 1;
+        if (const char *e = std::getenv("PA_DEP_GROUPS")) pl.dep_g = e[0] == '2' ? 2 : 1;
+        const int CS = (pl.dep_g * (R + 2)) | 1, CF = R + 1, NJ = pl.g.nt + lmin;
+        auto ring = [&](int nw, int &nr, unsigned &nrm) {
+            const int bzt = nw / 4 * PA_DEP_TPR;  // tiles along z in a round's block
+            const double dist = pl.g.h * std::sqrt((double)(TX * TX + TY * TY) + (double)(TZ * (bzt - 1)) * (TZ * (bzt - 1)));
+            const int need = std::max((int)std::ceil((dist + 2.0 * pl.g.rt_d + 2.0 * a) / a) + 16, (pl.g.nt + CS - 1) / CS);
+            int p2 = 64;
+            while (p2 < need) p2 *= 2;
+            if (p2 < NJ) {
+                nr = p2;
+                nrm = (unsigned)(p2 - 1);
+            } else {
+                nr = NJ;
+                nrm = ~0u;
+            }
+        };
+        auto smem = [&](int nr) { return ((size_t)CS * nr + (size_t)CF * NJ) * 4; };
         const size_t st8 = 8 * 32 * 8 + 4 * (32 + CS) + 64, st16 = 16 * 32 * 8 + 4 * (32 + CS) + 64;  // static smem
-        if (2 * (sm + st8 + 1024) <= 228 * 1024) pl.dep_nw = 8;
-        else if (sm + st16 <= 227 * 1024) pl.dep_nw = 16;
-        else return;
+        int nr8, nr16;
+        unsigned m8, m16;
+        ring(8, nr8, m8);
+        ring(16, nr16, m16);
+        if (2 * (smem(nr8) + st8 + 1024) <= 228 * 1024) {
+            pl.dep_nw = 8;
+            dc.nr = nr8;
+            dc.nrm = m8;
+        } else if (smem(nr16) + st16 <= 227 * 1024) {
+            pl.dep_nw = 16;
+            dc.nr = nr16;
+            dc.nrm = m16;
+        } else
+            return;
     }
     const int NB = dep_nb(pl.dep_nw), NB0 = NB + 10;  // == DepCfg<LMIN, NW>::NB, NB0
     auto G = [&](double t, int q) {  // tap q in [0, K): k = q - MA
@@ -820,13 +857,13 @@ inline bool fwd_direct_forced()
 }
 
 // Deposit-form forward (Gaussian): |p0| max (the fixed-point normalisation), then K1d.
-template <int LMIN, int NW>
+template <int LMIN, int NW, int NG>
 pa_status launch_forward_dep(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
                              float *out, int mode, const float *meas, const uint8_t *mask, double *rowloss,
                              cudaStream_t st)
 {
-    const size_t smem = DepCfg<LMIN, NW>::smem_bytes(pl.g.nt);
-    auto kern = k_fwd_dep<LMIN, NW>;
+    const size_t smem = DepCfg<LMIN, NW, NG>::smem_bytes(pl.g.nt, pl.dc.nr);
+    auto kern = k_fwd_dep<LMIN, NW, NG>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     unsigned *pm = reinterpret_cast<unsigned *>(ctx->dflag + 1);
     CUDA_TRY(cudaMemsetAsync(pm, 0, sizeof(unsigned), st));
@@ -845,8 +882,12 @@ pa_status launch_forward_dep_c(pa_ctx *ctx, const Plan &pl, const float *poses, 
                                float *out, int mode, const float *meas, const uint8_t *mask, double *rowloss,
                                cudaStream_t st)
 {
-    if (pl.dep_nw == 8) return launch_forward_dep<LMIN, 8>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    return launch_forward_dep<LMIN, 16>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    if (pl.dep_g == 2) {
+        if (pl.dep_nw == 8) return launch_forward_dep<LMIN, 8, 2>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+        return launch_forward_dep<LMIN, 16, 2>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    }
+    if (pl.dep_nw == 8) return launch_forward_dep<LMIN, 8, 1>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    return launch_forward_dep<LMIN, 16, 1>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
 }
 
 inline bool use_dep(const Plan &pl) { return pl.fam == KF_GAUSS && pl.dep_ok && pl.dep_nw > 0 && !fwd_direct_forced(); }
@@ -1495,6 +1536,8 @@ pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa
     out->tay_err = pl.tay_err;
     out->adj_svd = use_adj_svd(pl) ? 1 : 0;
     out->svd_derr = pl.svd_derr;
+    out->dep_groups = pl.dep_g;
+    out->dep_ring = pl.dc.nr;
     return PA_OK;
 }
 

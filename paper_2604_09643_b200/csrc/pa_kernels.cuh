@@ -1286,10 +1286,15 @@ struct DepConst {
     float tA, tB;              // t = tA * bse - clo * tB + tC   (= (D_m - Dc) / Dw)
     float tC;
     float W0;                  // r_lo(pos) = max(r_min, pos * a + W0) <= r of every pair depositing at pos
+    int nr;                    // positions of the round accumulator ring (>= the span a round can touch)
+    unsigned nrm;              // nr - 1 (nr a power of two), or ~0 when the ring covers the whole row (nr = NJ)
 };
 
 #ifndef PA_DEP_TPR
 #define PA_DEP_TPR 4
+#endif
+#ifndef PA_DEP_MAP
+#define PA_DEP_MAP 1  // lane -> voxel map of a tile: 1 = 2x4x1 per lane (x pair, 4 y rows, one z; default); 0 = 2x2x2 cluster
 #endif
 #ifndef PA_DEP_XPRED
 #define PA_DEP_XPRED 0  // 1: the last-tap deposit only by the lanes that have it (a branch)
@@ -1298,17 +1303,22 @@ struct DepConst {
 constexpr int dep_ilog2(int x) { return x <= 1 ? 0 : 1 + dep_ilog2(x / 2); }
 constexpr int dep_nb(int nw) { return 22 - dep_ilog2(nw * PA_DEP_TPR); }
 
-template <int LMIN, int NW>
+// G = copies of the round accumulator, interleaved per position; lane l deposits into copy l % G
+// (chosen per geometry on the host: Plan::dep_g)
+template <int LMIN, int NW, int G_ = 1>
 struct DepCfg {
     static constexpr int R = DepRank<LMIN>::R;
     static constexpr int NQ = R + 2;              // int words per position: R channels, X, low word of channel 0
-    static constexpr int CS = NQ | 1;             // odd stride
+    static constexpr int G = G_;                  // lanes of one deposit instruction at the same position hit
+                                                  // G different words (same-address atomics serialise)
+    static constexpr int CS = (G * NQ) | 1;       // odd stride
     static constexpr int CF = R + 1;              // fp32 words per position
     static constexpr int TPR = PA_DEP_TPR;        // tiles per warp per round
     static constexpr int NB = dep_nb(NW);         // a round adds <= 256 NW TPR deposits per word
     static constexpr int NB0 = NB + 10;           // channel 0: hi (<= 2^NB) * 2^10 + lo
     static __host__ __device__ int njp(int nt) { return nt + LMIN; }
-    static __host__ __device__ size_t smem_bytes(int nt) { return (size_t)(CS + CF) * njp(nt) * 4; }
+    // ring of nr positions x CS round words + NJ x CF fp32 row accumulators
+    static __host__ __device__ size_t smem_bytes(int nt, int nr) { return ((size_t)CS * nr + (size_t)CF * njp(nt)) * 4; }
 };
 
 // Row epilogue shared by the forward kernels: y (shared memory, nt floats) -> trace, or the MSE / NC
@@ -1395,7 +1405,7 @@ __device__ __forceinline__ void red_s32(unsigned addr, int v)
     asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
 }
 
-template <int LMIN, int NW>
+template <int LMIN, int NW, int NG>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, DepConst dc, const float *__restrict__ poses,
                                                                        const float *__restrict__ tmpl,
                                                                        const float *__restrict__ p0,
@@ -1405,17 +1415,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                                                                        const uint8_t *__restrict__ row_mask,
                                                                        double *__restrict__ rowloss)
 {
-    using C = DepCfg<LMIN, NW>;
-    constexpr int R = C::R, CS = C::CS, CF = C::CF, NQ = C::NQ;
+    using C = DepCfg<LMIN, NW, NG>;
+    constexpr int R = C::R, CS = C::CS, CF = C::CF, NQ = C::NQ, G = C::G;
     extern __shared__ int smi[];
-    const int NJ = C::njp(g.nt);
-    int *Qi = smi;                                         // [NJ][CS] fixed-point round accumulators
-    float *Qf = reinterpret_cast<float *>(smi + CS * NJ);  // [NJ][CF] fp32 row accumulators
+    const int NJ = C::njp(g.nt), NR = dc.nr;
+    const unsigned nrm = dc.nrm;
+    int *Qi = smi;                                         // [NR][CS] fixed-point round accumulators (ring: pos & nrm)
+    float *Qf = reinterpret_cast<float *>(smi + CS * NR);  // [NJ][CF] fp32 row accumulators
     __shared__ int rng[2][2];
     __shared__ double red[NW * 32];
-    __shared__ int dummy[32 + DepCfg<LMIN, NW>::CS];  // target of lanes without a deposit (adds 0)
+    __shared__ int dummy[32 + C::CS];  // target of lanes without a deposit (adds 0)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < (CS + CF) * NJ; i += blockDim.x) smi[i] = 0;
+    for (int i = tid; i < CS * NR + CF * NJ; i += blockDim.x) smi[i] = 0;
     if (tid < 2) {
         rng[tid][0] = 0x7fffffff;
         rng[tid][1] = -1;
@@ -1441,14 +1452,25 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
     }
     const float pm = __uint_as_float(__ldg(pmax_bits));
     const float invP = pm > 0.0f ? 1.0f / pm : 0.0f;
-    const int cx = lane & 3, cy = (lane >> 2) & 3, cz = lane >> 4;
+    // lane l's voxels of a tile: (bx + vx, by + dyv(v), bz + dzv(v)), v = 0..7, vx = v & 1 (the packed pair).
+    // PA_DEP_MAP 1 puts the 32 lanes of one deposit instruction on all 4 z planes of the tile (8 lanes
+    // each) instead of 2 (16 each): more distinct window positions per instruction, fewer same-word atomics.
+#if PA_DEP_MAP == 1
+    const int bx = 2 * (lane & 3), by = 4 * ((lane >> 2) & 1), bz = lane >> 3;
+    auto dyv = [](int v) { return v >> 1; };
+    auto dzv = [](int) { return 0; };
+#else
+    const int bx = 2 * (lane & 3), by = 2 * ((lane >> 2) & 3), bz = 2 * (lane >> 4);
+    auto dyv = [](int v) { return (v >> 1) & 1; };
+    auto dzv = [](int v) { return v >> 2; };
+#endif
     // rounds: NW tiles in a 2 x 2 x (NW/4) tile block, x fastest
     // a round = TPR tiles per warp: NW TPR tiles in a 2 x 2 x (NW TPR / 4) tile block, x fastest
     constexpr int TPR = C::TPR, BZ = NW / 4;
     const int nbx = (g.ntx + 1) >> 1, nby = (g.nty + 1) >> 1, nbz = (g.ntz + BZ * TPR - 1) / (BZ * TPR);
     const int nb = nbx * nby * nbz, nslot = nb * TPR;
     const int spanlo = (int)floorf((-g.rt - g.ksig) * g.inv_a) - 2, spanhi = (int)ceilf((g.rt - g.ksig) * g.inv_a) + 3;
-    const unsigned qbase = (unsigned)__cvta_generic_to_shared(Qi);
+    const unsigned qbase = (unsigned)__cvta_generic_to_shared(Qi) + 4u * NQ * (unsigned)(lane % G);  // this lane's copy
     const unsigned dbase = (unsigned)__cvta_generic_to_shared(dummy) + 4u * lane;
     __syncthreads();
 
@@ -1474,14 +1496,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
     const int sy = g.nx, sz = g.nx * g.ny;  // < 2^31 voxels per volume
     // the lane's 2x2x2 voxel amplitudes of a tile (0 outside the grid)
     auto load_p = [&](int tx, int ty, int tz, bool ok, float P[8]) {
-        const int ix0 = TX * tx + 2 * cx, iy0 = TY * ty + 2 * cy, iz0 = TZ * tz + 2 * cz;
-        const bool okx = ix0 + 1 < g.nx, oky = iy0 + 1 < g.ny, okz = iz0 + 1 < g.nz;
+        const int ix0 = TX * tx + bx, iy0 = TY * ty + by, iz0 = TZ * tz + bz;
         const bool ok0 = ok && ix0 < g.nx && iy0 < g.ny && iz0 < g.nz;
         const float *pb = p0 + (ok0 ? (iz0 * sz + iy0 * sy + ix0) : 0);
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-            const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
-            const bool in = ok0 && (!vx || okx) && (!vy || oky) && (!vz || okz);
+            const int vx = v & 1, vy = dyv(v), vz = dzv(v);
+            const bool in = ok0 && ix0 + vx < g.nx && iy0 + vy < g.ny && iz0 + vz < g.nz;
             P[v] = in ? __ldg(pb + (vx + vy * sy + vz * sz)) : 0.0f;
         }
     };
@@ -1507,19 +1528,17 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                     atomicMin(&rng[b & 1][0], max(base + spanlo, 0));
                     atomicMax(&rng[b & 1][1], min(base + spanhi, NJ - 1));
                 }
-                const float ex0 = ((float)(2 * cx) - 0.5f * (TX - 1)) * g.hf;
-                const float ey0 = ((float)(2 * cy) - 0.5f * (TY - 1)) * g.hf;
-                const float ez0 = ((float)(2 * cz) - 0.5f * (TZ - 1)) * g.hf;
+                // voxel offsets from the tile centre: the same expression as every other kernel (R17)
+                const float2 ex = make_float2(((float)bx - 0.5f * (TX - 1)) * g.hf, ((float)(bx + 1) - 0.5f * (TX - 1)) * g.hf);
                 const float posA = (float)(A.JA + LMIN);
                 const float2 tCA = f2(__fmaf_rn(A.CA, dc.tA, dc.tC));
-                const float2 ex = make_float2(ex0, ex0 + g.hf);
                 // two voxels (vx = 0, 1) per pass in packed fp32x2 (FFMA2/FMUL2/FADD2: half the issue
                 // slots); every scalar step below is the same operation as pair<LMIN>() (R17)
 #pragma unroll
                 for (int v = 0; v < 8; v += 2) {
-                    const int vy = (v >> 1) & 1, vz = v >> 2;
                     const float2 Pv = make_float2(P[v], P[v + 1]);
-                    const float ey = ey0 + (float)vy * g.hf, ez = ez0 + (float)vz * g.hf;
+                    const float ey = ((float)(by + dyv(v)) - 0.5f * (TY - 1)) * g.hf;
+                    const float ez = ((float)(bz + dzv(v)) - 0.5f * (TZ - 1)) * g.hf;
                     const float2 e2 = __ffma2_rn(ex, ex, f2(__fmaf_rn(ey, ey, __fmul_rn(ez, ez))));
                     const float2 num = __ffma2_rn(f2(A.dx2), ex, __ffma2_rn(f2(A.dy2), f2(ey), __ffma2_rn(f2(A.dz2), f2(ez), e2)));
                     const float2 r2 = __fadd2_rn(f2(A.rho2), num);
@@ -1555,8 +1574,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                     const float2 c1 = __fmul2_rn(ct, s2), c2 = __fmul2_rn(c1, s2), c3 = __fmul2_rn(c2, s2);
                     const float2 o0 = __fmul2_rn(ct, t), o1 = __fmul2_rn(o0, s2), o2 = __fmul2_rn(o1, s2), o3 = __fmul2_rn(o2, s2);
                     // a lane without a deposit (ct = 0: every word 0) adds to its dummy words
-                    const unsigned sax = vax ? qbase + (unsigned)posx * (CS * 4) : dbase;
-                    const unsigned say = vay ? qbase + (unsigned)posy * (CS * 4) : dbase;
+                    const unsigned sax = vax ? qbase + ((unsigned)posx & nrm) * (CS * 4) : dbase;
+                    const unsigned say = vay ? qbase + ((unsigned)posy & nrm) * (CS * 4) : dbase;
                     auto chan = [&](auto mc) {
                         constexpr int m = decltype(mc)::value;
                         const float2 a0 = (m & 1) ? o0 : ct, a1 = (m & 1) ? o1 : c1, a2 = (m & 1) ? o2 : c2,
@@ -1606,16 +1625,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
         {
             const int lo = rng[b & 1][0], hi = rng[b & 1][1];  // lo > hi when every tile was culled
             for (int p = (lo <= hi ? lo : hi + 1) + tid; p <= hi; p += blockDim.x) {
-                int *qi = Qi + p * CS;
+                int *qi = Qi + (int)((unsigned)p & nrm) * CS;
                 float *qf = Qf + p * CF;
                 int n[NQ];
 #pragma unroll
                 for (int c = 0; c < NQ; ++c) n[c] = qi[c];
+#pragma unroll
+                for (int k = 1; k < G; ++k)
+#pragma unroll
+                    for (int c = 0; c < NQ; ++c) n[c] += qi[k * NQ + c];  // all copies together < 2^30: no overflow
                 qf[0] += __fmaf_rn((float)n[0], 1024.0f, (float)n[R + 1]);
 #pragma unroll
                 for (int c = 1; c <= R; ++c) qf[c] += (float)n[c];
 #pragma unroll
-                for (int c = 0; c < NQ; ++c) qi[c] = 0;
+                for (int c = 0; c < G * NQ; ++c) qi[c] = 0;
             }
             if (tid < 1) {
                 rng[(b + 1) & 1][0] = 0x7fffffff;
