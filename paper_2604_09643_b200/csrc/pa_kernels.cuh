@@ -1294,7 +1294,7 @@ struct DepConst {
 #define PA_DEP_TPR 4
 #endif
 #ifndef PA_DEP_MAP
-#define PA_DEP_MAP 1  // lane -> voxel map of a tile: 1 = 2x4x1 per lane (x pair, 4 y rows, one z; default); 0 = 2x2x2 cluster
+#define PA_DEP_MAP 2  // lane -> voxel map: 2 = two z-adjacent tiles per warp slot (default); 1 = one tile, 2x4x1 per lane; 0 = 2x2x2 cluster
 #endif
 #ifndef PA_DEP_XPRED
 #define PA_DEP_XPRED 0  // 1: the last-tap deposit only by the lanes that have it (a branch)
@@ -1455,19 +1455,30 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
     // lane l's voxels of a tile: (bx + vx, by + dyv(v), bz + dzv(v)), v = 0..7, vx = v & 1 (the packed pair).
     // PA_DEP_MAP 1 puts the 32 lanes of one deposit instruction on all 4 z planes of the tile (8 lanes
     // each) instead of 2 (16 each): more distinct window positions per instruction, fewer same-word atomics.
-#if PA_DEP_MAP == 1
-    const int bx = 2 * (lane & 3), by = 4 * ((lane >> 2) & 1), bz = lane >> 3;
+    // PA_DEP_MAP 2: a warp slot covers two z-adjacent tiles (lanes 0-15: tile 2 tzp, 16-31: 2 tzp + 1)
+    // and half of their y rows (hh = slot parity): 8 z planes, 4 lanes each, per deposit instruction;
+    // the anchor of a tile is computed once for both halves.
+    constexpr bool PAIR = PA_DEP_MAP == 2;
+#if PA_DEP_MAP == 2
+    const int bx = 2 * (lane & 3), by = 0, bz = (lane >> 2) & 3, half = lane >> 4;
+    auto dyv = [](int v) { return v >> 1; };
+    auto dzv = [](int) { return 0; };
+#elif PA_DEP_MAP == 1
+    const int bx = 2 * (lane & 3), by = 4 * ((lane >> 2) & 1), bz = lane >> 3, half = 0;
     auto dyv = [](int v) { return v >> 1; };
     auto dzv = [](int) { return 0; };
 #else
-    const int bx = 2 * (lane & 3), by = 2 * ((lane >> 2) & 3), bz = 2 * (lane >> 4);
+    const int bx = 2 * (lane & 3), by = 2 * ((lane >> 2) & 3), bz = 2 * (lane >> 4), half = 0;
     auto dyv = [](int v) { return (v >> 1) & 1; };
     auto dzv = [](int v) { return v >> 2; };
 #endif
     // rounds: NW tiles in a 2 x 2 x (NW/4) tile block, x fastest
     // a round = TPR tiles per warp: NW TPR tiles in a 2 x 2 x (NW TPR / 4) tile block, x fastest
     constexpr int TPR = C::TPR, BZ = NW / 4;
-    const int nbx = (g.ntx + 1) >> 1, nby = (g.nty + 1) >> 1, nbz = (g.ntz + BZ * TPR - 1) / (BZ * TPR);
+    constexpr int TPRT = PAIR ? TPR / 2 : TPR;  // tiles (pairs) per warp per round
+    static_assert(!PAIR || TPR % 2 == 0, "paired tiles need an even slot count per round");
+    const int ntzu = PAIR ? (g.ntz + 1) >> 1 : g.ntz;  // z units (tile pairs)
+    const int nbx = (g.ntx + 1) >> 1, nby = (g.nty + 1) >> 1, nbz = (ntzu + BZ * TPRT - 1) / (BZ * TPRT);
     const int nb = nbx * nby * nbz, nslot = nb * TPR;
     const int spanlo = (int)floorf((-g.rt - g.ksig) * g.inv_a) - 2, spanhi = (int)ceilf((g.rt - g.ksig) * g.inv_a) + 3;
     const unsigned qbase = (unsigned)__cvta_generic_to_shared(Qi) + 4u * NQ * (unsigned)(lane % G);  // this lane's copy
@@ -1476,27 +1487,34 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
 
     // the next tile of this warp, advanced incrementally (slot q: round b = q / TPR, k = q % TPR;
     // rounds run over 2 x 2 x (BZ TPR) tile blocks, x fastest) — no integer division per tile
-    int nk = 0, nbx_ = 0, nby_ = 0, nbz_ = 0;
-    auto next_tile = [&](int &tx, int &ty, int &tz) {
-        tx = 2 * nbx_ + (warp & 1);
-        ty = 2 * nby_ + ((warp >> 1) & 1);
-        tz = BZ * (TPR * nbz_ + nk) + (warp >> 2);
-        if (++nk == TPR) {
-            nk = 0;
-            if (++nbx_ == nbx) {
-                nbx_ = 0;
-                if (++nby_ == nby) {
-                    nby_ = 0;
-                    ++nbz_;
+    int nk = 0, nbx_ = 0, nby_ = 0, nbz_ = 0, hh_ = 0, ptx = 0, pty = 0, ptz = 0;
+    auto next_tile = [&](int &tx, int &ty, int &tz, int &hh) {
+        if (!PAIR || hh_ == 0) {
+            ptx = 2 * nbx_ + (warp & 1);
+            pty = 2 * nby_ + ((warp >> 1) & 1);
+            ptz = BZ * (TPRT * nbz_ + nk) + (warp >> 2);
+            if (++nk == TPRT) {
+                nk = 0;
+                if (++nbx_ == nbx) {
+                    nbx_ = 0;
+                    if (++nby_ == nby) {
+                        nby_ = 0;
+                        ++nbz_;
+                    }
                 }
             }
         }
+        tx = ptx;
+        ty = pty;
+        tz = PAIR ? 2 * ptz + half : ptz;  // this lane's tile
+        hh = PAIR ? hh_ : 0;
+        if (PAIR) hh_ ^= 1;
         return tx < g.ntx && ty < g.nty && tz < g.ntz;
     };
     const int sy = g.nx, sz = g.nx * g.ny;  // < 2^31 voxels per volume
     // the lane's 2x2x2 voxel amplitudes of a tile (0 outside the grid)
-    auto load_p = [&](int tx, int ty, int tz, bool ok, float P[8]) {
-        const int ix0 = TX * tx + bx, iy0 = TY * ty + by, iz0 = TZ * tz + bz;
+    auto load_p = [&](int tx, int ty, int tz, int hh, bool ok, float P[8]) {
+        const int ix0 = TX * tx + bx, iy0 = TY * ty + by + 4 * hh, iz0 = TZ * tz + bz;
         const bool ok0 = ok && ix0 < g.nx && iy0 < g.ny && iz0 < g.nz;
         const float *pb = p0 + (ok0 ? (iz0 * sz + iy0 * sy + ix0) : 0);
 #pragma unroll
@@ -1506,25 +1524,28 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
             P[v] = in ? __ldg(pb + (vx + vy * sy + vz * sz)) : 0.0f;
         }
     };
-    int ntx_, nty_, ntz_;
-    bool nok = nslot > 0 && next_tile(ntx_, nty_, ntz_);
+    int ntx_ = 0, nty_ = 0, ntz_ = 0, nhh_ = 0;
+    bool nok = nslot > 0 && next_tile(ntx_, nty_, ntz_, nhh_);
     float Pn[8];
-    load_p(ntx_, nty_, ntz_, nok, Pn);
+    load_p(ntx_, nty_, ntz_, nhh_, nok, Pn);
+    Anc A;  // the lane's tile anchor (PAIR: kept for the second half of the tile pair)
     for (int q = 0; q < nslot; ++q) {
         const int b = q / TPR;
-        const int tx = ntx_, ty = nty_, tz = ntz_;
+        const int tx = ntx_, ty = nty_, tz = ntz_, hh = nhh_;
         const bool tok = nok;
         float P[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) P[v] = Pn[v];
         // software pipeline: the next tile's amplitudes are in flight during this one
-        nok = q + 1 < nslot && next_tile(ntx_, nty_, ntz_);
-        load_p(ntx_, nty_, ntz_, nok, Pn);
-        if (tok) {
-            const Anc A = make_anchor(g, x, tx, ty, tz);
-            if (!A.cull) {
+        nok = q + 1 < nslot && next_tile(ntx_, nty_, ntz_, nhh_);
+        load_p(ntx_, nty_, ntz_, nhh_, nok, Pn);
+        if (PAIR ? __any_sync(0xffffffffu, tok) : tok) {
+            if (hh == 0) A = make_anchor(g, x, tx, ty, tok ? tz : 0);
+            const bool live = tok && !A.cull;
+            if (PAIR ? __any_sync(0xffffffffu, live) : live) {
                 const int base = A.JA + LMIN + (int)floorf(A.CA * g.inv_a);
-                if (lane == 0) {
+                const bool leader = PAIR ? (lane & 15) == 0 : lane == 0;  // one lane per tile
+                if (leader && live && hh == 0) {
                     atomicMin(&rng[b & 1][0], max(base + spanlo, 0));
                     atomicMax(&rng[b & 1][1], min(base + spanhi, NJ - 1));
                 }
@@ -1537,7 +1558,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
 #pragma unroll
                 for (int v = 0; v < 8; v += 2) {
                     const float2 Pv = make_float2(P[v], P[v + 1]);
-                    const float ey = ((float)(by + dyv(v)) - 0.5f * (TY - 1)) * g.hf;
+                    const float ey = ((float)(by + 4 * hh + dyv(v)) - 0.5f * (TY - 1)) * g.hf;
                     const float ez = ((float)(bz + dzv(v)) - 0.5f * (TZ - 1)) * g.hf;
                     const float2 e2 = __ffma2_rn(ex, ex, f2(__fmaf_rn(ey, ey, __fmul_rn(ez, ez))));
                     const float2 num = __ffma2_rn(f2(A.dx2), ex, __ffma2_rn(f2(A.dy2), f2(ey), __ffma2_rn(f2(A.dz2), f2(ez), e2)));
@@ -1559,8 +1580,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                     const float2 cl2 = __fadd2_rn(clof, f2((float)LMIN));
                     const bool Lxx = xhi.x >= cl2.x, Lxy = xhi.y >= cl2.y;  // floor(xhi) - clo + 1 >= LMIN + 1
                     const int posx = A.JA + LMIN + clox, posy = A.JA + LMIN + cloy;  // j_m + OFF = jlo + LMIN
-                    const bool vax = Pv.x != 0.0f && (unsigned)posx < (unsigned)NJ;
-                    const bool vay = Pv.y != 0.0f && (unsigned)posy < (unsigned)NJ;
+                    const bool vax = live && Pv.x != 0.0f && (unsigned)posx < (unsigned)NJ;
+                    const bool vay = live && Pv.y != 0.0f && (unsigned)posy < (unsigned)NJ;
                     // t = (D_m - Dc)/Dw, D_m = bse - clo a - MA a
                     const float2 t = __ffma2_rn(clof, f2(-dc.tB), __ffma2_rn(drel, f2(dc.tA), tCA));
                     const float2 s2 = __fmul2_rn(t, t);
