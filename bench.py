@@ -365,6 +365,23 @@ def main():
             traffic_note = tr.get("note")
     except (OSError, KeyError, ValueError):
         traffic = None
+    # hardware-side check of the same kernel: warp instructions it issues per in-window update (ncu
+    # smsp__inst_executed.sum / exact updates of the captured launch, profiles/r1_issue_c4.json) x this
+    # run's updates / its live kernel time, against the issue peak 148 SM x 4 warp-instr/clk x sm_max
+    issue = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_issue_c4.json")) as fh:
+            iss = json.load(fh)
+        if args.config == "c4" and gauss:
+            key = "forward" if dom is k_fwd else "adjoint"
+            ipu = iss[key]["warp_inst_per_update"]
+            t_s = dom["ms_per_step"] / 1e3
+            ach = U_local_max * ipu / t_s / 1e12
+            ipk = N_SM * 4 * f_max / 1e12
+            issue = {"achieved": ach, "peak": ipk, "unit": "T warp-instr/s", "frac": ach / ipk,
+                     "warp_inst_per_update": ipu, "source": iss[key]["source"]}
+    except (OSError, KeyError, ValueError):
+        issue = None
     roofline = {"bound": "alu", "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
                 "unit": fam["unit"], "frac": dom["frac"], "traffic": traffic, "traffic_unit": "bytes/launch",
                 "peak_basis": f"148 SM x {fam['pipe']} x sm_max {f_max / 1e6:.0f} MHz (MEASURED_PEAKS.json)",
@@ -373,7 +390,7 @@ def main():
                 "frac_at_measured_clock": (dom["achieved"] * 1e12 / (N_SM * lanes * f_meas)) if (dom["achieved"] and f_meas) else None,
                 "other_kernel": other,
                 "step_frac": (U_local_max * (ops_fwd + ops_adj) / (ms / 1e3) / 1e12) / peak if ms > 0 else None,
-                "traffic_note": traffic_note}
+                "traffic_note": traffic_note, "issue": issue}
     cpu = None
     if world == 1 and not args.no_cpu:
         v, cores, sample = cpu_oracle_sample(w, p_true.astype(np.float64), w.poses_true())
