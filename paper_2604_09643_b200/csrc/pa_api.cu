@@ -1185,7 +1185,7 @@ pa_status launch_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const flo
     t.eps = eps;
     dim3 gd((t.nx + TGV_BX - 1) / TGV_BX, (t.ny + TGV_BY - 1) / TGV_BY, (t.nz + TGV_ZS - 1) / TGV_ZS);
     ++g_nlaunch;
-    k_tgv<<<gd, TGV_BX * TGV_BY, 0, st>>>(t, P, w, gP, gw, part);
+    k_tgv<<<gd, TGV_NT, 0, st>>>(t, P, w, gP, gw, part);
     CUDA_TRY(cudaGetLastError());
     ++g_nlaunch;
     k_sum_parts<<<1, 256, 0, st>>>(part, (long long)gd.x * gd.y * gd.z, scale, accumulate, value);
