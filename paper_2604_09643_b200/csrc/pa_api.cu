@@ -1183,6 +1183,8 @@ pa_status launch_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const flo
     t.a1 = a1;
     t.a0 = a0;
     t.eps = eps;
+    if (3.0 * (double)t.nx * t.ny * t.nz >= 2147483647.0)
+        return fail(PA_EUNSUPPORTED, "TGV: 3 x %d x %d x %d exceeds the kernel's 32-bit offsets", t.nx, t.ny, t.nz);
     dim3 gd((t.nx + TGV_BX - 1) / TGV_BX, (t.ny + TGV_BY - 1) / TGV_BY, (t.nz + TGV_ZS - 1) / TGV_ZS);
     ++g_nlaunch;
     k_tgv<<<gd, TGV_NT, 0, st>>>(t, P, w, gP, gw, part);

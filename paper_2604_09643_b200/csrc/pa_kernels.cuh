@@ -2263,9 +2263,10 @@ __device__ __forceinline__ bool tgv_in(const TgvArgs &t, int x, int y, int z)
 __device__ __forceinline__ void tgv_fields(const TgvArgs &t, const float *__restrict__ P, const float *__restrict__ w,
                                            int x, int y, int z, float n[3], float m[6], float &ng, float &ne)
 {
-    const size_t sy = (size_t)t.nx, sz = (size_t)t.nx * t.ny, nv = sz * t.nz;
-    const size_t k = (size_t)z * sz + (size_t)y * sy + x;
-    const size_t off[3] = {1, sy, sz};
+    // 32-bit offsets: 3 nv < 2^31 (checked by launch_tgv)
+    const int sy = t.nx, sz = t.nx * t.ny, nv = sz * t.nz;
+    const int k = z * sz + y * sy + x;
+    const int off[3] = {1, sy, sz};
     const float p = __ldg(P + k);
     float wv[3], D[3][3];  // D[a][b] = d_a w_b
 #pragma unroll
@@ -2322,7 +2323,7 @@ __global__ void __launch_bounds__(TGV_NT) k_tgv(TgvArgs t, const float *__restri
     const int x = x0 - 1 + i, y = y0 - 1 + j;
     const bool pt = threadIdx.x < PX * PY;
     const bool own = pt && i >= 1 && j >= 1;  // owns output voxel (x, y) and the value term of (x, y)
-    const size_t sz = (size_t)t.nx * t.ny, nv = sz * t.nz;
+    const int sz = t.nx * t.ny, nv = sz * t.nz;  // 3 nv < 2^31 (launch_tgv)
     double val = 0.0;
     auto fill = [&](int buf, int z, bool count) {
         if (!pt) return;
@@ -2367,7 +2368,7 @@ __global__ void __launch_bounds__(TGV_NT) k_tgv(TgvArgs t, const float *__restri
                 s += msym(mz, 2, d) - msym(m0, 2, d);
                 gwv[d] = -t.a1 * nn[d] + t.a0 * t.inv_h * s;
             }
-            const size_t k = (size_t)z * sz + (size_t)y * t.nx + x;
+            const int k = z * sz + y * t.nx + x;
             gP[k] = gpv;
 #pragma unroll
             for (int d = 0; d < 3; ++d) gw[d * nv + k] = gwv[d];
