@@ -176,6 +176,8 @@ typedef struct {
  *   L = alpha1 sum_O phi(grad P - w) + alpha0 sum_O phi(E w),  E w = (grad w + grad w^T)/2
  *   P [nz][ny][nx], w [3][nz][ny][nx] (components x, y, z); value (device, 1 float);
  *   grad_P, grad_w outputs (overwritten).  HBM-bound stencil, deterministic.
+ *   Errors: PA_EUNSUPPORTED when 3 nx ny nz >= 2^31 (32-bit offsets); pa_step with
+ *   tgv_lambda > 0 returns the same.
  */
 pa_status pa_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const float *w, float alpha1, float alpha0,
                  float eps, float *value, float *grad_P, float *grad_w, void *stream);
