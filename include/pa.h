@@ -26,9 +26,11 @@
  *     C-contiguous, 4-byte aligned, unless stated "host".  Outputs are overwritten.
  *     The library keeps no pointer after a call returns.
  *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).  Kernels are
- *     enqueued asynchronously on it.  Validation (arguments, supported window class,
- *     degenerate geometry) runs before any output is written; the degenerate-geometry
- *     check enqueues a tiny kernel and synchronises `stream` to read its verdict.
+ *     enqueued asynchronously on it.  Validation (arguments, supported geometry, degenerate
+ *     geometry) runs before any output is written; in pa_forward / pa_adjoint / pa_pose_grad /
+ *     pa_adjoint_pose the degenerate-geometry check enqueues a tiny kernel and synchronises
+ *     `stream` to read its verdict.  pa_step does NOT synchronise: its check stays on the
+ *     device (a degenerate step skips its Adam updates) and pa_step_status() reports it.
  *   - F == 0 is a no-op returning PA_OK.
  *   - Results are bitwise deterministic run-to-run for a fixed GPU, shapes and inputs
  *     (no floating-point atomics: the forward's shared-memory deposits are fixed-point
@@ -54,7 +56,10 @@ typedef enum {
     PA_EDEGENERATE = 3,   /* an element lies within 1e-6 mm of a voxel centre (R10) */
     PA_ECUDA = 4,         /* a CUDA call or launch failed                                     */
     PA_ENOMEM = 5,        /* workspace allocation failed                                      */
-    PA_EUNSUPPORTED = 6   /* window/pitch ratio outside the compiled kernel classes           */
+    PA_EUNSUPPORTED = 6   /* geometry outside every kernel (see pa_get_plan_info): the Gaussian
+                             kernel runs any L_min = floor(2 kappa sigma/(c dt)) in [12, 160]
+                             (nt + L_min row accumulators permitting); the exponential and
+                             power-law families L_min in {26, 53, 106} (compiled direct classes) */
 } pa_status;
 
 /* Voxel grid.  Voxel (i,j,l) centre = origin + pitch*(i,j,l); p0[l][j][i]. */
@@ -90,6 +95,20 @@ typedef struct pa_ctx pa_ctx;
  * beyond the duration of the call).  *ctx = NULL on failure. */
 pa_status pa_create(pa_ctx **ctx, int device);
 void pa_destroy(pa_ctx *ctx);
+
+/* Kernel-selection policy of a context (default 0: the fastest kernels the geometry supports,
+ * DESIGN.md §6).  Bits force the alternatives, for tests and diagnostics: the direct forward K1,
+ * the direct adjoint K2, or prefer the rank-R-basis adjoint K2s / the moment-filter adjoint K2c.
+ * A forced kernel that the geometry does not support makes the calls return PA_EUNSUPPORTED.
+ * Unknown bits -> PA_EINVAL.  The policy is per context (no global state). */
+enum {
+    PA_POLICY_DEFAULT = 0,
+    PA_POLICY_FWD_DIRECT = 1,
+    PA_POLICY_ADJ_DIRECT = 2,
+    PA_POLICY_ADJ_SVD = 4,
+    PA_POLICY_ADJ_TAYLOR = 8
+};
+pa_status pa_set_policy(pa_ctx *ctx, int32_t policy);
 
 /* Thread-local description of the last error on this thread ("" if none). */
 const char *pa_last_error(void);
@@ -200,6 +219,13 @@ pa_status pa_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const float *
  *   adam_w    [2][3][nvox] its Adam state; NULL iff tgv_lambda == 0
  *   With tgv_lambda > 0, grad_p0 on return includes lambda * dTGV/dP (added after the
  *   all-reduce, identically on every rank) and loss[1] includes lambda * TGV.
+ *   `ar` is called on the calling thread, in order, for grad_p0 (nvox floats) and for loss + 1
+ *   (1 float); it must enqueue the sum on `stream` (or complete it before returning) so that the
+ *   kernels pa_step enqueues after it see the reduced values.  A non-zero return -> PA_ECUDA.
+ *   No host synchronisation: the degenerate-geometry check (R10) runs on the device; when it
+ *   fires the step's Adam updates are skipped (p0, euler_t, tgv_w and every Adam state are left
+ *   unchanged; grad_p0 / loss are unspecified) and pa_step_status() returns PA_EDEGENERATE.
+ *   All other errors are returned by pa_step itself, before any device work.
  */
 pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E, int32_t F,
                   const float *meas, const uint8_t *row_mask, float *p0, float *euler_t, float *adam_p0,
@@ -210,7 +236,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
  * no device work, no context).  For tests and diagnostics.  PA_EUNSUPPORTED /
  * PA_EINVAL as the entry points for a geometry outside the compiled window classes. */
 typedef struct {
-    int32_t lmin;        /* L_min = floor(2 kappa sigma / (c dt)): the window class              */
+    int32_t lmin;        /* L_min = floor(2 kappa sigma / (c dt)): windows have L_min or L_min+1 samples */
     int32_t fwd_deposit; /* 1: the deposit-form forward K1d runs (Gaussian kernel); 0: direct K1 */
     int32_t dep_rank;    /* K1d: separable rank R of the pulse factorisation                     */
     int32_t dep_warps;   /* K1d: warps per CTA (8: two CTAs per SM, 16: one)                    */
@@ -222,8 +248,17 @@ typedef struct {
     double svd_derr;     /* K2s: max error of d/dt of the factorisation (pose moment), relative  */
     int32_t dep_groups;  /* K1d: round-accumulator copies (2 when pitch < 4 c dt, else 1)         */
     int32_t dep_ring;    /* K1d: positions of the round-accumulator ring (= nt + L_min: no ring)  */
+    int32_t adj_kernel;  /* the adjoint that runs: 0 direct K2, 1 moment-filter K2a+K2c, 2 K2s     */
+    int32_t direct_class;/* L_min of the direct kernels' compiled class (K1/K2), 0 if none fits    */
 } pa_plan_info;
 pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out);
+/* The same for a context (its pa_set_policy applied). */
+pa_status pa_ctx_plan_info(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out);
+
+/* Verdict of the last pa_step on this context: synchronises on the step's degenerate-geometry
+ * check (not on the rest of the step) and returns PA_EDEGENERATE (message naming the frame,
+ * element and voxel) if it fired, else PA_OK.  Idempotent until the next pa_step. */
+pa_status pa_step_status(pa_ctx *ctx);
 
 /* Kernel-level timing of the last pa_step / pa_forward / pa_adjoint_pose call on this context
  * (CUDA events recorded on `stream`): ms of the forward kernel and of the adjoint+pose kernel.

@@ -118,6 +118,17 @@ def adjoint(grid, acq, tmpl, poses, cot):
     return out
 
 
+def adjoint_abs(grid, acq, tmpl, poses, cot):
+    """Per-voxel error scale of the adjoint: sum of |terms| (test infrastructure; see pa_oracle.c)."""
+    tmpl, poses, cot = _d(tmpl), _d(poses), _d(cot)
+    E, F = tmpl.shape[0], poses.shape[0]
+    out = np.zeros((int(grid["nz"]), int(grid["ny"]), int(grid["nx"])))
+    g, a = _grid(grid), _acq(acq)
+    _load().oracle_adjoint_abs(ctypes.byref(g), ctypes.byref(a), _p(tmpl), ctypes.c_int32(E), _p(poses),
+                               ctypes.c_int32(F), _p(cot), _p(out))
+    return out
+
+
 def elem_grad(grid, acq, tmpl, poses, p0, cot):
     """dL/dx_fe [F][E][3] (P:80; S:100-108)."""
     tmpl, poses, p0, cot = _d(tmpl), _d(poses), _d(p0).reshape(-1), _d(cot)

@@ -193,6 +193,32 @@ void oracle_adjoint(const og_grid *g, const og_acq *a, const double *tmpl, int32
     free(pos);
 }
 
+/* Error scale of a4 per voxel (test infrastructure, not part of the operator): the sum of the
+ * magnitudes of the terms a4 adds, sum_f sum_e sum_j |cot[f,e,j]| |h(D)/(2r)| [window].  A per-voxel
+ * parity bound |z_gpu - z| <= tol * grad_abs[k] judges each voxel against its own terms (the fp32
+ * rounding of a sum scales with the sum of its |terms|, not with its value). */
+void oracle_adjoint_abs(const og_grid *g, const og_acq *a, const double *tmpl, int32_t E, const double *poses,
+                        int32_t F, const double *cot, double *grad_abs)
+{
+    int64_t nvox = (int64_t)g->nx * g->ny * g->nz;
+    double *pos = (double *)malloc(sizeof(double) * 3 * (size_t)F * E);
+    oracle_place(tmpl, E, poses, F, pos);
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < nvox; ++k) {
+        double y[3], z = 0.0;
+        voxel_centre(g, k, y);
+        for (int64_t fe = 0; fe < (int64_t)F * E; ++fe) {
+            double r = dist3(pos + 3 * fe, y);
+            int jlo, jhi;
+            if (!window(a, r, &jlo, &jhi)) continue;
+            const double *gfe = cot + fe * a->nt;
+            for (int j = jlo; j <= jhi; ++j) z += fabs(gfe[j]) * fabs(kern(a, r, j));
+        }
+        grad_abs[k] = z;
+    }
+    free(pos);
+}
+
 /* ---------------------------------------------------------------------------
  * a5: element-position gradient ("sensor spatial coordinates")
  * grad_elem[f,e,:] = sum_k p0[k] sum_j cot[f,e,j] d/dr[h/(2r)] * (x_fe - y_k)/r.

@@ -19,7 +19,10 @@ PA_OK, PA_EINVAL, PA_ESHAPE, PA_EDEGENERATE, PA_ECUDA, PA_ENOMEM, PA_EUNSUPPORTE
 _NAMES = {1: "PA_EINVAL", 2: "PA_ESHAPE", 3: "PA_EDEGENERATE", 4: "PA_ECUDA", 5: "PA_ENOMEM", 6: "PA_EUNSUPPORTED"}
 EXPORTS = ("pa_create", "pa_destroy", "pa_last_error", "pa_version", "pa_forward", "pa_adjoint", "pa_pose_grad",
            "pa_adjoint_pose", "pa_count", "pa_loss", "pa_tgv", "pa_step", "pa_last_kernel_ms", "pa_launch_count",
-           "pa_get_plan_info")
+           "pa_get_plan_info", "pa_ctx_plan_info", "pa_set_policy", "pa_step_status")
+
+# kernel-selection policy bits of a context (pa_set_policy, include/pa.h)
+POLICY = {"default": 0, "fwd_direct": 1, "adj_direct": 2, "adj_svd": 4, "adj_taylor": 8}
 
 
 class PlanInfo(ctypes.Structure):
@@ -27,7 +30,8 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("lmin", ctypes.c_int32), ("fwd_deposit", ctypes.c_int32), ("dep_rank", ctypes.c_int32),
                 ("dep_warps", ctypes.c_int32), ("dep_err", ctypes.c_double), ("adj_taylor", ctypes.c_int32),
                 ("tay_order", ctypes.c_int32), ("tay_err", ctypes.c_double), ("adj_svd", ctypes.c_int32),
-                ("svd_derr", ctypes.c_double), ("dep_groups", ctypes.c_int32), ("dep_ring", ctypes.c_int32)]
+                ("svd_derr", ctypes.c_double), ("dep_groups", ctypes.c_int32), ("dep_ring", ctypes.c_int32),
+                ("adj_kernel", ctypes.c_int32), ("direct_class", ctypes.c_int32)]
 
 
 def plan_info(grid, acq, E: int) -> dict:
@@ -103,6 +107,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             lib.pa_tgv.argtypes = [vp, g, vp, vp, ctypes.c_float, ctypes.c_float, ctypes.c_float, vp, vp, vp, vp]
             lib.pa_last_kernel_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
             lib.pa_get_plan_info.argtypes = [g, a, i32, ctypes.POINTER(PlanInfo)]
+            lib.pa_ctx_plan_info.argtypes = [vp, g, a, i32, ctypes.POINTER(PlanInfo)]
+            lib.pa_set_policy.argtypes = [vp, i32]
+            lib.pa_step_status.argtypes = [vp]
             _lib = lib
     return _lib
 
@@ -155,8 +162,10 @@ def _stream(stream):
 
 def make_allreduce_callback(tensors, allreduce):
     """C callback for pa_step: maps the raw pointer libpa passes back to the torch tensor that
-    owns it and calls `allreduce(tensor)` (in place, e.g. torch.distributed SUM).  Non-zero return
-    = failure (pa_step then returns PA_ECUDA)."""
+    owns it and calls `allreduce(tensor)` (in place, e.g. torch.distributed SUM) with libpa's
+    stream made torch's current stream, so the collective is ordered after the kernels that
+    produced the buffer and before the ones pa_step enqueues next (pa.h).  Non-zero return =
+    failure (pa_step then returns PA_ECUDA)."""
     views = {t.data_ptr(): t for t in tensors}
 
     def _cb(buf, n, stream_ptr, user):
@@ -164,7 +173,13 @@ def make_allreduce_callback(tensors, allreduce):
             t = views[buf]
             if t.numel() != n:
                 return 2
-            allreduce(t)
+            if t.is_cuda:
+                ext = torch.cuda.ExternalStream(int(stream_ptr or 0), device=t.device) if stream_ptr else \
+                    torch.cuda.default_stream(t.device)
+                with torch.cuda.stream(ext):
+                    allreduce(t)
+            else:
+                allreduce(t)
             return 0
         except Exception:  # noqa: BLE001 - reported through the status code
             return 1
@@ -185,6 +200,25 @@ class Context:
         h = ctypes.c_void_p()
         _check(self.lib.pa_create(ctypes.byref(h), self.device))
         self.h = h
+
+    def set_policy(self, policy):
+        """Kernel-selection policy of this context: an int of PA_POLICY_* bits or names from POLICY."""
+        if isinstance(policy, str):
+            policy = POLICY[policy]
+        elif not isinstance(policy, int):
+            policy = sum(POLICY[p] for p in policy)
+        _check(self.lib.pa_set_policy(self.h, int(policy)))
+
+    def plan_info(self, grid, acq, E: int) -> dict:
+        """pa_ctx_plan_info: the kernels this context runs for a geometry (its policy applied)."""
+        out = PlanInfo()
+        _check(self.lib.pa_ctx_plan_info(self.h, ctypes.byref(make_grid(grid)), ctypes.byref(make_acq(acq)), int(E),
+                                         ctypes.byref(out)))
+        return {k: getattr(out, k) for k, _ in PlanInfo._fields_}
+
+    def step_status(self):
+        """pa_step_status: raises PAError(PA_EDEGENERATE) if the last step's geometry was degenerate."""
+        _check(self.lib.pa_step_status(self.h))
 
     def close(self):
         if getattr(self, "h", None):
@@ -266,9 +300,10 @@ class Context:
         return val, gP, gw
 
     def step(self, grid, acq, tmpl, meas, p0, euler_t, adam_p0, adam_pose, grad_p0, loss, cfg: dict, row_mask=None,
-             allreduce=None, grad_euler=None, row_loss=None, tgv_w=None, adam_w=None, stream=None):
+             allreduce=None, grad_euler=None, row_loss=None, tgv_w=None, adam_w=None, stream=None, check=False):
         """One SfM iteration (pa_step).  `allreduce(tensor)` (optional) sums a CUDA tensor in place across ranks;
-        it is called for grad_p0 and for the global loss slot."""
+        it is called for grad_p0 and for the global loss slot, on libpa's stream.  pa_step does not synchronise
+        the host; check=True reads the step's degenerate-geometry verdict (pa_step_status) before returning."""
         F, E = euler_t.shape[0], tmpl.shape[0]
         c = StepCfg()
         c.lr_p0, c.lr_rot, c.lr_trans = float(cfg["lr_p0"]), float(cfg["lr_rot"]), float(cfg["lr_trans"])
@@ -287,6 +322,8 @@ class Context:
                                 _f32(meas), _ptr(m), _f32(p0), _f32(euler_t), _f32(adam_p0), _f32(adam_pose),
                                 ctypes.byref(c), cb, None, _f32(grad_p0), _f32(loss), _ptr(grad_euler),
                                 _ptr(row_loss), _ptr(tgv_w), _ptr(adam_w), _stream(stream)))
+        if check:
+            self.step_status()
         return loss
 
     def launch_count(self):

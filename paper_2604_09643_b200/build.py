@@ -1,34 +1,60 @@
-"""Build libpa.so in-tree with nvcc for sm_100a (no JIT cache, so the .so travels with the repo)."""
+"""Build libpa.so in-tree with nvcc for sm_100a (no JIT cache, so the .so travels with the repo).
+
+The library is split into translation units (host API + small kernels, and one unit per operator-kernel
+family) compiled in parallel, then linked into one shared object."""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", "pa_api.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "pa_kernels.cuh"), os.path.join(ROOT, "include", "pa.h")]
+CSRC = os.path.join(HERE, "csrc")
+SRC = [os.path.join(CSRC, f) for f in ("pa_api.cu", "k_dep.cu", "k_tay.cu", "k_svd.cu", "k_direct_gauss.cu",
+                                       "k_direct_exp.cu", "k_direct_pow.cu")]
+HDRS = [os.path.join(CSRC, f) for f in ("pa_kernels.cuh", "pa_plan.h", "k_direct_impl.cuh")] + \
+    [os.path.join(ROOT, "include", "pa.h")]
+DEPS = SRC + HDRS
 LIB = os.path.join(HERE, "libpa.so")
+OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-ftz=true", "-Xcompiler", "-fPIC",
-         "-shared", "-Xptxas", "-warn-spills"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-std=c++17", "-O3", *ARCH, "-lineinfo", "-ftz=true", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or stale():
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SRC]
+def build(force: bool = False, verbose: bool = False, defs=(), lib: str = LIB, objdir: str = OBJ) -> str:
+    """Compile every translation unit (in parallel) and link libpa.so; `defs` are extra -D flags (variants)."""
+    if not (force or stale(lib)):
+        return lib
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *defs, *inc, "-c", "-o", obj, src]
         if verbose:
-            print(" ".join(cmd))
-        subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
+        if verbose and r.stderr.strip():
+            print(r.stderr, flush=True)
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=min(len(SRC), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, SRC))
+    tmp = lib + ".tmp"
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs])
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -1,7 +1,10 @@
-// pa_api.cu — C ABI of libpa (see include/pa.h) + the small kernels (checks, count, K3 pose
-// reduction, Euler chain, Adam, loss sums).  Citations as in pa_kernels.cuh.
-#include "pa.h"
-#include "pa_kernels.cuh"
+// pa_api.cu — C ABI of libpa (see include/pa.h): argument checks, the per-geometry plan (window length,
+// approximation orders, the kernels that run), the small kernels (degenerate check, count, K3 pose
+// reduction, Euler chain, Adam, loss sums) and the entry points.  The operator kernels are launched from
+// k_dep.cu (K1d), k_tay.cu (K2a/K2c), k_svd.cu (K2s) and k_direct_<family>.cu (K1/K2).
+// Citations as in pa_kernels.cuh.
+#define PA_API_TU
+#include "pa_plan.h"
 
 #include <cmath>
 #include <cstdarg>
@@ -14,10 +17,12 @@
 
 using namespace pa;
 
-namespace {
+namespace pa {
 
-thread_local std::string g_err;
 thread_local long long g_nlaunch = 0;  // kernels enqueued by this thread (pa_launch_count)
+static thread_local std::string g_err;
+
+const char *g_err_cstr() { return g_err.c_str(); }
 
 pa_status fail(pa_status s, const char *fmt, ...)
 {
@@ -30,76 +35,66 @@ pa_status fail(pa_status s, const char *fmt, ...)
     return s;
 }
 
-#define CUDA_TRY(x)                                                                          \
-    do {                                                                                     \
-        cudaError_t _e = (x);                                                                \
-        if (_e != cudaSuccess) return fail(PA_ECUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
-    } while (0)
+}  // namespace pa
+
+namespace {
 
 inline bool aligned4(const void *p) { return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 
-// ------------------------------------------------------------------------ kernel classes
-struct Klass {
-    int lmin, omax, span, seg;
-};
-// Compiled window classes: sigma/(c dt) in {5.33, 2.67, 10.67} at kappa = 5
-// for the BASELINE configs; any geometry whose L_min, cluster spread, tile span and
-// segment need fit a class is supported.
-constexpr Klass kClasses[] = {{53, 11, 58, 128}, {26, 6, 30, 64}, {106, 21, 114, 256}};
+// shortest window of the Gaussian fast path (K1d / K2a+K2c / K2s); the longest is PA_LMAX
+constexpr int FAST_LMIN = 12;
 
-struct Plan {
-    Geo g;
-    FwdConst fc;
-    AdjConst ac;
-    TayConst tc;     // moment-filter adjoint constants (Gaussian)
-    bool tay_ok;     // Taylor remainder below the bound for this geometry
-    double tay_err;  // host bound on the remainder (relative to sum |terms|)
-    DepConst dc;     // deposit-form forward constants (Gaussian)
-    SvdConst sv;     // the same factorisation for the adjoint K2s (unscaled)
-    double svd_derr; // measured error of its t-derivative (the pose moment), relative to max |dG/dt|
-    bool dep_ok;     // factorisation error below the bound for this geometry
-    int dep_nw;      // K1d warps per CTA (8: two CTAs per SM; 16: one)
-    int dep_g;       // K1d round-accumulator copies (lane l deposits into copy l % dep_g)
-    double dep_err;  // measured error of the factorisation (relative to max |G|)
-    int klass;
-    int fam;  // pa_kernel (KF_*)
-};
-
-// Series order of the moment-filter adjoint per class (must equal TayCfg<LMIN>::M).
-inline int tay_order(int lmin) { return lmin <= 32 ? 7 : (lmin <= 64 ? 5 : 4); }
-
-// Moment-filter constants (K2a/K2b, pa_kernels.cuh) and the bound on the Taylor remainder of
-// e^{dl k}, |dl| <= (a/s)^2/2 (+2%), relative to sum_k C'_k |k|^n, n = 0..2.
+// Moment-filter constants (K2a/K2c, pa_kernels.cuh) and the bound on the Taylor remainder of
+// e^{dl k}, |dl| <= (a/s)^2/2 (+2%), relative to sum_k C'_k |k|^n, n = 0..2: the smallest order
+// M in [4, 8] whose bound is <= 4e-7 (below the direct sum's fp32 rounding, L 2^-24).
 void make_tay(Plan &pl, int lmin, double a, double sig)
 {
-    const int MA = (lmin + 1) / 2, M = tay_order(lmin), NP = M + 3;
+    const int MA = (lmin + 1) / 2;
     const double W = pl.g.ksig_d / a, as2 = a / (sig * sig);
     const double lam0 = as2 * a * (W - MA - 0.5);
     std::memset(&pl.tc, 0, sizeof pl.tc);
+    std::memset(&pl.tf, 0, sizeof pl.tf);
     pl.tc.lam0 = (float)lam0;
     pl.tc.lam_s = (float)as2;
     const int kt = lmin - MA;
     pl.tc.Ckt = (float)std::exp(-(double)kt * kt * a * a / (2.0 * sig * sig));
     for (int m = 0; m < 8; ++m) pl.tc.inv[m] = (float)(1.0 / (m + 1));
     const double dl = 0.5 * as2 * a * 1.02;
-    double fact = 1.0;
-    for (int i = 2; i <= M + 1; ++i) fact *= i;
-    double worst = 0.0;
-    for (int n = 0; n < 3; ++n) {
-        double num = 0.0, den = 0.0;
-        for (int t = 0; t <= lmin; ++t) {
-            const double k = t - MA;
-            const double cp = std::exp(-k * k * a * a / (2.0 * sig * sig)) * std::exp(lam0 * k);
-            const double x = dl * std::fabs(k);
-            num += cp * std::pow(std::fabs(k), n) * std::pow(x, M + 1) / fact * std::exp(x);
-            den += cp * std::pow(std::fabs(k), n);
-            if (t < lmin && n == 0)
-                for (int p = 0; p < NP; ++p) pl.tc.H[t * NP + p] = (float)(cp * std::pow(k, p));
+    auto bound = [&](int M) {
+        double fact = 1.0;
+        for (int i = 2; i <= M + 1; ++i) fact *= i;
+        double worst = 0.0;
+        for (int n = 0; n < 3; ++n) {
+            double num = 0.0, den = 0.0;
+            for (int t = 0; t <= lmin; ++t) {
+                const double k = t - MA;
+                const double cp = std::exp(-k * k * a * a / (2.0 * sig * sig)) * std::exp(lam0 * k);
+                const double x = dl * std::fabs(k);
+                num += cp * std::pow(std::fabs(k), n) * std::pow(x, M + 1) / fact * std::exp(x);
+                den += cp * std::pow(std::fabs(k), n);
+            }
+            worst = std::max(worst, num / den);
         }
-        worst = std::max(worst, num / den);
+        return worst;
+    };
+    pl.tay_ok = false;
+    pl.tay_M = 8;
+    pl.tay_err = 1.0;
+    for (int M = 4; M <= 8; ++M) {
+        const double b = bound(M);
+        pl.tay_M = M;
+        pl.tay_err = b;
+        if (b <= 4e-7) {
+            pl.tay_ok = true;
+            break;
+        }
     }
-    pl.tay_err = worst;
-    pl.tay_ok = lmin * NP <= 768 && worst <= 4e-7;
+    const int NP = pl.tay_M + 3;
+    for (int t = 0; t < lmin; ++t) {
+        const double k = t - MA;
+        const double cp = std::exp(-k * k * a * a / (2.0 * sig * sig)) * std::exp(lam0 * k);
+        for (int p = 0; p < NP; ++p) pl.tf.H[t * NP + p] = (float)(cp * std::pow(k, p));
+    }
 }
 
 // Separable factorisation of the forward pulse for the deposit-form forward K1d (pa_kernels.cuh):
@@ -107,68 +102,28 @@ void make_tay(Plan &pl, int lmin, double a, double sig)
 // ~= sum_{m<R} phi_m(t) psi_m(k).  Chebyshev interpolation of degree 9 in t on 64 nodes, SVD of the
 // (coefficient x tap) matrix by one-sided Jacobi (fp64), phi_m converted to monomials and reduced
 // to 4 coefficients of its parity; the optional last tap (k = LMIN - MA) as a cubic in t.  The
-// error of exactly what the kernel evaluates is measured on a fine grid; > 2e-7 of max|G| (or a
-// geometry outside the class) keeps the direct kernel K1.
+// error of exactly what the kernel evaluates is measured on a fine grid; rank 5 (6 for L_min <= 32,
+// where the adjoint K2s needs the more accurate derivative), raised to 6 / 7 while it misses the
+// bound; > 2e-7 of max|G| at rank 7 keeps the direct kernels.
+#ifndef PA_DEP_MAXERR
+#define PA_DEP_MAXERR 2e-7
+#endif
 void make_dep(Plan &pl, int lmin, double a, double sig)
 {
     constexpr int N = 64, DG = 10;  // nodes, Chebyshev coefficients (degree 9)
-    const int R = lmin <= 32 ? PA_DEP_RANK_SHORT : 5;  // == DepRank<LMIN>::R
     const int MA = (lmin + 1) / 2, KT = lmin - MA, K = lmin;
     const double ks = pl.g.ksig_d;
     const double Dlo = ks - (MA + 1) * a, Dhi = ks - MA * a;
     const double Dc = 0.5 * (Dlo + Dhi), Dw = 0.5 * a * 1.02;
     DepConst &dc = pl.dc;
     std::memset(&dc, 0, sizeof dc);
+    std::memset(&pl.sv, 0, sizeof pl.sv);
     pl.dep_ok = false;
     pl.dep_err = 1.0;
-    pl.svd_derr = 1.0;  // not computed (K2s unavailable) unless the factorisation below succeeds
+    pl.svd_derr = 1.0;
     pl.dep_nw = 0;
     pl.dep_g = 1;
-    if (lmin > 128) return;
-    // warps per CTA: 8 (two CTAs per SM) when two CTAs' accumulators fit in shared memory, else 16.
-    // The fixed-point round accumulator is a ring of nr positions (pos & (nr - 1)): nr >= the positions
-    // one round can touch = the window-base spread of its 2 x 2 x (NW/4 TPR) tile block (centre
-    // distance / a) + a tile's own spread (2 rt / a) + the margins of spanlo/spanhi; nr = NJ (no ring)
-    // when that is not smaller.  The ring also holds the final trace (nt floats).
-    {
-        // accumulator copies: 2 when a tile spans few window positions (h / a < 4: many lanes of a
-        // deposit instruction share a position, and same-address atomics serialise), else 1 (the larger
-        // stride only adds bank conflicts and flush work); PA_DEP_GROUPS=1|2 overrides
-        pl.dep_g = pl.g.h / a < 4.0 ? 2 : 1;
-        if (const char *e = std::getenv("PA_DEP_GROUPS")) pl.dep_g = e[0] == '2' ? 2 : 1;
-        const int CS = (pl.dep_g * (R + 2)) | 1, CF = R + 1, NJ = pl.g.nt + lmin;
-        auto ring = [&](int nw, int &nr, unsigned &nrm) {
-            const int bzt = nw / 4 * PA_DEP_TPR;  // tiles along z in a round's block
-            const double dist = pl.g.h * std::sqrt((double)(TX * TX + TY * TY) + (double)(TZ * (bzt - 1)) * (TZ * (bzt - 1)));
-            const int need = std::max((int)std::ceil((dist + 2.0 * pl.g.rt_d + 2.0 * a) / a) + 16, (pl.g.nt + CS - 1) / CS);
-            int p2 = 64;
-            while (p2 < need) p2 *= 2;
-            if (p2 < NJ) {
-                nr = p2;
-                nrm = (unsigned)(p2 - 1);
-            } else {
-                nr = NJ;
-                nrm = ~0u;
-            }
-        };
-        auto smem = [&](int nr) { return ((size_t)CS * nr + (size_t)CF * NJ) * 4; };
-        const size_t st8 = 8 * 32 * 8 + 4 * (32 + CS) + 64, st16 = 16 * 32 * 8 + 4 * (32 + CS) + 64;  // static smem
-        int nr8, nr16;
-        unsigned m8, m16;
-        ring(8, nr8, m8);
-        ring(16, nr16, m16);
-        if (2 * (smem(nr8) + st8 + 1024) <= 228 * 1024) {
-            pl.dep_nw = 8;
-            dc.nr = nr8;
-            dc.nrm = m8;
-        } else if (smem(nr16) + st16 <= 227 * 1024) {
-            pl.dep_nw = 16;
-            dc.nr = nr16;
-            dc.nrm = m16;
-        } else
-            return;
-    }
-    const int NB = dep_nb(pl.dep_nw), NB0 = NB + 10;  // == DepCfg<LMIN, NW>::NB, NB0
+    pl.dep_R = lmin <= 32 ? 6 : 5;
     auto G = [&](double t, int q) {  // tap q in [0, K): k = q - MA
         const double D = Dc + Dw * t - (double)(q - MA) * a;
         return D * std::exp(-D * D / (2.0 * sig * sig));
@@ -236,73 +191,72 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     for (int p = 2; p < DG; ++p)
         for (int i = 0; i < DG; ++i) Tm[p][i] = (i > 0 ? 2.0 * Tm[p - 1][i - 1] : 0.0) - Tm[p - 2][i];
     // B = V S U^T  =>  G(t, q) ~ sum_c phi_c(t) psi_c(q),  phi_c = sum_p V[p][c] / w_p T_p,  psi_c = A[:, c] (= U s)
-    double mono[DEP_MAXR][DG] = {}, psi[DEP_MAXR][128] = {};
-    for (int m = 0; m < R; ++m) {
-        const int c = ord[m];
-        for (int p = 0; p < DG; ++p) {
-            const double cp = V[p * DG + c] * (p == 0 ? 1.0 / std::sqrt(2.0) : 1.0);
-            for (int i = 0; i < DG; ++i) mono[m][i] += cp * Tm[p][i];
-        }
-        for (int q = 0; q < K; ++q) psi[m][q] = A[(size_t)q * DG + c];
-    }
-    // reduce each phi_m to its parity (m % 2) and 4 coefficients
-    double cfd[DEP_MAXR + 1][4] = {};
-    for (int m = 0; m < R; ++m)
-        for (int r = 0; r < 4; ++r) {
-            const int i = 2 * r + (m & 1);
-            cfd[m][r] = i < DG ? mono[m][i] : 0.0;
-        }
-    auto phi = [&](int m, double t) {
-        const double s2 = t * t;
-        double v = ((cfd[m][3] * s2 + cfd[m][2]) * s2 + cfd[m][1]) * s2 + cfd[m][0];
-        return (m & 1) ? v * t : v;
-    };
-    // X: cubic fit of GX (Chebyshev, degree 3)
-    {
-        double cx[4] = {};
-        for (int p = 0; p < 4; ++p) {
-            double sum = 0.0;
-            for (int i = 0; i < N; ++i) sum += GX(tn[i]) * cheb(p, tn[i]);
-            cx[p] = sum * (p == 0 ? 1.0 : 2.0) / N;
-        }
-        for (int p = 0; p < 4; ++p)
-            for (int i = 0; i < 4; ++i) cfd[R][i] += cx[p] * Tm[p][i];
-    }
-    auto phix = [&](double t) { return ((cfd[R][3] * t + cfd[R][2]) * t + cfd[R][1]) * t + cfd[R][0]; };
-    // error of the truncated factorisation on a fine grid, relative to max |G|
-    double gmax = 0.0, err = 0.0, pmaxv[DEP_MAXR + 1] = {};
-    for (int it = 0; it <= 2000; ++it) {
-        const double t = -1.0 + 2.0 * it / 2000.0;
-        double ph[DEP_MAXR];
+    std::vector<double> psi((size_t)DEP_MAXR * K, 0.0);
+    double cfd[DEP_MAXR + 1][4] = {}, pmaxv[DEP_MAXR + 1] = {};
+    int R = pl.dep_R;
+    for (;;) {
+        double mono[DEP_MAXR][DG] = {};
+        std::memset(cfd, 0, sizeof cfd);
         for (int m = 0; m < R; ++m) {
-            ph[m] = phi(m, t);
-            pmaxv[m] = std::max(pmaxv[m], std::fabs(ph[m]));
+            const int c = ord[m];
+            for (int p = 0; p < DG; ++p) {
+                const double cp = V[p * DG + c] * (p == 0 ? 1.0 / std::sqrt(2.0) : 1.0);
+                for (int i = 0; i < DG; ++i) mono[m][i] += cp * Tm[p][i];
+            }
+            for (int q = 0; q < K; ++q) psi[(size_t)m * K + q] = A[(size_t)q * DG + c];
         }
-        for (int q = 0; q < K; ++q) {
-            const double gv = G(t, q);
-            double ap = 0.0;
-            for (int m = 0; m < R; ++m) ap += ph[m] * psi[m][q];
-            gmax = std::max(gmax, std::fabs(gv));
-            err = std::max(err, std::fabs(gv - ap));
+        // reduce each phi_m to its parity (m % 2) and 4 coefficients
+        for (int m = 0; m < R; ++m)
+            for (int r = 0; r < 4; ++r) {
+                const int i = 2 * r + (m & 1);
+                cfd[m][r] = i < DG ? mono[m][i] : 0.0;
+            }
+        // X: cubic fit of GX (Chebyshev, degree 3)
+        {
+            double cx[4] = {};
+            for (int p = 0; p < 4; ++p) {
+                double sum = 0.0;
+                for (int i = 0; i < N; ++i) sum += GX(tn[i]) * cheb(p, tn[i]);
+                cx[p] = sum * (p == 0 ? 1.0 : 2.0) / N;
+            }
+            for (int p = 0; p < 4; ++p)
+                for (int i = 0; i < 4; ++i) cfd[R][i] += cx[p] * Tm[p][i];
         }
-        const double xv = phix(t);
-        pmaxv[R] = std::max(pmaxv[R], std::fabs(xv));
-        err = std::max(err, std::fabs(GX(t) - xv));
+        auto phi = [&](int m, double t) {
+            const double s2 = t * t;
+            double v = ((cfd[m][3] * s2 + cfd[m][2]) * s2 + cfd[m][1]) * s2 + cfd[m][0];
+            return (m & 1) ? v * t : v;
+        };
+        auto phix = [&](double t) { return ((cfd[R][3] * t + cfd[R][2]) * t + cfd[R][1]) * t + cfd[R][0]; };
+        // error of the truncated factorisation on a fine grid, relative to max |G|
+        double gmax = 0.0, err = 0.0;
+        std::memset(pmaxv, 0, sizeof pmaxv);
+        for (int it = 0; it <= 2000; ++it) {
+            const double t = -1.0 + 2.0 * it / 2000.0;
+            double ph[DEP_MAXR];
+            for (int m = 0; m < R; ++m) {
+                ph[m] = phi(m, t);
+                pmaxv[m] = std::max(pmaxv[m], std::fabs(ph[m]));
+            }
+            for (int q = 0; q < K; ++q) {
+                const double gv = G(t, q);
+                double ap = 0.0;
+                for (int m = 0; m < R; ++m) ap += ph[m] * psi[(size_t)m * K + q];
+                gmax = std::max(gmax, std::fabs(gv));
+                err = std::max(err, std::fabs(gv - ap));
+            }
+            const double xv = phix(t);
+            pmaxv[R] = std::max(pmaxv[R], std::fabs(xv));
+            err = std::max(err, std::fabs(GX(t) - xv));
+        }
+        pl.dep_err = err / gmax;
+        if (pl.dep_err <= PA_DEP_MAXERR || R == DEP_MAXR) break;
+        ++R;  // the rank missed the bound: one more term
     }
-    pl.dep_err = err / gmax;
-    // fixed-point scales: |c| <= 1 (P / Pmax, r_lo / r), |n| <= 2^NB (channel 0: 2^NB0)
-    for (int m = 0; m <= R; ++m) {
-        const double S = std::ldexp(1.0, m == 0 ? NB0 : NB) / (pmaxv[m] * (1.0 + 1e-3) + 1e-300);
-        for (int r = 0; r < 4; ++r) dc.cf2[m][r] = make_float2((float)(cfd[m][r] * S), (float)(cfd[m][r] * S));
-        dc.dec[m] = (float)(0.5 / S);
-    }
-    // psi[m][q-1] = psi_m(k = OFF - q), tap index OFF - q + MA = LMIN - q
-    for (int m = 0; m < R; ++m)
-        for (int q = 1; q <= lmin; ++q) dc.psi[m][q - 1] = (float)psi[m][lmin - q];
+    pl.dep_R = R;
+    pl.dep_ok = pl.dep_err <= PA_DEP_MAXERR;
     // the adjoint K2s: the same basis, unscaled, and the error of the derivative d/dt (pose moment)
     SvdConst &svc = pl.sv;
-    std::memset(&svc, 0, sizeof svc);
-    std::memcpy(svc.psi, dc.psi, sizeof svc.psi);
     for (int m = 0; m <= R; ++m)
         for (int r = 0; r < 4; ++r) svc.c[m][r] = (float)cfd[m][r];
     {
@@ -322,7 +276,7 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
             for (int q = 0; q < K; ++q) {
                 const double dg = (G(t + hstep, q) - G(t - hstep, q)) / (2.0 * hstep);
                 double ap = 0.0;
-                for (int m = 0; m < R; ++m) ap += dphi(m, t) * psi[m][q];
+                for (int m = 0; m < R; ++m) ap += dphi(m, t) * psi[(size_t)m * K + q];
                 dmax = std::max(dmax, std::fabs(dg));
                 derr = std::max(derr, std::fabs(dg - ap));
             }
@@ -331,23 +285,70 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
         }
         pl.svd_derr = derr / dmax;
     }
+    // psi[m][q-1] = psi_m(k = OFF - q), tap index OFF - q + MA = LMIN - q
+    for (int m = 0; m < R; ++m)
+        for (int q = 1; q <= lmin; ++q) {
+            dc.psi[m][q - 1] = (float)psi[(size_t)m * K + (lmin - q)];
+            svc.psi[m][q - 1] = dc.psi[m][q - 1];
+        }
     // t = (D_m - Dc)/Dw with D_m = drel + CA - clo a - MA a
-    dc.tA = (float)(1.0 / Dw);
-    dc.tB = (float)(a / Dw);
-    dc.tC = (float)((-MA * a - Dc) / Dw);
-    svc.tA = dc.tA;
-    svc.tB = dc.tB;
-    svc.tC = dc.tC;
+    dc.tA = svc.tA = (float)(1.0 / Dw);
+    dc.tB = svc.tB = (float)(a / Dw);
+    dc.tC = svc.tC = (float)((-MA * a - Dc) / Dw);
     svc.invDw = (float)(1.0 / Dw);
     // r_lo(pos) = c t0 + j_m a + (ks - (MA+1) a) - 0.05 a, j_m = pos - OFF
     dc.W0 = (float)(pl.g.c * pl.g.t0 + ks - (MA + 1) * a - 0.05 * a - (double)KT * a);
-#ifndef PA_DEP_MAXERR
-#define PA_DEP_MAXERR 2e-7
-#endif
-    pl.dep_ok = pl.dep_err <= PA_DEP_MAXERR;
+    // K1d launch shape: warps per CTA 8 (two CTAs per SM) when two CTAs' accumulators fit in shared memory,
+    // else 16.  The fixed-point round accumulator is a ring of nr positions (pos & (nr - 1)): nr >= the
+    // positions one round can touch = the window-base spread of its 2 x 2 x (NW/4 TPR) tile block (centre
+    // distance / a) + a tile's own spread (2 rt / a) + the margins of spanlo/spanhi; nr = NJ (no ring) when
+    // that is not smaller.  The ring also holds the final trace (nt floats).  Accumulator copies: 2 when a
+    // tile spans few window positions (h / a < 4: many lanes of a deposit instruction share a position, and
+    // same-address atomics serialise), else 1.
+    pl.dep_g = pl.g.h / a < 4.0 ? 2 : 1;
+    const int CS = (pl.dep_g * (R + 2)) | 1, CF = R + 1, NJ = pl.g.nt + lmin;
+    auto ring = [&](int nw, int &nr, unsigned &nrm) {
+        const int bzt = nw / 4 * PA_DEP_TPR;  // tiles along z in a round's block
+        const double dist = pl.g.h * std::sqrt((double)(TX * TX + TY * TY) + (double)(TZ * (bzt - 1)) * (TZ * (bzt - 1)));
+        const int need = std::max((int)std::ceil((dist + 2.0 * pl.g.rt_d + 2.0 * a) / a) + 16, (pl.g.nt + CS - 1) / CS);
+        int p2 = 64;
+        while (p2 < need) p2 *= 2;
+        if (p2 < NJ) {
+            nr = p2;
+            nrm = (unsigned)(p2 - 1);
+        } else {
+            nr = NJ;
+            nrm = ~0u;
+        }
+    };
+    auto smem = [&](int nr) { return ((size_t)CS * nr + (size_t)CF * NJ) * 4; };
+    const size_t st8 = 8 * 32 * 8 + 4 * (32 + CS) + 64, st16 = 16 * 32 * 8 + 4 * (32 + CS) + 64;  // static smem
+    int nr8, nr16;
+    unsigned m8, m16;
+    ring(8, nr8, m8);
+    ring(16, nr16, m16);
+    if (2 * (smem(nr8) + st8 + 1024) <= 228 * 1024) {
+        pl.dep_nw = 8;
+        dc.nr = nr8;
+        dc.nrm = m8;
+    } else if (smem(nr16) + st16 <= 227 * 1024) {
+        pl.dep_nw = 16;
+        dc.nr = nr16;
+        dc.nrm = m16;
+    } else {
+        pl.dep_nw = 0;  // the row accumulators do not fit: the direct forward K1
+        return;
+    }
+    const int NB = dep_nb(pl.dep_nw), NB0 = NB + 10;  // == DepCfg<R, NW>::NB, NB0
+    // fixed-point scales: |c| <= 1 (P / Pmax, r_lo / r), |n| <= 2^NB (channel 0: 2^NB0)
+    for (int m = 0; m <= R; ++m) {
+        const double S = std::ldexp(1.0, m == 0 ? NB0 : NB) / (pmaxv[m] * (1.0 + 1e-3) + 1e-300);
+        for (int r = 0; r < 4; ++r) dc.cf2[m][r] = make_float2((float)(cfd[m][r] * S), (float)(cfd[m][r] * S));
+        dc.dec[m] = (float)(0.5 / S);
+    }
 }
 
-pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &pl)
+pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int policy, Plan &pl)
 {
     if (!grid || !acq) return fail(PA_EINVAL, "null grid/acq");
     if (grid->nx <= 0 || grid->ny <= 0 || grid->nz <= 0) return fail(PA_EINVAL, "grid dims must be positive");
@@ -367,6 +368,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     if (E < 1) return fail(PA_ESHAPE, "E must be >= 1");
     if (F < 0) return fail(PA_ESHAPE, "F must be >= 0");
     Geo &g = pl.g;
+    std::memset(&g, 0, sizeof g);
     g.nx = grid->nx;
     g.ny = grid->ny;
     g.nz = grid->nz;
@@ -405,14 +407,19 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     g.ls = (float)(1.4426950408889634 / sig);
     g.nu = acq->kernel == PA_KERNEL_POW ? acq->nu : 0.0f;
     pl.fam = acq->kernel;
+    pl.policy = policy;
 
     const double K2 = 2.0 * g.ksig_d / a;
-    const int wmin = (int)std::floor(K2);
+    if (!(K2 < 1e6)) return fail(PA_EINVAL, "window 2 kappa sigma / (c dt) = %g samples is too long", K2);
+    const int wmin = (int)std::floor(K2);  // L_min: every window has L_min or L_min + 1 samples
+    g.lmin = wmin;
+    g.mA = (wmin + 1) / 2;
     const int o_need = (int)std::floor(std::sqrt(3.0) * g.h / a) + 2;
     const int span_need = (int)std::ceil(2.0 * g.rt_d / a) + 2;  // max lane window-base spread in a tile
     const int seg_need = (int)std::ceil(2.0 * g.rt_d / a) + 5 + (wmin + 1);
+    // direct kernels (K1/K2): a compiled class must match L_min and hold the geometry's spreads
     pl.klass = -1;
-    for (int k = 0; k < (int)(sizeof kClasses / sizeof kClasses[0]); ++k) {
+    for (int k = 0; k < kNumClasses; ++k) {
         const Klass &c = kClasses[k];
         if (c.lmin == wmin && o_need <= c.omax && span_need <= c.span && seg_need <= c.seg) {
             pl.klass = k;
@@ -421,9 +428,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
     }
     if (pl.klass >= 0) {
         const Klass &c = kClasses[pl.klass];
-        const double kc = g.ksig_d / a;  // window half-width in samples
         g.mF = ((c.lmin + c.omax) / 2) & ~1;  // == FwdMid<LMIN,OMAX>::m
-        g.mA = (c.lmin + 1) / 2;  // == AdjMid<LMIN>::m
         const double be = a * a / (2.0 * sig * sig);
         const double as = a / sig;  // exponential family: K_i = exp((i - m) a / s)
         for (int k = 0; k < 64; ++k) {
@@ -437,8 +442,6 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
             }
             pl.fc.I2[k] = make_float2((float)(-2 * k), (float)(-2 * k - 1));
         }
-        make_tay(pl, c.lmin, a, sig);
-        make_dep(pl, c.lmin, a, sig);
         for (int i = 0; i < 128; ++i) {
             const double ka = i - g.mA;
             if (pl.fam == PA_KERNEL_EXP) {
@@ -453,11 +456,40 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &
             }
         }
     }
-    if (pl.klass < 0)
+    // Gaussian fast path (runtime window length L_min in [FAST_LMIN, PA_LMAX]): K1d, K2a/K2c, K2s
+    pl.tay_ok = pl.dep_ok = false;
+    pl.tay_M = 0;
+    pl.tay_err = pl.dep_err = pl.svd_derr = 1.0;
+    pl.dep_R = 0;
+    pl.dep_nw = 0;
+    pl.dep_g = 1;
+    const bool fast = pl.fam == KF_GAUSS && wmin >= FAST_LMIN && wmin <= PA_LMAX;
+    if (fast) {
+        make_tay(pl, wmin, a, sig);
+        make_dep(pl, wmin, a, sig);
+    }
+    // the kernels this geometry runs (policy bits force / prefer alternatives; pa.h PA_POLICY_*)
+    const bool dep_avail = fast && pl.dep_ok && pl.dep_nw > 0;
+    const bool svd_avail = fast && pl.dep_ok && pl.svd_derr <= 1e-5;
+    const bool tay_avail = fast && pl.tay_ok;
+    pl.fwd_dep = dep_avail && !(policy & PA_POLICY_FWD_DIRECT);
+    if (policy & PA_POLICY_ADJ_DIRECT) pl.adj = ADJ_DIRECT;
+    else if ((policy & PA_POLICY_ADJ_SVD) && svd_avail) pl.adj = ADJ_SVD;
+    else if ((policy & PA_POLICY_ADJ_TAYLOR) && tay_avail) pl.adj = ADJ_TAY;
+    // default: the Taylor form, except where it needs 48-B filter records (M >= 6, short windows) and the
+    // rank-R basis is accurate enough (K2s measured 5% faster for the C5 class)
+    else if (svd_avail && (!tay_avail || pl.tay_M >= 6)) pl.adj = ADJ_SVD;
+    else if (tay_avail) pl.adj = ADJ_TAY;
+    else pl.adj = ADJ_DIRECT;
+    if ((!pl.fwd_dep || pl.adj == ADJ_DIRECT) && pl.klass < 0)
         return fail(PA_EUNSUPPORTED,
-                    "window class not compiled: L_min=%d (2 kappa sigma/(c dt)=%.4f), cluster spread %d, tile span %d, "
-                    "segment %d; compiled classes L_min in {53, 26, 106}",
-                    wmin, K2, o_need, span_need, seg_need);
+                    "no kernel for this geometry: L_min=%d (2 kappa sigma/(c dt)=%.4f), kernel family %d, %s; the direct "
+                    "kernels are compiled for L_min in {53, 26, 106} (cluster spread %d, tile span %d, segment %d)",
+                    wmin, K2, pl.fam,
+                    !fast ? "outside the Gaussian fast path (Gaussian kernel, 12 <= L_min <= 160)"
+                          : (!pl.fwd_dep ? "the deposit forward is unavailable or not selected"
+                                         : "the moment-filter adjoints are unavailable or not selected"),
+                    o_need, span_need, seg_need);
     return PA_OK;
 }
 
@@ -632,11 +664,13 @@ __global__ void k_euler_grad(const float *__restrict__ grad_pose, const float *_
     }
 }
 
-// a8 — Adam with optional clamp x >= 0.
+// a8 — Adam with optional clamp x >= 0.  `ok` (nullable): the step's
+// degenerate-geometry verdict (~0 = none); a degenerate step leaves x, m and v untouched.
 __global__ void k_adam(float *__restrict__ x, float *__restrict__ m, float *__restrict__ v,
                        const float *__restrict__ g, long long n, float lr, float b1, float b2, float eps, float bc1,
-                       float bc2, int clamp)
+                       float bc2, int clamp, const unsigned long long *__restrict__ ok)
 {
+    if (ok && *ok != ~0ull) return;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const float gi = g[i];
         const float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -651,10 +685,10 @@ __global__ void k_adam(float *__restrict__ x, float *__restrict__ m, float *__re
 
 __global__ void k_adam_pose(float *__restrict__ x, float *__restrict__ m, float *__restrict__ v,
                             const float *__restrict__ g, int F, float lr_rot, float lr_t, float b1, float b2, float eps,
-                            float bc1, float bc2)
+                            float bc1, float bc2, const unsigned long long *__restrict__ ok)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 6 * F) return;
+    if (i >= 6 * F || (ok && *ok != ~0ull)) return;
     const float lr = (i % 6) < 3 ? lr_rot : lr_t;
     const float gi = g[i];
     const float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -759,14 +793,60 @@ __global__ void k_loss_rows(int kind, const float *__restrict__ y, const float *
 struct pa_ctx {
     int device = 0;
     int nsm = 148;
+    int policy = PA_POLICY_DEFAULT;
     void *ws = nullptr;
     size_t ws_bytes = 0;
-    void *fws = nullptr;  // moment filters of one frame chunk (adjoint K2a -> K2b)
+    void *fws = nullptr;  // moment filters of one frame chunk (adjoint K2a -> K2c / K2s)
     size_t fws_bytes = 0;
-    unsigned long long *dflag = nullptr;
+    unsigned long long *dflag = nullptr;  // [0] synchronous degenerate check, [1] K1d max|p0|, [2] pa_step check
+    unsigned long long *hflag = nullptr;  // pinned host copy of the pa_step verdict
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_chk = nullptr;         // recorded after the pa_step verdict's D2H copy
     bool ev_fwd = false, ev_adj = false;
+    bool chk_pending = false;             // a pa_step verdict is in flight / not yet read
+    int chk_E = 1;                        // elements of that step (to decode the verdict)
 };
+
+namespace pa {
+pa_status ctx_filter_ws(pa_ctx *ctx, size_t bytes, float **out)
+{
+    if (bytes > ctx->fws_bytes) {
+        if (ctx->fws) cudaFree(ctx->fws);
+        ctx->fws = nullptr;
+        ctx->fws_bytes = 0;
+        if (cudaMalloc(&ctx->fws, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(PA_ENOMEM, "filter workspace allocation of %zu bytes failed", bytes);
+        }
+        ctx->fws_bytes = bytes;
+    }
+    *out = static_cast<float *>(ctx->fws);
+    return PA_OK;
+}
+int ctx_nsm(const pa_ctx *ctx) { return ctx->nsm; }
+unsigned *ctx_pmax(pa_ctx *ctx) { return reinterpret_cast<unsigned *>(ctx->dflag + 1); }
+
+pa_status launch_forward_direct(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out,
+                                int mode, const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
+{
+    switch (pl.fam) {
+    case KF_EXP: return launch_forward_direct_exp(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    case KF_POW: return launch_forward_direct_pow(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    default: return launch_forward_direct_gauss(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    }
+}
+
+pa_status launch_adjoint_direct(pa_ctx *ctx, const Plan &pl, bool pose, bool adj, const float *poses,
+                                const float *tmpl, const float *p0, const float *cot, float *grad_p0, float *partial,
+                                AdjLaunch &L, bool dry, cudaStream_t st)
+{
+    switch (pl.fam) {
+    case KF_EXP: return launch_adjoint_direct_exp(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    case KF_POW: return launch_adjoint_direct_pow(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    default: return launch_adjoint_direct_gauss(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    }
+}
+}  // namespace pa
 
 namespace {
 
@@ -783,20 +863,6 @@ struct DevGuard {
     }
 };
 
-pa_status fws_reserve(pa_ctx *ctx, size_t bytes)
-{
-    if (bytes <= ctx->fws_bytes) return PA_OK;
-    if (ctx->fws) cudaFree(ctx->fws);
-    ctx->fws = nullptr;
-    ctx->fws_bytes = 0;
-    if (cudaMalloc(&ctx->fws, bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(PA_ENOMEM, "filter workspace allocation of %zu bytes failed", bytes);
-    }
-    ctx->fws_bytes = bytes;
-    return PA_OK;
-}
-
 pa_status ws_reserve(pa_ctx *ctx, size_t bytes)
 {
     if (bytes <= ctx->ws_bytes) return PA_OK;
@@ -812,12 +878,19 @@ pa_status ws_reserve(pa_ctx *ctx, size_t bytes)
     return PA_OK;
 }
 
-inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+pa_status degenerate_message(unsigned long long best, int E)
+{
+    const int fe = (int)(best >> 32);
+    const unsigned v = (unsigned)(best & 0xffffffffu);
+    return fail(PA_EDEGENERATE, "degenerate geometry: frame %d element %d lies within 1e-6 mm of voxel (%u,%u,%u)",
+                fe / E, fe % E, v & 0x3ff, (v >> 10) & 0x3ff, (v >> 20) & 0x3ff);
+}
 
+// Synchronous degenerate-geometry check of the standalone operator calls (R10; pa.h): the verdict is read
+// back before anything else is enqueued.
 pa_status check_degenerate(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, cudaStream_t st)
 {
-    const unsigned long long init = ~0ull;
-    CUDA_TRY(cudaMemcpyAsync(ctx->dflag, &init, sizeof init, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(ctx->dflag, 0xff, sizeof(unsigned long long), st));
     const int n = pl.g.F * pl.g.E;
     ++g_nlaunch;
     k_check<<<(n + 127) / 128, 128, 0, st>>>(pl.g, poses, tmpl, ctx->dflag);
@@ -825,315 +898,43 @@ pa_status check_degenerate(pa_ctx *ctx, const Plan &pl, const float *poses, cons
     unsigned long long best = 0;
     CUDA_TRY(cudaMemcpyAsync(&best, ctx->dflag, sizeof best, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (best != ~0ull) {
-        const int fe = (int)(best >> 32);
-        const unsigned v = (unsigned)(best & 0xffffffffu);
-        return fail(PA_EDEGENERATE, "degenerate geometry: frame %d element %d lies within 1e-6 mm of voxel (%u,%u,%u)",
-                    fe / pl.g.E, fe % pl.g.E, v & 0x3ff, (v >> 10) & 0x3ff, (v >> 20) & 0x3ff);
-    }
+    if (best != ~0ull) return degenerate_message(best, pl.g.E);
     return PA_OK;
 }
 
-// ---------------------------------------------------------------- launchers per class
-template <int LMIN, int OMAX, int SPAN, int FAM>
-pa_status launch_forward_t(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
-                           const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
+// The same check inside pa_step, without a host synchronisation: the verdict stays on the device (the
+// Adam kernels of the step skip their update when it is set) and is copied to pinned host memory; the
+// host reads it in pa_step_status.
+pa_status check_degenerate_async(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, cudaStream_t st)
 {
-    using C = FwdCfg<LMIN, OMAX, SPAN>;
-    const size_t smem = (size_t)FWD_WARPS * C::warp_floats(pl.g.nt) * sizeof(float);
-    if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "nt=%d too long for the forward kernel's shared memory", pl.g.nt);
-    auto kern = k_forward<LMIN, OMAX, SPAN, FAM>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    unsigned long long *flag = ctx->dflag + 2;
+    CUDA_TRY(cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), st));
+    const int n = pl.g.F * pl.g.E;
     ++g_nlaunch;
-    kern<<<pl.g.F * pl.g.E, FWD_WARPS * 32, smem, st>>>(pl.g, pl.fc, poses, tmpl, p0, out, mode, meas, mask, rowloss);
+    k_check<<<(n + 127) / 128, 128, 0, st>>>(pl.g, poses, tmpl, flag);
     CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(ctx->hflag, flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(ctx->ev_chk, st));
+    ctx->chk_pending = true;
+    ctx->chk_E = pl.g.E;
     return PA_OK;
-}
-
-inline bool fwd_direct_forced()
-{
-    const char *e = std::getenv("PA_FWD_DIRECT");
-    return e != nullptr && e[0] == '1';
-}
-
-// Deposit-form forward (Gaussian): |p0| max (the fixed-point normalisation), then K1d.
-template <int LMIN, int NW, int NG>
-pa_status launch_forward_dep(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
-                             float *out, int mode, const float *meas, const uint8_t *mask, double *rowloss,
-                             cudaStream_t st)
-{
-    const size_t smem = DepCfg<LMIN, NW, NG>::smem_bytes(pl.g.nt, pl.dc.nr);
-    auto kern = k_fwd_dep<LMIN, NW, NG>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    unsigned *pm = reinterpret_cast<unsigned *>(ctx->dflag + 1);
-    CUDA_TRY(cudaMemsetAsync(pm, 0, sizeof(unsigned), st));
-    const long long nvox = (long long)pl.g.nx * pl.g.ny * pl.g.nz;
-    ++g_nlaunch;
-    k_absmax<<<ctx->nsm * 4, 256, 0, st>>>(p0, nvox, pm);
-    CUDA_TRY(cudaGetLastError());
-    ++g_nlaunch;
-    kern<<<pl.g.F * pl.g.E, NW * 32, smem, st>>>(pl.g, pl.dc, poses, tmpl, p0, pm, out, mode, meas, mask, rowloss);
-    CUDA_TRY(cudaGetLastError());
-    return PA_OK;
-}
-
-template <int LMIN>
-pa_status launch_forward_dep_c(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
-                               float *out, int mode, const float *meas, const uint8_t *mask, double *rowloss,
-                               cudaStream_t st)
-{
-    if (pl.dep_g == 2) {
-        if (pl.dep_nw == 8) return launch_forward_dep<LMIN, 8, 2>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-        return launch_forward_dep<LMIN, 16, 2>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    }
-    if (pl.dep_nw == 8) return launch_forward_dep<LMIN, 8, 1>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    return launch_forward_dep<LMIN, 16, 1>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-}
-
-inline bool use_dep(const Plan &pl) { return pl.fam == KF_GAUSS && pl.dep_ok && pl.dep_nw > 0 && !fwd_direct_forced(); }
-
-template <int FAM>
-pa_status launch_forward_f(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out, int mode,
-                           const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
-{
-    switch (pl.klass) {
-    case 0: return launch_forward_t<53, 11, 58, FAM>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    case 1: return launch_forward_t<26, 6, 30, FAM>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    default: return launch_forward_t<106, 21, 114, FAM>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    }
 }
 
 pa_status launch_forward(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out,
                          int mode, const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
 {
-    if (use_dep(pl)) {
-        switch (pl.klass) {
-        case 0: return launch_forward_dep_c<53>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-        case 1: return launch_forward_dep_c<26>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-        default: return launch_forward_dep_c<106>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-        }
-    }
-    switch (pl.fam) {
-    case KF_EXP: return launch_forward_f<KF_EXP>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    case KF_POW: return launch_forward_f<KF_POW>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    default: return launch_forward_f<KF_GAUSS>(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    }
+    if (pl.fwd_dep) return launch_forward_dep(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    return launch_forward_direct(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
 }
 
-struct AdjLaunch {
-    int P = 0, Fc = 0;
-    size_t smem = 0;
-};
-
-// Moment-filter adjoint (Gaussian): per frame chunk, K2a (filters, L2-resident) then K2b.
-template <int LMIN, bool POSE, bool ADJ>
-pa_status launch_adjoint_tay(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
-                             const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
+pa_status launch_adjoint(pa_ctx *ctx, const Plan &pl, bool pose, bool adj, const float *poses, const float *tmpl,
+                         const float *p0, const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry,
+                         cudaStream_t st)
 {
-    using T = TayCfg<LMIN>;
-    const int E = pl.g.E, F = pl.g.F, NJ = pl.g.nt + LMIN;
-    const size_t per_frame = (size_t)E * NJ * T::NF * sizeof(float);
-    int Fc = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t(48) << 20) / per_frame));
-    // K2c (two voxels per thread, packed) unless PA_ADJ_TAY1=1 selects K2b (one voxel per thread)
-    const char *t1 = std::getenv("PA_ADJ_TAY1");
-    const bool v2 = !(t1 != nullptr && t1[0] == '1');
-    const size_t nanc = v2 ? 2 : 1;  // anchor sets per CTA
-    auto smem_of = [&](int fc) {
-        return ((size_t)E * 12 * nanc + (size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
-    };
-    while (Fc > 1 && smem_of(Fc) > 113 * 1024) --Fc;
-    Fc = std::min(Fc, std::max(1, 65535 / E));  // K2a grid.y = Fc E
-    Fc = std::min(Fc, F > 0 ? F : 1);
-    const size_t smem = smem_of(Fc);
-    if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "E=%d too large for the adjoint kernel's shared memory", E);
-    auto kern = v2 ? k_adjoint_tay2<LMIN, POSE, ADJ> : k_adjoint_tay<LMIN, POSE, ADJ>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
-    if (occ < 1) occ = 1;
-    int P = occ * ctx->nsm;
-    const int nwork = v2 ? pl.g.ntx * pl.g.nty * ((pl.g.ntz + 1) / 2) : pl.g.ntiles;  // tile pairs / tiles
-    if (P > nwork) P = nwork;
-    L.P = P;
-    L.Fc = Fc;
-    L.smem = smem;
-    if (dry) return PA_OK;
-    pa_status s;
-    if ((s = fws_reserve(ctx, (size_t)Fc * per_frame))) return s;
-    float *Fg = static_cast<float *>(ctx->fws);
-    // PA_DEBUG_CHUNKS=1: per-kernel device time of the chunk loop on stderr (diagnostic)
-    const char *dbg = std::getenv("PA_DEBUG_CHUNKS");
-    std::vector<cudaEvent_t> evs;
-    for (int f0 = 0; f0 < F; f0 += Fc) {
-        const int fn = std::min(Fc, F - f0);
-        if (dbg) {
-            evs.emplace_back();
-            cudaEventCreate(&evs.back());
-            cudaEventRecord(evs.back(), st);
-        }
-        ++g_nlaunch;
-        k_adj_filter<LMIN><<<dim3((NJ + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.tc, cot, f0, fn, Fg);
-        CUDA_TRY(cudaGetLastError());
-        if (dbg) {
-            evs.emplace_back();
-            cudaEventCreate(&evs.back());
-            cudaEventRecord(evs.back(), st);
-        }
-        ++g_nlaunch;
-        kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.tc, poses, tmpl, p0, cot, Fg, grad_p0, partial, f0, fn);
-        CUDA_TRY(cudaGetLastError());
-    }
-    if (dbg) {
-        evs.emplace_back();
-        cudaEventCreate(&evs.back());
-        cudaEventRecord(evs.back(), st);
-        cudaEventSynchronize(evs.back());
-        double ta = 0, tb = 0;
-        for (size_t i = 0; i + 2 < evs.size() + 1 && i + 1 < evs.size(); i += 2) {
-            float x = 0, y = 0;
-            cudaEventElapsedTime(&x, evs[i], evs[i + 1]);
-            if (i + 2 < evs.size()) cudaEventElapsedTime(&y, evs[i + 1], evs[i + 2]);
-            ta += x;
-            tb += y;
-        }
-        std::fprintf(stderr, "[pa] adjoint chunks=%zu Fc=%d P=%d smem=%zu: K2a %.3f ms, K2b %.3f ms\n", evs.size() / 2, Fc, P,
-                     smem, ta, tb);
-        for (auto e : evs) cudaEventDestroy(e);
-    }
-    return PA_OK;
-}
-
-// The adjoint in the forward's basis (K2s): per frame chunk, K2s-a (filter records, L2-resident) then K2s.
-template <int LMIN, bool POSE, bool ADJ>
-pa_status launch_adjoint_svd(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
-                             const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
-{
-    const int E = pl.g.E, F = pl.g.F, NJ = pl.g.nt + LMIN;
-    const size_t per_frame = (size_t)E * NJ * SVD_NF * sizeof(float);
-    int Fc = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t(48) << 20) / per_frame));
-    auto smem_of = [&](int fc) {
-        return ((size_t)E * 12 * 2 + (size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
-    };
-    while (Fc > 1 && smem_of(Fc) > 113 * 1024) --Fc;
-    Fc = std::min(Fc, std::max(1, 65535 / E));  // filter grid.y = Fc E
-    Fc = std::min(Fc, F > 0 ? F : 1);
-    const size_t smem = smem_of(Fc);
-    if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "E=%d too large for the adjoint kernel's shared memory", E);
-    auto kern = k_adjoint_svd<LMIN, POSE, ADJ>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
-    if (occ < 1) occ = 1;
-    int P = occ * ctx->nsm;
-    const int nwork = pl.g.ntx * pl.g.nty * ((pl.g.ntz + 1) / 2);  // tile pairs
-    if (P > nwork) P = nwork;
-    L.P = P;
-    L.Fc = Fc;
-    L.smem = smem;
-    if (dry) return PA_OK;
-    pa_status s;
-    if ((s = fws_reserve(ctx, (size_t)Fc * per_frame))) return s;
-    float *Fg = static_cast<float *>(ctx->fws);
-    for (int f0 = 0; f0 < F; f0 += Fc) {
-        const int fn = std::min(Fc, F - f0);
-        ++g_nlaunch;
-        k_adj_svd_filter<LMIN><<<dim3((NJ + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.sv, cot, f0, fn, Fg);
-        CUDA_TRY(cudaGetLastError());
-        ++g_nlaunch;
-        kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.sv, poses, tmpl, p0, Fg, grad_p0, partial, f0, fn);
-        CUDA_TRY(cudaGetLastError());
-    }
-    return PA_OK;
-}
-
-// K2s is opt-in (PA_ADJ_SVD=1): measured slower than K2c at C4 (150.5 vs 142.7 ms per 16 frames —
-// the polynomial evaluation costs more FFMAs than the Taylor series saves in exp/loads)
-inline bool adj_svd_selected()
-{
-    const char *e = std::getenv("PA_ADJ_SVD");
-    return e != nullptr && e[0] == '1';
-}
-
-// ... except for the short-window class (L_min <= 32), where the Taylor form needs M = 7 (48-B filter
-// records, three 128-bit loads) and K2s measured 5% faster (C5, 8 frames: 600 vs 633 ms)
-inline bool use_adj_svd(const Plan &pl)
-{
-    const char *t = std::getenv("PA_ADJ_TAYLOR");
-    const bool taylor = t != nullptr && t[0] == '1';
-    const bool pref = adj_svd_selected() || (kClasses[pl.klass].lmin <= 32 && !taylor);
-    return pl.fam == KF_GAUSS && pl.dep_ok && pl.svd_derr <= 1e-5 && pref;
-}
-
-inline bool adj_direct_forced()
-{
-    const char *e = std::getenv("PA_ADJ_DIRECT");
-    return e != nullptr && e[0] == '1';
-}
-
-template <int LMIN, int SEG, bool POSE, bool ADJ, int FAM>
-pa_status launch_adjoint_t(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
-                           const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
-{
-    if constexpr (FAM == KF_GAUSS) {
-        if (!adj_direct_forced()) {
-            if (use_adj_svd(pl))
-                return launch_adjoint_svd<LMIN, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-            if (pl.tay_ok)
-                return launch_adjoint_tay<LMIN, POSE, ADJ>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-        }
-    }
-    auto kern = k_adjoint<LMIN, SEG, POSE, ADJ, FAM>;
-    const int E = pl.g.E, F = pl.g.F;
-    int Fc = POSE ? 64 : F;
-    size_t smem = AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float);
-    // prefer 2 CTAs/SM with a frame chunk >= 8, else the largest chunk that fits one CTA/SM
-    const size_t two = 113 * 1024, one = 227 * 1024;
-    if (POSE) {
-        Fc = 64;
-        while (Fc > 8 && AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float) > two) Fc -= 4;
-        if (AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float) > two) {
-            Fc = 64;
-            while (Fc > 1 && AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float) > one) Fc -= 1;
-        }
-        Fc = Fc < F ? Fc : (F > 0 ? F : 1);
-        smem = AdjCfg::smem_floats(E, SEG, Fc, POSE) * sizeof(float);
-    }
-    if (smem > one) return fail(PA_EUNSUPPORTED, "E=%d too large for the adjoint kernel's shared memory", E);
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
-    if (occ < 1) occ = 1;
-    int P = occ * ctx->nsm;
-    if (P > pl.g.ntiles) P = pl.g.ntiles;
-    L.P = P;
-    L.Fc = Fc;
-    L.smem = smem;
-    if (dry) return PA_OK;
-    ++g_nlaunch;
-    kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.ac, poses, tmpl, p0, cot, grad_p0, partial, Fc);
-    CUDA_TRY(cudaGetLastError());
-    return PA_OK;
-}
-
-template <bool POSE, bool ADJ, int FAM>
-pa_status launch_adjoint_f(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
-                           const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
-{
-    switch (pl.klass) {
-    case 0: return launch_adjoint_t<53, 128, POSE, ADJ, FAM>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    case 1: return launch_adjoint_t<26, 64, POSE, ADJ, FAM>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    default: return launch_adjoint_t<106, 256, POSE, ADJ, FAM>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    }
-}
-
-template <bool POSE, bool ADJ>
-pa_status launch_adjoint(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
-                         const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
-{
-    switch (pl.fam) {
-    case KF_EXP: return launch_adjoint_f<POSE, ADJ, KF_EXP>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    case KF_POW: return launch_adjoint_f<POSE, ADJ, KF_POW>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    default: return launch_adjoint_f<POSE, ADJ, KF_GAUSS>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    switch (pl.adj) {
+    case ADJ_TAY: return launch_adjoint_tay(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    case ADJ_SVD: return launch_adjoint_svd(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    default: return launch_adjoint_direct(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
     }
 }
 
@@ -1147,13 +948,11 @@ pa_status check_ptrs(std::initializer_list<const void *> ps)
 // Fused adjoint+pose core used by pa_pose_grad / pa_adjoint_pose / pa_step.
 pa_status adjoint_pose_core(pa_ctx *ctx, const Plan &pl, const float *tmpl, const float *poses, const float *p0,
                             const float *cot, float *grad_p0, float *grad_pose, float *grad_elem, bool want_adj,
-                            cudaStream_t st, char *ws_base, size_t ws_off)
+                            cudaStream_t st, size_t ws_off)
 {
     AdjLaunch L;
-    pa_status s = want_adj ? launch_adjoint<true, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, nullptr, L, true, st)
-                           : launch_adjoint<true, false>(ctx, pl, poses, tmpl, p0, cot, grad_p0, nullptr, L, true, st);
+    pa_status s = launch_adjoint(ctx, pl, true, want_adj, poses, tmpl, p0, cot, grad_p0, nullptr, L, true, st);
     if (s) return s;
-    (void)ws_base;
     const size_t part_b = align256((size_t)L.P * pl.g.F * pl.g.E * 3 * sizeof(float));
     const size_t ge_b = grad_elem ? 0 : align256((size_t)pl.g.F * pl.g.E * 3 * sizeof(float));
     if ((s = ws_reserve(ctx, ws_off + part_b + ge_b))) return s;
@@ -1161,8 +960,7 @@ pa_status adjoint_pose_core(pa_ctx *ctx, const Plan &pl, const float *tmpl, cons
     float *partial = reinterpret_cast<float *>(base);
     float *ge = grad_elem ? grad_elem : reinterpret_cast<float *>(base + part_b);
     CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
-    s = want_adj ? launch_adjoint<true, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, false, st)
-                 : launch_adjoint<true, false>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, false, st);
+    s = launch_adjoint(ctx, pl, true, want_adj, poses, tmpl, p0, cot, grad_p0, partial, L, false, st);
     if (s) return s;
     CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
     ctx->ev_adj = true;
@@ -1172,10 +970,8 @@ pa_status adjoint_pose_core(pa_ctx *ctx, const Plan &pl, const float *tmpl, cons
     return PA_OK;
 }
 
-pa_status launch_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const float *w, float a1, float a0, float eps,
-                     float *gP, float *gw, double *part, float *value, float scale, int accumulate, cudaStream_t st)
+pa_status tgv_args(const pa_grid *grid, float a1, float a0, float eps, float gs, TgvArgs &t)
 {
-    TgvArgs t;
     t.nx = grid->nx;
     t.ny = grid->ny;
     t.nz = grid->nz;
@@ -1183,16 +979,23 @@ pa_status launch_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const flo
     t.a1 = a1;
     t.a0 = a0;
     t.eps = eps;
+    t.gs = gs;
     if (3.0 * (double)t.nx * t.ny * t.nz >= 2147483647.0)
         return fail(PA_EUNSUPPORTED, "TGV: 3 x %d x %d x %d exceeds the kernel's 32-bit offsets", t.nx, t.ny, t.nz);
+    return PA_OK;
+}
+
+// value: out[0] = vscale * TGV (+ out[0] if accumulate); gradients scaled by gscale (TgvArgs::gs)
+pa_status launch_tgv(const TgvArgs &t, const float *P, const float *w, float *gP, float *gw, double *part, float *value,
+                     float vscale, int accumulate, cudaStream_t st)
+{
     dim3 gd((t.nx + TGV_BX - 1) / TGV_BX, (t.ny + TGV_BY - 1) / TGV_BY, (t.nz + TGV_ZS - 1) / TGV_ZS);
     ++g_nlaunch;
     k_tgv<<<gd, TGV_NT, 0, st>>>(t, P, w, gP, gw, part);
     CUDA_TRY(cudaGetLastError());
     ++g_nlaunch;
-    k_sum_parts<<<1, 256, 0, st>>>(part, (long long)gd.x * gd.y * gd.z, scale, accumulate, value);
+    k_sum_parts<<<1, 256, 0, st>>>(part, (long long)gd.x * gd.y * gd.z, vscale, accumulate, value);
     CUDA_TRY(cudaGetLastError());
-    (void)ctx;
     return PA_OK;
 }
 
@@ -1206,11 +1009,14 @@ inline size_t tgv_parts(const pa_grid *g)
 // ============================================================================ C ABI
 extern "C" {
 
-const char *pa_last_error(void) { return g_err.c_str(); }
+const char *pa_last_error(void) { return pa::g_err_cstr(); }
 
 long long pa_launch_count(void) { return g_nlaunch; }
 
-const char *pa_version(void) { return "libpa 0.2 (sm_100a, fp32 + fp64 anchors; Gaussian/exponential/power-law kernels)"; }
+const char *pa_version(void)
+{
+    return "libpa 0.3 (sm_100a, fp32 + fp64 anchors; Gaussian/exponential/power-law kernels; runtime window length)";
+}
 
 pa_status pa_create(pa_ctx **out, int device)
 {
@@ -1223,13 +1029,18 @@ pa_status pa_create(pa_ctx **out, int device)
     pa_ctx *c = new pa_ctx;
     c->device = device;
     cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-    if (cudaMalloc(&c->dflag, 64) != cudaSuccess) {
+    if (cudaMalloc(&c->dflag, 256) != cudaSuccess ||
+        cudaHostAlloc(reinterpret_cast<void **>(&c->hflag), sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        if (c->dflag) cudaFree(c->dflag);
         delete c;
         return fail(PA_ENOMEM, "flag allocation failed");
     }
+    *c->hflag = ~0ull;
     for (int i = 0; i < 3; ++i) cudaEventCreate(&c->ev[i]);
+    cudaEventCreateWithFlags(&c->ev_chk, cudaEventDisableTiming);
     *out = c;
-    g_err.clear();
+    pa::fail(PA_OK, "");
     return PA_OK;
 }
 
@@ -1240,9 +1051,20 @@ void pa_destroy(pa_ctx *c)
     if (c->ws) cudaFree(c->ws);
     if (c->fws) cudaFree(c->fws);
     if (c->dflag) cudaFree(c->dflag);
+    if (c->hflag) cudaFreeHost(c->hflag);
     for (int i = 0; i < 3; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->ev_chk) cudaEventDestroy(c->ev_chk);
     delete c;
+}
+
+pa_status pa_set_policy(pa_ctx *ctx, int32_t policy)
+{
+    if (!ctx) return fail(PA_EINVAL, "null ctx");
+    if (policy & ~(PA_POLICY_FWD_DIRECT | PA_POLICY_ADJ_DIRECT | PA_POLICY_ADJ_SVD | PA_POLICY_ADJ_TAYLOR))
+        return fail(PA_EINVAL, "unknown policy bits 0x%x", (unsigned)policy);
+    ctx->policy = policy;
+    return PA_OK;
 }
 
 pa_status pa_forward(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
@@ -1250,7 +1072,7 @@ pa_status pa_forward(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, pl);
+    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
     if (s) return s;
     if (F == 0) return PA_OK;
     if ((s = check_ptrs({tmpl, poses, p0, traces}))) return s;
@@ -1269,7 +1091,7 @@ pa_status pa_adjoint(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, pl);
+    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
     if (s) return s;
     if ((s = check_ptrs({tmpl, grad_p0}))) return s;
     if (F > 0 && (s = check_ptrs({poses, cot}))) return s;
@@ -1282,7 +1104,7 @@ pa_status pa_adjoint(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
     if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
     AdjLaunch L;
     CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
-    if ((s = launch_adjoint<false, true>(ctx, pl, poses, tmpl, nullptr, cot, grad_p0, nullptr, L, false, st))) return s;
+    if ((s = launch_adjoint(ctx, pl, false, true, poses, tmpl, nullptr, cot, grad_p0, nullptr, L, false, st))) return s;
     CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
     ctx->ev_adj = true;
     return PA_OK;
@@ -1294,7 +1116,7 @@ pa_status pa_adjoint_pose(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, c
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, pl);
+    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
     if (s) return s;
     if ((s = check_ptrs({tmpl, p0, grad_p0}))) return s;
     if (F > 0 && (s = check_ptrs({poses, cot, grad_pose}))) return s;
@@ -1306,7 +1128,7 @@ pa_status pa_adjoint_pose(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, c
         return PA_OK;
     }
     if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
-    return adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, grad_pose, grad_elem, true, st, nullptr, 0);
+    return adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, grad_pose, grad_elem, true, st, 0);
 }
 
 pa_status pa_pose_grad(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
@@ -1315,7 +1137,7 @@ pa_status pa_pose_grad(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, cons
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, pl);
+    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
     if (s) return s;
     if (F == 0) return PA_OK;
     if ((s = check_ptrs({tmpl, poses, p0, cot, grad_pose}))) return s;
@@ -1323,7 +1145,7 @@ pa_status pa_pose_grad(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, cons
     DevGuard dg(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
     if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
-    return adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, nullptr, grad_pose, grad_elem, false, st, nullptr, 0);
+    return adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, nullptr, grad_pose, grad_elem, false, st, 0);
 }
 
 pa_status pa_count(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E,
@@ -1331,7 +1153,7 @@ pa_status pa_count(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const fl
 {
     if (!ctx || !total) return fail(PA_EINVAL, "null ctx/total");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, pl);
+    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
     if (s && s != PA_EUNSUPPORTED) return s;  // the count is defined for every valid geometry
     *total = 0;
     if (F == 0) return PA_OK;
@@ -1366,6 +1188,7 @@ pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, con
     if (F < 0 || E < 1 || nt < 1) return fail(PA_ESHAPE, "bad shape");
     pa_status s;
     if ((s = check_ptrs({y, S, cot, loss}))) return s;
+    if (row_loss && !aligned4(row_loss)) return fail(PA_ESHAPE, "misaligned row_loss");
     DevGuard dg(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
     const long long rows = (long long)F * E;
@@ -1376,7 +1199,6 @@ pa_status pa_loss(pa_ctx *ctx, int32_t kind, const float *y, const float *S, con
         k_loss_rows<<<(unsigned)rows, 128, 0, st>>>(kind, y, S, row_mask, nt, cot, rl);
         CUDA_TRY(cudaGetLastError());
     }
-    if (row_loss && !aligned4(row_loss)) return fail(PA_ESHAPE, "misaligned row_loss");
     ++g_nlaunch;
     k_rowloss_sum<<<1, 256, 0, st>>>(rl, rows, loss, row_loss);
     CUDA_TRY(cudaGetLastError());
@@ -1392,11 +1214,12 @@ pa_status pa_tgv(pa_ctx *ctx, const pa_grid *grid, const float *P, const float *
     if (!(alpha1 >= 0.f) || !(alpha0 >= 0.f) || !(eps > 0.f)) return fail(PA_EINVAL, "need alpha >= 0, eps > 0");
     pa_status s;
     if ((s = check_ptrs({P, w, value, grad_P, grad_w}))) return s;
+    TgvArgs t;
+    if ((s = tgv_args(grid, alpha1, alpha0, eps, 1.0f, t))) return s;
     DevGuard dg(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
     if ((s = ws_reserve(ctx, tgv_parts(grid) * sizeof(double)))) return s;
-    return launch_tgv(ctx, grid, P, w, alpha1, alpha0, eps, grad_P, grad_w, static_cast<double *>(ctx->ws), value, 1.0f,
-                      0, st);
+    return launch_tgv(t, P, w, grad_P, grad_w, static_cast<double *>(ctx->ws), value, 1.0f, 0, st);
 }
 
 pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const float *tmpl, int32_t E, int32_t F,
@@ -1406,7 +1229,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
 {
     if (!ctx || !cfg) return fail(PA_EINVAL, "null ctx/cfg");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, pl);
+    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
     if (s) return s;
     if (cfg->step < 1) return fail(PA_EINVAL, "cfg.step must be >= 1");
     if (cfg->loss_kind != 0 && cfg->loss_kind != 1) return fail(PA_EINVAL, "cfg.loss_kind must be 0 or 1");
@@ -1417,17 +1240,19 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     if (grad_euler && !aligned4(grad_euler)) return fail(PA_ESHAPE, "misaligned grad_euler");
     if (row_loss && !aligned4(row_loss)) return fail(PA_ESHAPE, "misaligned row_loss");
     const bool use_tgv = cfg->tgv_lambda != 0.0f;
-    if (use_tgv) {
+    TgvArgs tg{};
+    if (use_tgv) {  // every check before any device work
         if (!(cfg->tgv_lambda > 0.f) || !(cfg->tgv_alpha1 >= 0.f) || !(cfg->tgv_alpha0 >= 0.f) || !(cfg->tgv_eps > 0.f))
             return fail(PA_EINVAL, "bad TGV parameters");
         if ((s = check_ptrs({tgv_w, adam_w}))) return s;
+        if ((s = tgv_args(grid, cfg->tgv_alpha1, cfg->tgv_alpha0, cfg->tgv_eps, cfg->tgv_lambda, tg))) return s;
     }
     DevGuard dg(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
     const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
     const size_t ntr = (size_t)F * E * acq->nt;
 
-    // workspace: poses | dR | cot | rowloss | grad_pose | geul | (partials, grad_elem from core)
+    // workspace: poses | dR | cot | rowloss | grad_pose | geul | tgv grads | tgv parts | (partials, grad_elem)
     size_t off = 0;
     const size_t o_poses = off; off += align256(sizeof(float) * 12 * (size_t)(F > 0 ? F : 1));
     const size_t o_dR = off; off += align256(sizeof(float) * 27 * (size_t)(F > 0 ? F : 1));
@@ -1439,7 +1264,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     const size_t o_tp = off; off += use_tgv ? align256(sizeof(double) * tgv_parts(grid)) : 0;
     // reserve enough for the core as well (partials + grad_elem)
     AdjLaunch L;
-    if (F > 0 && (s = launch_adjoint<true, true>(ctx, pl, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, true, st)))
+    if (F > 0 && (s = launch_adjoint(ctx, pl, true, true, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, true, st)))
         return s;
     const size_t core_b = align256((size_t)L.P * (F > 0 ? F : 1) * E * 3 * sizeof(float)) +
                           align256((size_t)(F > 0 ? F : 1) * E * 3 * sizeof(float));
@@ -1454,12 +1279,14 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     float *tg_p = use_tgv ? reinterpret_cast<float *>(ws + o_tg) : nullptr;
     float *tg_w = use_tgv ? tg_p + nvox : nullptr;
     double *tg_parts = use_tgv ? reinterpret_cast<double *>(ws + o_tp) : nullptr;
+    const unsigned long long *ok = nullptr;  // the step's degenerate verdict (device; read by the Adam kernels)
 
     if (F > 0) {
         ++g_nlaunch;
         k_euler_pose<<<(F + 127) / 128, 128, 0, st>>>(euler_t, F, poses, dR);
         CUDA_TRY(cudaGetLastError());
-        if ((s = check_degenerate(ctx, pl, poses, tmpl, st))) return s;
+        if ((s = check_degenerate_async(ctx, pl, poses, tmpl, st))) return s;
+        ok = ctx->dflag + 2;
         // a2 + a3: forward with fused loss/cotangent epilogue
         CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
         if ((s = launch_forward(ctx, pl, poses, tmpl, p0, cot, cfg->loss_kind == 0 ? FWD_MSE : FWD_NC, meas, row_mask, rl,
@@ -1470,13 +1297,14 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
         k_rowloss_sum<<<1, 256, 0, st>>>(rl, (long long)F * E, loss, row_loss);
         CUDA_TRY(cudaGetLastError());
         // a4 + a5 + a6 (records ev[1], ev[2])
-        if ((s = adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, gpose, nullptr, true, st, ws, off))) return s;
+        if ((s = adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, gpose, nullptr, true, st, off))) return s;
         ++g_nlaunch;
         k_euler_grad<<<(F + 127) / 128, 128, 0, st>>>(gpose, dR, F, geul);
         CUDA_TRY(cudaGetLastError());
     } else {
         CUDA_TRY(cudaMemsetAsync(grad_p0, 0, sizeof(float) * nvox, st));
         CUDA_TRY(cudaMemsetAsync(loss, 0, 2 * sizeof(float), st));
+        ctx->chk_pending = false;
     }
     // a7: cross-rank sum of dL/dp0 and of the loss (Stage 5)
     if (ar) {
@@ -1484,41 +1312,67 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
         if (ar(loss + 1, 1, stream, user) != 0) return fail(PA_ECUDA, "all-reduce callback failed (loss)");
     }
     // Eq. 2 regulariser (f4): replicated on every rank after the data all-reduce, so every rank
-    // applies the identical update; loss[1] += lambda * TGV
+    // applies the identical update; loss[1] += lambda TGV, grad_p0 += lambda dTGV/dP (k_tgv scales both
+    // gradients by lambda), w's Adam step takes lambda dTGV/dw
     if (use_tgv) {
-        if ((s = launch_tgv(ctx, grid, p0, tgv_w, cfg->tgv_alpha1, cfg->tgv_alpha0, cfg->tgv_eps, tg_p, tg_w, tg_parts,
-                            loss + 1, cfg->tgv_lambda, 1, st)))
-            return s;
+        if ((s = launch_tgv(tg, p0, tgv_w, tg_p, tg_w, tg_parts, loss + 1, cfg->tgv_lambda, 1, st))) return s;
         ++g_nlaunch;
-        k_axpy<<<ctx->nsm * 8, 256, 0, st>>>(grad_p0, tg_p, cfg->tgv_lambda, nvox);
+        k_axpy<<<ctx->nsm * 8, 256, 0, st>>>(grad_p0, tg_p, 1.0f, nvox);
         CUDA_TRY(cudaGetLastError());
     }
-    // a8: Adam
+    // a8: Adam (skipped on the device when the step's geometry is degenerate)
     const double bc1 = 1.0 - std::pow((double)cfg->beta1, cfg->step), bc2 = 1.0 - std::pow((double)cfg->beta2, cfg->step);
     if (cfg->update_p0) {
         int blocks = ctx->nsm * 8;
         ++g_nlaunch;
         k_adam<<<blocks, 256, 0, st>>>(p0, adam_p0, adam_p0 + nvox, grad_p0, nvox, cfg->lr_p0, cfg->beta1, cfg->beta2,
-                                      cfg->eps, (float)bc1, (float)bc2, 1);
+                                      cfg->eps, (float)bc1, (float)bc2, 1, ok);
         CUDA_TRY(cudaGetLastError());
     }
-    if (use_tgv && cfg->update_p0) {  // Adam on the TGV auxiliary field w with lambda * dTGV/dw
+    if (use_tgv && cfg->update_p0) {  // Adam on the TGV auxiliary field w with lambda dTGV/dw
         int blocks = ctx->nsm * 8;
         ++g_nlaunch;
-        k_axpy<<<blocks, 256, 0, st>>>(tg_w, tg_w, cfg->tgv_lambda - 1.0f, 3 * nvox);  // tg_w *= lambda
-        ++g_nlaunch;
         k_adam<<<blocks, 256, 0, st>>>(tgv_w, adam_w, adam_w + 3 * nvox, tg_w, 3 * nvox, cfg->lr_p0, cfg->beta1,
-                                       cfg->beta2, cfg->eps, (float)bc1, (float)bc2, 0);
+                                       cfg->beta2, cfg->eps, (float)bc1, (float)bc2, 0, ok);
         CUDA_TRY(cudaGetLastError());
     }
     if (cfg->update_pose && F > 0) {
         ++g_nlaunch;
         k_adam_pose<<<(6 * F + 127) / 128, 128, 0, st>>>(euler_t, adam_pose, adam_pose + 6 * F, geul, F, cfg->lr_rot,
                                                          cfg->lr_trans, cfg->beta1, cfg->beta2, cfg->eps, (float)bc1,
-                                                         (float)bc2);
+                                                         (float)bc2, ok);
         CUDA_TRY(cudaGetLastError());
     }
     return PA_OK;
+}
+
+pa_status pa_step_status(pa_ctx *ctx)
+{
+    if (!ctx) return fail(PA_EINVAL, "null ctx");
+    if (!ctx->chk_pending) return PA_OK;
+    DevGuard dg(ctx->device);
+    CUDA_TRY(cudaEventSynchronize(ctx->ev_chk));
+    const unsigned long long best = *ctx->hflag;
+    if (best != ~0ull) return degenerate_message(best, ctx->chk_E);
+    return PA_OK;
+}
+
+static void fill_info(const Plan &pl, pa_plan_info *out)
+{
+    out->lmin = pl.g.lmin;
+    out->fwd_deposit = pl.fwd_dep ? 1 : 0;
+    out->dep_rank = pl.dep_R;
+    out->dep_warps = pl.dep_nw;
+    out->dep_err = pl.dep_err;
+    out->adj_taylor = (pl.fam == KF_GAUSS && pl.tay_ok && !(pl.policy & PA_POLICY_ADJ_DIRECT)) ? 1 : 0;
+    out->tay_order = pl.tay_M;
+    out->tay_err = pl.tay_err;
+    out->adj_svd = pl.adj == ADJ_SVD ? 1 : 0;
+    out->svd_derr = pl.svd_derr;
+    out->dep_groups = pl.dep_g;
+    out->dep_ring = pl.dc.nr;
+    out->adj_kernel = pl.adj;
+    out->direct_class = pl.klass >= 0 ? kClasses[pl.klass].lmin : 0;
 }
 
 pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out)
@@ -1526,20 +1380,20 @@ pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa
     if (!out) return fail(PA_EINVAL, "null out");
     std::memset(out, 0, sizeof *out);
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, 1, pl);
+    pa_status s = make_plan(grid, acq, E, 1, PA_POLICY_DEFAULT, pl);
     if (s) return s;
-    out->lmin = kClasses[pl.klass].lmin;
-    out->fwd_deposit = use_dep(pl) ? 1 : 0;
-    out->dep_rank = out->lmin <= 32 ? PA_DEP_RANK_SHORT : 5;  // == DepRank<LMIN>::R
-    out->dep_warps = pl.dep_nw;
-    out->dep_err = pl.dep_err;
-    out->adj_taylor = (pl.fam == KF_GAUSS && pl.tay_ok && !adj_direct_forced()) ? 1 : 0;
-    out->tay_order = tay_order(out->lmin);
-    out->tay_err = pl.tay_err;
-    out->adj_svd = use_adj_svd(pl) ? 1 : 0;
-    out->svd_derr = pl.svd_derr;
-    out->dep_groups = pl.dep_g;
-    out->dep_ring = pl.dc.nr;
+    fill_info(pl, out);
+    return PA_OK;
+}
+
+pa_status pa_ctx_plan_info(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out)
+{
+    if (!ctx || !out) return fail(PA_EINVAL, "null ctx/out");
+    std::memset(out, 0, sizeof *out);
+    Plan pl;
+    pa_status s = make_plan(grid, acq, E, 1, ctx->policy, pl);
+    if (s) return s;
+    fill_info(pl, out);
     return PA_OK;
 }
 

@@ -45,6 +45,7 @@ struct Geo {
     float k2, two_a_k2, a2_k2;  // log2(e)/(2 s^2), 2a*k2, a^2*k2
     float s2, inv_s2, rt;
     int mF, mA;                 // recurrence centres (forward cluster window / adjoint pair window)
+    int lmin;                   // L_min = floor(2 kappa sigma / (c dt)): window length (L in {lmin, lmin+1})
     float ls, nu;               // exponential: log2(e)/s; power law: nu   (kernel families, R23)
 };
 
@@ -991,37 +992,44 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
 // rounding (checked on the host for the actual geometry, else the direct kernel runs).  The
 // window's optional last sample (L = LMIN + 1, k = LMIN - MA) is added directly.  Then
 //   A1 = sum g E D = u_m (D_m S0 - a S1),  Bq = sum g E (D^2 - s^2) = u_m ((D_m^2-s^2) S0 - 2a D_m S1 + a^2 S2)
-// exactly as the direct kernel.  K2a computes F for a frame chunk (L2-resident); K2b replaces the
-// per-voxel L-sample walk by NF/4 128-bit loads and three M-term Horner evaluations.
+// exactly as the direct kernel.  K2a computes F for a frame chunk (L2-resident); K2c (below) replaces
+// the per-voxel L-sample walk by one filter-record load and three M-term Horner evaluations.
 // ============================================================================================
-template <int LMIN>
+// Series order M of the Taylor form (a template parameter: it sizes the filter records); the window
+// length L_min is a runtime value (Geo::lmin), up to PA_LMAX.
+constexpr int PA_LMAX = 160;  // longest window (L_min) of the Gaussian fast path (K1d, K2a/K2c, K2s)
+template <int M_>
 struct TayCfg {
-    static constexpr int M = LMIN <= 32 ? 7 : (LMIN <= 64 ? 5 : 4);  // series order per class
+    static constexpr int M = M_;
     static constexpr int NP = M + 3;                                    // F_0 .. F_{M+2}
     static constexpr int NF = (NP + 3) & ~3;                            // floats per j (16-B rows)
 };
+constexpr int TAY_MAXNP = 11;  // M <= 8
 
-struct TayConst {
-    float H[768];      // H[t][p] = C'_k k^p, k = t - MA, t in [0, LMIN), p in [0, NP)
+struct TayFilt {               // K2a: the filter taps
+    float H[PA_LMAX * TAY_MAXNP];  // H[t][p] = C'_k k^p, k = t - MA, t in [0, L_min), p in [0, NP)
+};
+struct TayConst {              // K2c: the series constants
     float lam0;        // series centre (natural units)
     float lam_s;       // a / s^2: lam = lam_s D_m
-    float Ckt;         // C_k at the extra tap k_t = LMIN - MA
+    float Ckt;         // C_k at the extra tap k_t = L_min - MA
     float inv[8];      // 1/(m+1)
 };
 
-template <int LMIN>
-__global__ void __launch_bounds__(256) k_adj_filter(Geo g, TayConst tc, const float *__restrict__ cot, int f0, int fn,
+template <int M>
+__global__ void __launch_bounds__(256) k_adj_filter(Geo g, TayFilt tf, const float *__restrict__ cot, int f0, int fn,
                                                     float *__restrict__ Fg)
 {
-    using T = TayCfg<LMIN>;
-    __shared__ float s[256 + LMIN];
-    const int NJ = g.nt + LMIN;
+    using T = TayCfg<M>;
+    __shared__ float s[256 + PA_LMAX];
+    const int lmin = g.lmin;
+    const int NJ = g.nt + lmin;
     const int row = blockIdx.y;  // chunk-local row (f - f0) E + e
     const int jj0 = blockIdx.x * 256;
     const float *gr = cot + ((size_t)f0 * g.E + row) * g.nt;
-    // j_m = jj + MA - LMIN; the taps k in [-MA, LMIN - MA) read samples jj - LMIN + t, t = k + MA
-    for (int t = threadIdx.x; t < 256 + LMIN; t += 256) {
-        const int j = jj0 - LMIN + t;
+    // j_m = jj + MA - L_min; the taps k in [-MA, L_min - MA) read samples jj - L_min + t, t = k + MA
+    for (int t = threadIdx.x; t < 256 + lmin; t += 256) {
+        const int j = jj0 - lmin + t;
         s[t] = (j >= 0 && j < g.nt) ? __ldg(gr + j) : 0.0f;
     }
     __syncthreads();
@@ -1030,219 +1038,15 @@ __global__ void __launch_bounds__(256) k_adj_filter(Geo g, TayConst tc, const fl
     float acc[T::NF];
 #pragma unroll
     for (int p = 0; p < T::NF; ++p) acc[p] = 0.0f;
-#pragma unroll
-    for (int t = 0; t < LMIN; ++t) {
+#pragma unroll 2
+    for (int t = 0; t < lmin; ++t) {
         const float v = s[threadIdx.x + t];
 #pragma unroll
-        for (int p = 0; p < T::NP; ++p) acc[p] = __fmaf_rn(v, tc.H[t * T::NP + p], acc[p]);
+        for (int p = 0; p < T::NP; ++p) acc[p] = __fmaf_rn(v, tf.H[t * T::NP + p], acc[p]);
     }
     float4 *o = reinterpret_cast<float4 *>(Fg + ((size_t)row * NJ + jj) * T::NF);
 #pragma unroll
     for (int q = 0; q < T::NF / 4; ++q) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-}
-
-// Stage A of the moment-filter adjoint for element e (clamped to E-1; valid = false when
-// e >= E, the element is culled for this tile, the voxel is outside the grid or its window
-// misses [0, nt)): the window, D_m and the NF filter values at j_m.
-template <int NF>
-struct TayA {
-    float Fv[NF];
-    float Dm, inv_r, dx, dy, dz;
-    int jx;     // the window's optional last sample (j_lo + LMIN), or -1
-    int e;
-    bool valid;
-};
-
-template <int LMIN>
-__device__ __forceinline__ TayA<TayCfg<LMIN>::NF> tay_stage_a(const Geo &g, const AncS *anc, int e, int E, bool inside,
-                                                              float ex, float ey, float ez, float e2,
-                                                              const float *__restrict__ Frow, int NJ)
-{
-    constexpr int NF = TayCfg<LMIN>::NF, MA = AdjMid<LMIN>::m;
-    TayA<NF> o;
-    const int ec = min(e, E - 1);
-    const AncS sa = anc[ec];
-    Anc A;
-    A.dx2 = sa.dx2; A.dy2 = sa.dy2; A.dz2 = sa.dz2; A.dx = sa.dx; A.dy = sa.dy; A.dz = sa.dz;
-    A.rho = sa.rho; A.rho2 = sa.rho2; A.CA = sa.CA; A.JA = sa.JA; A.cull = 0;
-    const Pair pa = pair<LMIN>(g, A, ex, ey, ez, e2);
-    o.valid = e < E && !sa.cull && inside && pa.jlo <= g.nt - 1 && pa.jlo + pa.L - 1 >= 0;
-    const int jj = o.valid ? pa.jlo + LMIN : 0;  // j_m - (MA - LMIN)
-    const float4 *fp = reinterpret_cast<const float4 *>(Frow + (size_t)ec * NJ * NF) + jj * (NF / 4);
-#pragma unroll
-    for (int r = 0; r < NF / 4; ++r) {
-        const float4 v = __ldg(fp + r);
-        o.Fv[4 * r] = v.x;
-        o.Fv[4 * r + 1] = v.y;
-        o.Fv[4 * r + 2] = v.z;
-        o.Fv[4 * r + 3] = v.w;
-    }
-    o.Dm = __fmaf_rn(-(float)(pa.jlo - sa.JA), g.af, __fadd_rn(pa.drel, sa.CA)) - (float)MA * g.af;
-    o.inv_r = pa.inv_r;
-    o.dx = sa.dx;
-    o.dy = sa.dy;
-    o.dz = sa.dz;
-    const int jx = pa.jlo + LMIN;
-    o.jx = (o.valid && pa.L == LMIN + 1 && jx >= 0 && jx < g.nt) ? jx : -1;
-    o.e = ec;
-    return o;
-}
-
-// Stage B: S_n = sum_m dl^m/m! F_{n+m} (+ the extra sample), A1 = sum g E D, Bq = sum g E (D^2 - s^2).
-template <int LMIN, bool POSE>
-__device__ __forceinline__ void tay_stage_b(const Geo &g, const TayConst &tc, const TayA<TayCfg<LMIN>::NF> &a,
-                                            const float *__restrict__ crow, float &A1, float &Bq)
-{
-    constexpr int M = TayCfg<LMIN>::M, MA = AdjMid<LMIN>::m, KT = LMIN - MA;
-    const float Dm = a.Dm;
-    const float dl = __fmaf_rn(tc.lam_s, Dm, -tc.lam0);
-    float qm[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) qm[m] = dl * tc.inv[m];
-    float S[3];
-#pragma unroll
-    for (int n = 0; n < (POSE ? 3 : 2); ++n) {
-        float t = a.Fv[n + M];
-#pragma unroll
-        for (int m = M - 1; m >= 0; --m) t = __fmaf_rn(t, qm[m], a.Fv[n + m]);
-        S[n] = t;
-    }
-    const float gx = a.jx >= 0 ? __ldg(crow + (size_t)a.e * g.nt + a.jx) : 0.0f;
-    const float w = gx * tc.Ckt * ex2(g.two_a_k2 * Dm * (float)KT);
-    S[0] += w;
-    S[1] = __fmaf_rn(w, (float)KT, S[1]);
-    const float um = ex2(-g.k2 * Dm * Dm);
-    A1 = a.valid ? um * __fmaf_rn(-g.af, S[1], Dm * S[0]) : 0.0f;
-    Bq = 0.0f;
-    if (POSE) {
-        S[2] = __fmaf_rn(w, (float)(KT * KT), S[2]);
-        const float b = um * ((Dm * Dm - g.s2) * S[0] - 2.0f * g.af * Dm * S[1] + g.af * g.af * S[2]);
-        Bq = a.valid ? b : 0.0f;
-    }
-}
-
-template <int LMIN, bool POSE, bool ADJ>
-__global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay(Geo g, TayConst tc, const float *__restrict__ poses,
-                                                               const float *__restrict__ tmpl,
-                                                               const float *__restrict__ p0,
-                                                               const float *__restrict__ cot,
-                                                               const float *__restrict__ Fg,
-                                                               float *__restrict__ grad_p0,
-                                                               float *__restrict__ partial, int f0, int fn)
-{
-    using T = TayCfg<LMIN>;
-    constexpr int NF = T::NF;
-    extern __shared__ float sm[];
-    const int E = g.E, F = g.F, NJ = g.nt + LMIN;
-    AncS *anc = reinterpret_cast<AncS *>(sm);
-    float *wred = reinterpret_cast<float *>(anc + E);  // [8][E][3]
-    float *gacc = wred + (ADJ_THREADS / 32) * E * 3;  // [fn][E][3]
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
-    const float ex = ((float)lx - 0.5f * (TX - 1)) * g.hf;
-    const float ey = ((float)ly - 0.5f * (TY - 1)) * g.hf;
-    const float ez = ((float)lz - 0.5f * (TZ - 1)) * g.hf;
-    const float e2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
-
-    if (POSE) {
-        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS) gacc[q] = 0.0f;
-    }
-    for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
-        const int tx = tile % g.ntx, ty = (tile / g.ntx) % g.nty, tz = tile / (g.ntx * g.nty);
-        const int ix = TX * tx + lx, iy = TY * ty + ly, iz = TZ * tz + lz;
-        const bool inside = ix < g.nx && iy < g.ny && iz < g.nz;
-        const size_t kidx = ((size_t)iz * g.ny + iy) * g.nx + ix;
-        const float P = (POSE && inside) ? __ldg(p0 + kidx) : 0.0f;
-        float z = 0.0f;
-        for (int fl = 0; fl < fn; ++fl) {
-            const int f = f0 + fl;
-            __syncthreads();  // previous frame's anchors / wred consumed
-            for (int e = tid; e < E; e += ADJ_THREADS) {
-                double x[3];
-                elem_pos(poses, tmpl, f, e, x);
-                const Anc A = make_anchor(g, x, tx, ty, tz);
-                AncS sa;
-                sa.dx2 = A.dx2; sa.dy2 = A.dy2; sa.dz2 = A.dz2;
-                sa.dx = A.dx; sa.dy = A.dy; sa.dz = A.dz;
-                sa.rho = A.rho; sa.rho2 = A.rho2; sa.CA = A.CA;
-                sa.JA = A.JA; sa.cull = A.cull; sa.jseg = 0;
-                anc[e] = sa;
-            }
-            __syncthreads();
-            const float *Frow = Fg + (size_t)fl * E * NJ * NF;
-            const float *crow = cot + (size_t)f * E * g.nt;
-            // two-stage software pipeline over elements: stage A (window, filter loads) of element
-            // e + 1 is issued before stage B (series, gradients) of element e; culled and
-            // out-of-range elements are predicated, not branched, so the loads can be hoisted
-            TayA<NF> cur = tay_stage_a<LMIN>(g, anc, min(0, E - 1), E, inside, ex, ey, ez, e2, Frow, NJ);
-#pragma unroll 1
-            for (int e0 = 0; e0 < E; e0 += 4) {
-                float G[4][3];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int e = e0 + q;
-                    const TayA<NF> nxt = tay_stage_a<LMIN>(g, anc, e + 1, E, inside, ex, ey, ez, e2, Frow, NJ);
-                    float A1, Bq;
-                    tay_stage_b<LMIN, POSE>(g, tc, cur, crow, A1, Bq);
-                    const float ir = cur.inv_r;
-                    if (ADJ) z = __fmaf_rn(A1, 0.5f * ir, z);
-                    if (POSE) {
-                        const float dL = P * 0.5f * ir * (-Bq * g.inv_s2 - A1 * ir);
-                        const float sc = -dL * ir;  // x - y_k = -(d + delta)
-                        G[q][0] = sc * (cur.dx + ex);
-                        G[q][1] = sc * (cur.dy + ey);
-                        G[q][2] = sc * (cur.dz + ez);
-                    }
-                    cur = nxt;
-                }
-                if (POSE) {
-                    // transposed warp reduction of 4 elements x 3 components (as k_adjoint)
-                    const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
-                    float r6[6];
-#pragma unroll
-                    for (int j = 0; j < 6; ++j) {
-                        const float lo = G[j / 3][j % 3], hi = G[2 + j / 3][j % 3];
-                        const float snd = h16 ? lo : hi, kp = h16 ? hi : lo;
-                        r6[j] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
-                    }
-                    float r3[3];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float lo = r6[c], hi = r6[3 + c];
-                        const float snd = h8 ? lo : hi, kp = h8 ? hi : lo;
-                        r3[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
-                    }
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 4);
-                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 2);
-                        r3[c] += __shfl_xor_sync(0xffffffffu, r3[c], 1);
-                    }
-                    const int e = e0 + ((lane >> 3) & 3);
-                    if ((lane & 7) == 0 && e < E) {
-                        wred[(warp * E + e) * 3 + 0] = r3[0];
-                        wred[(warp * E + e) * 3 + 1] = r3[1];
-                        wred[(warp * E + e) * 3 + 2] = r3[2];
-                    }
-                }
-            }
-            if (POSE) {
-                __syncthreads();
-                for (int q = tid; q < E * 3; q += ADJ_THREADS) {
-                    float s = 0.0f;
-#pragma unroll
-                    for (int w = 0; w < ADJ_THREADS / 32; ++w) s += wred[w * E * 3 + q];
-                    gacc[fl * E * 3 + q] += s;
-                }
-            }
-        }
-        if (ADJ && inside) grad_p0[kidx] = (f0 == 0 ? 0.0f : grad_p0[kidx]) + z;
-    }
-    if (POSE) {
-        __syncthreads();
-        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS)
-            partial[((size_t)blockIdx.x * F + f0) * E * 3 + q] = gacc[q];
-    }
 }
 
 // ============================================================================================
@@ -1266,20 +1070,16 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay(Geo g, TayConst 
 // in a fixed order.  Layout [pos][channel] with an odd stride: the R + 2 words of a deposit are
 // immediate offsets of one address, and 32 lanes at distinct positions hit distinct banks.
 // ============================================================================================
-constexpr int DEP_MAXR = 6;
+constexpr int DEP_MAXR = 7;  // separable rank 5, 6 or 7 (7 for the shortest windows, L_min < ~21)
 
 // rank per window class: the factorisation error is <= ~2e-8 (L_min 53), 5e-9 (26, rank 6),
 // 6e-10 (106) of max|G|
 #ifndef PA_DEP_RANK_SHORT
 #define PA_DEP_RANK_SHORT 6  // rank for the short-window class (L_min <= 32)
 #endif
-template <int LMIN>
-struct DepRank {
-    static constexpr int R = LMIN <= 32 ? PA_DEP_RANK_SHORT : 5;
-};
 
 struct DepConst {
-    float psi[DEP_MAXR][128];  // psi[m][q-1] = psi_m(k = OFF - q), q in [1, LMIN]
+    float psi[DEP_MAXR][PA_LMAX];  // psi[m][q-1] = psi_m(k = OFF - q), q in [1, L_min]
     float2 cf2[DEP_MAXR + 1][4]; // (c, c): phi_m(t) = t^(m%2) (c0 + s c1 + s^2 c2 + s^3 c3), s = t^2, scaled by S_m;
                                  // X (index R): c0 + t c1 + t^2 c2 + t^3 c3, scaled by S_X
     float dec[DEP_MAXR + 1];   // 0.5 / S_m  (x Pmax / r_lo at decode)
@@ -1305,9 +1105,9 @@ constexpr int dep_nb(int nw) { return 22 - dep_ilog2(nw * PA_DEP_TPR); }
 
 // G = copies of the round accumulator, interleaved per position; lane l deposits into copy l % G
 // (chosen per geometry on the host: Plan::dep_g)
-template <int LMIN, int NW, int G_ = 1>
+template <int R_, int NW, int G_ = 1>
 struct DepCfg {
-    static constexpr int R = DepRank<LMIN>::R;
+    static constexpr int R = R_;                  // separable rank (5 or 6; chosen per geometry on the host)
     static constexpr int NQ = R + 2;              // int words per position: R channels, X, low word of channel 0
     static constexpr int G = G_;                  // lanes of one deposit instruction at the same position hit
                                                   // G different words (same-address atomics serialise)
@@ -1316,9 +1116,9 @@ struct DepCfg {
     static constexpr int TPR = PA_DEP_TPR;        // tiles per warp per round
     static constexpr int NB = dep_nb(NW);         // a round adds <= 256 NW TPR deposits per word
     static constexpr int NB0 = NB + 10;           // channel 0: hi (<= 2^NB) * 2^10 + lo
-    static __host__ __device__ int njp(int nt) { return nt + LMIN; }
+    static __host__ __device__ int njp(int nt, int lmin) { return nt + lmin; }
     // ring of nr positions x CS round words + NJ x CF fp32 row accumulators
-    static __host__ __device__ size_t smem_bytes(int nt, int nr) { return ((size_t)CS * nr + (size_t)CF * njp(nt)) * 4; }
+    static __host__ __device__ size_t smem_bytes(int nt, int lmin, int nr) { return ((size_t)CS * nr + (size_t)CF * njp(nt, lmin)) * 4; }
 };
 
 // Row epilogue shared by the forward kernels: y (shared memory, nt floats) -> trace, or the MSE / NC
@@ -1405,7 +1205,7 @@ __device__ __forceinline__ void red_s32(unsigned addr, int v)
     asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
 }
 
-template <int LMIN, int NW, int NG>
+template <int RK, int NW, int NG>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, DepConst dc, const float *__restrict__ poses,
                                                                        const float *__restrict__ tmpl,
                                                                        const float *__restrict__ p0,
@@ -1415,10 +1215,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                                                                        const uint8_t *__restrict__ row_mask,
                                                                        double *__restrict__ rowloss)
 {
-    using C = DepCfg<LMIN, NW, NG>;
+    using C = DepCfg<RK, NW, NG>;
     constexpr int R = C::R, CS = C::CS, CF = C::CF, NQ = C::NQ, G = C::G;
     extern __shared__ int smi[];
-    const int NJ = C::njp(g.nt), NR = dc.nr;
+    const int LMIN = g.lmin;  // runtime window length L_min
+    const int NJ = C::njp(g.nt, LMIN), NR = dc.nr;
     const unsigned nrm = dc.nrm;
     int *Qi = smi;                                         // [NR][CS] fixed-point round accumulators (ring: pos & nrm)
     float *Qf = reinterpret_cast<float *>(smi + CS * NR);  // [NJ][CF] fp32 row accumulators
@@ -1511,12 +1312,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
         if (PAIR) hh_ ^= 1;
         return tx < g.ntx && ty < g.nty && tz < g.ntz;
     };
-    const int sy = g.nx, sz = g.nx * g.ny;  // < 2^31 voxels per volume
+    const size_t sy = (size_t)g.nx, sz = (size_t)g.nx * g.ny;  // 64-bit offsets: volumes of >= 2^31 voxels
     // the lane's 2x2x2 voxel amplitudes of a tile (0 outside the grid)
     auto load_p = [&](int tx, int ty, int tz, int hh, bool ok, float P[8]) {
         const int ix0 = TX * tx + bx, iy0 = TY * ty + by + 4 * hh, iz0 = TZ * tz + bz;
         const bool ok0 = ok && ix0 < g.nx && iy0 < g.ny && iz0 < g.nz;
-        const float *pb = p0 + (ok0 ? (iz0 * sz + iy0 * sy + ix0) : 0);
+        const float *pb = p0 + (ok0 ? ((size_t)iz0 * sz + (size_t)iy0 * sy + (size_t)ix0) : (size_t)0);
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
             const int vx = v & 1, vy = dyv(v), vz = dzv(v);
@@ -1624,7 +1425,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                     chan(std::integral_constant<int, 3>{});
                     chan(std::integral_constant<int, 4>{});
                     if constexpr (R > 5) chan(std::integral_constant<int, 5>{});
-                    static_assert(R == 5 || R == 6, "rank 5 or 6");
+                    if constexpr (R > 6) chan(std::integral_constant<int, 6>{});
+                    static_assert(R >= 5 && R <= 7, "rank 5, 6 or 7");
                     {  // X: the optional last tap (L = LMIN + 1), a cubic in t
                         const float2 cx = make_float2(Lxx ? ct.x : 0.0f, Lxy ? ct.y : 0.0f);
                         const float2 ox = make_float2(Lxx ? o0.x : 0.0f, Lxy ? o0.y : 0.0f);
@@ -1683,7 +1485,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
             const float *qm = Qf + j * CF + m;
             float am = 0.0f;
 #pragma unroll 8
-            for (int q = 1; q <= LMIN; ++q) am = __fmaf_rn(qm[q * CF], dc.psi[m][q - 1], am);
+            for (int q = 1; q <= LMIN; ++q) am = __fmaf_rn(qm[q * CF], dc.psi[m][q - 1], am);  // runtime L_min
             acc += am;
         }
         y[j] = acc;
@@ -1695,8 +1497,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
 // ============================================================================================
 // K2c — the moment-filter adjoint (a4 + a5) with two voxels per thread in packed fp32x2.
 //
-// Same arithmetic as K2b (k_adjoint_tay) per (voxel, element): the window of pair<LMIN>() (every
-// step bit-identical, ceil on the FP32 pipe), the Taylor moments S_n = sum_m dl^m/m! F_{n+m}[j_m]
+// Per (voxel, element): the window of pair() (every step bit-identical, ceil on the FP32 pipe; L_min
+// is the runtime Geo::lmin), the Taylor moments S_n = sum_m dl^m/m! F_{n+m}[j_m]
 // from the L2-resident per-row filters, the exact optional last tap, A1 = u_m (D_m S0 - a S1)
 // and Bq = u_m ((D_m^2 - s^2) S0 - 2 a D_m S1 + a^2 S2).  A thread owns voxels z and z + 2 of an
 // 8x8x4 anchor tile (a CTA = two tiles stacked in z, 128 threads each), so the geometry, the
@@ -1712,13 +1514,13 @@ struct Tay2A {
     bool va, vb;
 };
 
-template <int LMIN>
-__device__ __forceinline__ Tay2A<TayCfg<LMIN>::NF> tay2_stage_a(const Geo &g, const AncS *anc, int e, int E, bool ina,
+template <int NF>
+__device__ __forceinline__ Tay2A<NF> tay2_stage_a(const Geo &g, const AncS *anc, int e, int E, bool ina,
                                                                 bool inb, float ex, float ey, float2 ez, float2 e2,
                                                                 const float *__restrict__ Frow,
                                                                 const float *__restrict__ crow, int NJ)
 {
-    constexpr int NF = TayCfg<LMIN>::NF, MA = AdjMid<LMIN>::m;
+    const int LMIN = g.lmin, MA = g.mA;  // runtime window length and centre
     Tay2A<NF> o;
     const int ec = min(e, E - 1);
     const AncS sa = anc[ec];
@@ -1767,11 +1569,11 @@ __device__ __forceinline__ Tay2A<TayCfg<LMIN>::NF> tay2_stage_a(const Geo &g, co
     return o;
 }
 
-template <int LMIN, bool POSE>
-__device__ __forceinline__ void tay2_stage_b(const Geo &g, const TayConst &tc, const Tay2A<TayCfg<LMIN>::NF> &a,
+template <int M, bool POSE>
+__device__ __forceinline__ void tay2_stage_b(const Geo &g, const TayConst &tc, const Tay2A<TayCfg<M>::NF> &a,
                                              float2 &A1, float2 &Bq)
 {
-    constexpr int M = TayCfg<LMIN>::M, MA = AdjMid<LMIN>::m, KT = LMIN - MA;
+    const int KT = g.lmin - g.mA;  // the optional last tap k_t = L_min - MA
     const float2 Dm = a.Dm;
     const float2 dl = __ffma2_rn(f2(tc.lam_s), Dm, f2(-tc.lam0));
     float2 qm[M];
@@ -1811,7 +1613,7 @@ __device__ __forceinline__ void tay2_stage_b(const Geo &g, const TayConst &tc, c
     }
 }
 
-template <int LMIN, bool POSE, bool ADJ>
+template <int M, bool POSE, bool ADJ>
 __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst tc, const float *__restrict__ poses,
                                                                 const float *__restrict__ tmpl,
                                                                 const float *__restrict__ p0,
@@ -1820,10 +1622,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
                                                                 float *__restrict__ grad_p0,
                                                                 float *__restrict__ partial, int f0, int fn)
 {
-    using T = TayCfg<LMIN>;
+    using T = TayCfg<M>;
     constexpr int NF = T::NF;
     extern __shared__ float sm[];
-    const int E = g.E, F = g.F, NJ = g.nt + LMIN;
+    const int E = g.E, F = g.F, NJ = g.nt + g.lmin;
     AncS *anc = reinterpret_cast<AncS *>(sm);             // [2][E]: the two tiles of the CTA
     float *wred = reinterpret_cast<float *>(anc + 2 * E);  // [8][E][3]
     float *gacc = wred + (ADJ_THREADS / 32) * E * 3;       // [fn][E][3]
@@ -1870,7 +1672,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
             const float *Frow = Fg + (size_t)fl * E * NJ * NF;
             const float *crow = cot + (size_t)f * E * g.nt;
             const size_t fstep = (size_t)NJ * NF;
-            Tay2A<NF> cur = tay2_stage_a<LMIN>(g, anch, 0, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
+            Tay2A<NF> cur = tay2_stage_a<NF>(g, anch, 0, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
 #pragma unroll 1
             for (int e0 = 0; e0 < E; e0 += 4) {
                 float G[4][3];
@@ -1881,9 +1683,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
                         Frow += fstep;
                         crow += g.nt;
                     }
-                    const Tay2A<NF> nxt = tay2_stage_a<LMIN>(g, anch, e + 1, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
+                    const Tay2A<NF> nxt = tay2_stage_a<NF>(g, anch, e + 1, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
                     float2 A1, Bq;
-                    tay2_stage_b<LMIN, POSE>(g, tc, cur, A1, Bq);
+                    tay2_stage_b<M, POSE>(g, tc, cur, A1, Bq);
                     const float2 ir = cur.inv_r;
                     const float2 hir = __fmul2_rn(f2(0.5f), ir);
                     if (ADJ) z = __ffma2_rn(A1, hir, z);
@@ -1964,19 +1766,19 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
 // pose reduction are K2c's.
 // ============================================================================================
 struct SvdConst {
-    float psi[DEP_MAXR][128];   // as DepConst::psi
+    float psi[DEP_MAXR][PA_LMAX];  // as DepConst::psi
     float c[DEP_MAXR + 1][4];   // unscaled phi_m coefficients (index R: the last-tap cubic in t)
     float tA, tB, tC;           // t = (D_m - Dc)/Dw as in K1d
     float invDw;                // dt/dD_m
 };
 constexpr int SVD_NF = 8;  // floats per position record
 
-template <int LMIN>
+template <int R>
 __global__ void __launch_bounds__(256) k_adj_svd_filter(Geo g, SvdConst sc, const float *__restrict__ cot, int f0,
                                                         int fn, float *__restrict__ Fg)
 {
-    constexpr int R = DepRank<LMIN>::R;
-    __shared__ float sg[256 + LMIN];
+    __shared__ float sg[256 + PA_LMAX];
+    const int LMIN = g.lmin;  // runtime window length
     const int NJ = g.nt + LMIN;
     const int row = blockIdx.y;  // chunk-local row (f - f0) E + e
     const int p0 = blockIdx.x * 256;
@@ -1993,7 +1795,7 @@ __global__ void __launch_bounds__(256) k_adj_svd_filter(Geo g, SvdConst sc, cons
 #pragma unroll
     for (int m = 0; m < R; ++m) acc[m] = 0.0f;
 #pragma unroll 4
-    for (int q = 1; q <= LMIN; ++q) {
+    for (int q = 1; q <= LMIN; ++q) {  // runtime L_min
         const float v = sg[threadIdx.x + LMIN - q];
 #pragma unroll
         for (int m = 0; m < R; ++m) acc[m] = __fmaf_rn(v, sc.psi[m][q - 1], acc[m]);
@@ -2016,12 +1818,12 @@ struct SvdA {
     bool va, vb, xa, xb;  // valid; last tap in-window
 };
 
-template <int LMIN>
 __device__ __forceinline__ SvdA svd_stage_a(const Geo &g, const SvdConst &sc, const AncS *anc, int e, int E, bool ina,
                                             bool inb, float ex, float ey, float2 ez, float2 e2,
                                             const float *__restrict__ Frow)
 {
     SvdA o;
+    const int LMIN = g.lmin;  // runtime window length
     const int ec = min(e, E - 1);
     const AncS sa = anc[ec];
     const float2 num = __ffma2_rn(f2(sa.dx2), f2(ex), __ffma2_rn(f2(sa.dy2), f2(ey), __ffma2_rn(f2(sa.dz2), ez, e2)));
@@ -2059,11 +1861,10 @@ __device__ __forceinline__ SvdA svd_stage_a(const Geo &g, const SvdConst &sc, co
 }
 
 // A1 and dA1/dt of one voxel from its record
-template <int LMIN, bool POSE>
+template <int R, bool POSE>
 __device__ __forceinline__ void svd_eval(const SvdConst &sc, const float F[SVD_NF], float t, bool lx, float &A1,
                                          float &dA1)
 {
-    constexpr int R = DepRank<LMIN>::R;
     const float s = t * t;
     float e[4], o[4];
 #pragma unroll
@@ -2091,7 +1892,7 @@ __device__ __forceinline__ void svd_eval(const SvdConst &sc, const float F[SVD_N
     }
 }
 
-template <int LMIN, bool POSE, bool ADJ>
+template <int R, bool POSE, bool ADJ>
 __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_svd(Geo g, SvdConst sc, const float *__restrict__ poses,
                                                                const float *__restrict__ tmpl,
                                                                const float *__restrict__ p0,
@@ -2100,7 +1901,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_svd(Geo g, SvdConst 
                                                                float *__restrict__ partial, int f0, int fn)
 {
     extern __shared__ float sm[];
-    const int E = g.E, F = g.F, NJ = g.nt + LMIN;
+    const int E = g.E, F = g.F, NJ = g.nt + g.lmin;
     AncS *anc = reinterpret_cast<AncS *>(sm);             // [2][E]: the two tiles of the CTA
     float *wred = reinterpret_cast<float *>(anc + 2 * E);  // [8][E][3]
     float *gacc = wred + (ADJ_THREADS / 32) * E * 3;       // [fn][E][3]
@@ -2145,7 +1946,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_svd(Geo g, SvdConst 
             __syncthreads();
             const float *Frow = Fg + (size_t)fl * E * NJ * SVD_NF;
             const size_t fstep = (size_t)NJ * SVD_NF;
-            SvdA cur = svd_stage_a<LMIN>(g, sc, anch, 0, E, ina, inb, ex, ey, ez, e2, Frow);
+            SvdA cur = svd_stage_a(g, sc, anch, 0, E, ina, inb, ex, ey, ez, e2, Frow);
 #pragma unroll 1
             for (int e0 = 0; e0 < E; e0 += 4) {
                 float G[4][3];
@@ -2153,10 +1954,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_svd(Geo g, SvdConst 
                 for (int q = 0; q < 4; ++q) {
                     const int e = e0 + q;
                     if (e + 1 < E) Frow += fstep;
-                    const SvdA nxt = svd_stage_a<LMIN>(g, sc, anch, e + 1, E, ina, inb, ex, ey, ez, e2, Frow);
+                    const SvdA nxt = svd_stage_a(g, sc, anch, e + 1, E, ina, inb, ex, ey, ez, e2, Frow);
                     float a1x, a1y, d1x = 0.0f, d1y = 0.0f;
-                    svd_eval<LMIN, POSE>(sc, cur.Fa, cur.t.x, cur.xa, a1x, d1x);
-                    svd_eval<LMIN, POSE>(sc, cur.Fb, cur.t.y, cur.xb, a1y, d1y);
+                    svd_eval<R, POSE>(sc, cur.Fa, cur.t.x, cur.xa, a1x, d1x);
+                    svd_eval<R, POSE>(sc, cur.Fb, cur.t.y, cur.xb, a1y, d1y);
                     float2 A1 = make_float2(cur.va ? a1x : 0.0f, cur.vb ? a1y : 0.0f);
                     const float2 ir = cur.inv_r;
                     const float2 hir = __fmul2_rn(f2(0.5f), ir);
@@ -2227,7 +2028,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_svd(Geo g, SvdConst 
 
 // max |p0| as float bits (non-negative floats order like unsigned integers): the 1/Pmax
 // normalisation of the fixed-point deposits of K1d.
-__global__ void k_absmax(const float *__restrict__ p, long long n, unsigned *__restrict__ out)
+static __global__ void k_absmax(const float *__restrict__ p, long long n, unsigned *__restrict__ out)
 {
     unsigned m = 0u;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -2238,6 +2039,7 @@ __global__ void k_absmax(const float *__restrict__ p, long long n, unsigned *__r
 
 }  // namespace pa
 
+#ifdef PA_API_TU  // the TGV kernel is launched from pa_api.cu only
 namespace pa {
 
 // ============================================================================================
@@ -2252,6 +2054,7 @@ namespace pa {
 struct TgvArgs {
     int nx, ny, nz;
     float inv_h, a1, a0, eps;
+    float gs;  // scale of both gradients (lambda of Eq. 2 inside pa_step, 1 for pa_tgv)
 };
 
 __device__ __forceinline__ bool tgv_in(const TgvArgs &t, int x, int y, int z)
@@ -2369,9 +2172,9 @@ __global__ void __launch_bounds__(TGV_NT) k_tgv(TgvArgs t, const float *__restri
                 gwv[d] = -t.a1 * nn[d] + t.a0 * t.inv_h * s;
             }
             const int k = z * sz + y * t.nx + x;
-            gP[k] = gpv;
+            gP[k] = t.gs * gpv;
 #pragma unroll
-            for (int d = 0; d < 3; ++d) gw[d * nv + k] = gwv[d];
+            for (int d = 0; d < 3; ++d) gw[d * nv + k] = t.gs * gwv[d];
         }
         __syncthreads();
         cur ^= 1;
@@ -2390,3 +2193,4 @@ __global__ void __launch_bounds__(TGV_NT) k_tgv(TgvArgs t, const float *__restri
 }
 
 }  // namespace pa
+#endif  // PA_API_TU

@@ -92,17 +92,28 @@ def test_long_traces(ctx, nt, want_dep, want_warps, record_parity):
     assert r <= TOL_FA, r
 
 
-@pytest.mark.parametrize("variant", ["PA_ADJ_SVD", "PA_ADJ_TAY1", "PA_FWD_DIRECT", "PA_ADJ_DIRECT"])
-def test_alternative_kernels_parity(ctx, variant, monkeypatch, record_parity):
-    """The opt-in / fallback kernels selected by environment switches (K2s, K2b, direct K1, direct K2)
-    keep parity with the oracle on a ragged multi-tile case."""
-    monkeypatch.setenv(variant, "1")
+@pytest.mark.parametrize("variant", ["adj_svd", "fwd_direct", "adj_direct", "adj_taylor"])
+def test_alternative_kernels_parity(ctx, variant, record_parity):
+    """The alternative kernels a context's policy selects (pa_set_policy: K2s, direct K1, direct K2, K2c) keep
+    parity with the oracle on a ragged multi-tile case."""
+    ctx.set_policy(variant)
+    try:
+        _alternative(ctx, variant, record_parity)
+    finally:
+        ctx.set_policy("default")
+
+
+def _alternative(ctx, variant, record_parity):
     grid = gen.make_grid((21, 19, 13), 0.2)
     acq = gen.make_acq(301, 0.2, t0=1.3)
     tmpl, poses = random_scene(14, grid, E=5, F=3)
     p0 = gen.random_volume(grid, 8)
     cot = gen.random_cotangent((3, 5, 301), 9)
     g, a = grid32(grid), acq32(acq)
+    info = ctx.plan_info(g, a, 5)
+    want = {"adj_svd": ("adj_kernel", 2), "fwd_direct": ("fwd_deposit", 0), "adj_direct": ("adj_kernel", 0),
+            "adj_taylor": ("adj_kernel", 1)}[variant]
+    assert info[want[0]] == want[1], info
     y = ctx.forward(g, a, T(tmpl), T(poses), T(p0)).cpu().numpy()
     gz, gp, _ = ctx.adjoint_pose(g, a, T(tmpl), T(poses), T(p0), T(cot))
     yo = oracle.forward(g, a, f64(tmpl), f64(poses), f64(p0))

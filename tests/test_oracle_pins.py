@@ -374,6 +374,7 @@ def brute(grid, acq, tmpl, poses, p0, cot):
     s2 = acq["sigma"] ** 2
     fwd = np.zeros((F, E, acq["nt"]))
     adj = np.zeros(P.size)
+    adj_abs = np.zeros(P.size)
     gel = np.zeros((F, E, 3))
     cnt = 0
     for f in range(F):
@@ -388,10 +389,12 @@ def brute(grid, acq, tmpl, poses, p0, cot):
             k = D / (2 * r[:, None]) * Ek
             fwd[f, e] = P @ k
             adj += k @ cot[f, e]
+            adj_abs += np.abs(k) @ np.abs(cot[f, e])
             dk = Ek / (2 * r[:, None]) * ((1 - D * D / s2) - D / r[:, None])
             dLdr = P * (dk @ cot[f, e])
             gel[f, e] = (dLdr[:, None] * d / r[:, None]).sum(0)
             cnt += int(m.sum())
+    brute.adj_abs = adj_abs.reshape(np.shape(p0))
     return fwd, adj.reshape(np.shape(p0)), gel, cnt
 
 
@@ -409,6 +412,8 @@ def test_P8_brute_force_tiny(kappa):
     assert rel(oracle.forward(g, a, tmpl, poses, p0), bf) <= 1e-12
     assert rel(oracle.adjoint(g, a, tmpl, poses, cot), ba) <= 1e-12
     assert rel(oracle.elem_grad(g, a, tmpl, poses, p0, cot), bg) <= 1e-12
+    za = oracle.adjoint_abs(g, a, tmpl, poses, cot)  # the per-voxel error scale of the GPU parity tests
+    assert rel(za, brute.adj_abs) <= 1e-12 and np.all(za >= np.abs(ba) - 1e-15)
     if kappa > 0:
         n, pf = oracle.count(g, a, tmpl, poses)
         assert n == bc and pf.sum() == n
@@ -529,3 +534,62 @@ def test_step_composes_and_descends():
     assert np.all(out["p0"] >= 0.0)
     L1 = float(np.sum((oracle.forward(g, a, tmpl, gen.poses_from_euler(out["euler_t"]), out["p0"]) - meas) ** 2))
     assert L1 < L
+
+
+def _adam_golden():
+    import os
+
+    rows = []
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "adam_steps.txt")) as fh:
+        for ln in fh:
+            if ln.strip() and not ln.startswith("#"):
+                p = ln.split()
+                rows.append((float(p[0]), int(p[1]), int(p[2]), float(p[3]), float(p[4]), float(p[5])))
+    return rows
+
+
+def test_adam_three_steps_from_nonzero_state_golden():
+    """oracle.adam against tests/golden/adam_steps.txt: three steps (t = 1..3) from m0 = 0.1, v0 = 3/999,
+    b1 = 0.9, b2 = 0.999, worked by hand; with and without the p0 >= 0 clamp.
+    A dropped b1 m_{t-1} term or bc2 = 1 - b2 (not 1 - b2^t) fails it."""
+    rows = _adam_golden()
+    grads = {1: 1.0, 2: -2.0, 3: 2.0}
+    for x0 in sorted({r[0] for r in rows}):
+        want = [r for r in rows if r[0] == x0]
+        clamp = 0.0 if want[0][1] else None
+        x, m, v = np.array([x0]), np.array([0.1]), np.array([3.0 / 999.0])
+        for (_, _, t, xw, mw, vw) in sorted(want, key=lambda r: r[2]):
+            x, m, v = oracle.adam(x, m, v, np.array([grads[t]]), lr=0.1, b1=0.9, b2=0.999, eps=1e-8, t=t, clamp=clamp)
+            assert abs(x[0] - xw) <= 1e-12 and abs(m[0] - mw) <= 1e-15 and abs(v[0] - vw) <= 1e-15, (x0, t, x, m, v)
+    # per-element learning rates (the pose Adam: angles and translations, S:509) scale the step only
+    x, m, v = oracle.adam(np.array([1.0, 1.0]), np.array([0.1, 0.1]), np.array([3.0 / 999.0] * 2), np.array([1.0, 1.0]),
+                          lr=np.array([0.1, 0.01]), t=1)
+    assert abs(x[0] - 0.905000000475) <= 1e-12 and abs(x[1] - (1.0 - 0.0094999999525)) <= 1e-12
+
+
+def test_step_adam_state_recurrence_t2_t3():
+    """oracle.step carries the Adam state: from a nonzero state at t = 2 and 3 its p0 / Euler updates are
+    oracle.adam (pinned above by the golden steps) applied to its own gradients (pinned by FD, P6), and the
+    state it returns is that of oracle.adam."""
+    g = grid_of((5, 5, 4), 0.2)
+    a = acq_of(200, 0.2, t0=0.5)
+    tmpl = gen.linear_array(3, 0.3)
+    e_true = np.array([[0.1, -0.2, 0.05, 0.2, 0.1, -3.5]])
+    p_true = gen.random_volume(g, 5)
+    meas = oracle.forward(g, a, tmpl, gen.poses_from_euler(e_true), p_true)
+    rng = np.random.default_rng(3)
+    p0 = np.full_like(p_true, 0.4)
+    e0 = e_true + 0.01
+    nv = p0.size
+    st_p = np.concatenate([rng.normal(size=nv) * 1e-3, rng.uniform(1e-7, 2e-6, size=nv)])
+    st_q = np.concatenate([rng.normal(size=6) * 1e-2, rng.uniform(1e-5, 1e-4, size=6)])
+    for t in (2, 3):
+        out = oracle.step(g, a, tmpl, meas, p0, e0, st_p, st_q, lr_p0=1e-2, lr_rot=1e-3, lr_trans=2e-3, t=t)
+        xp, mp, vp = oracle.adam(p0.ravel(), st_p[:nv], st_p[nv:], out["grad_p0"], lr=1e-2, t=t, clamp=0.0)
+        lr_e = np.array([1e-3] * 3 + [2e-3] * 3)
+        xe, me, ve = oracle.adam(e0.ravel(), st_q[:6], st_q[6:], out["grad_euler"].ravel(), lr=lr_e, t=t)
+        assert np.allclose(out["p0"].ravel(), xp, rtol=0, atol=1e-15)
+        assert np.allclose(out["adam_p0"], np.concatenate([mp, vp]), rtol=0, atol=1e-18)
+        assert np.allclose(out["euler_t"].ravel(), xe, rtol=0, atol=1e-15)
+        assert np.allclose(out["adam_pose"], np.concatenate([me, ve]), rtol=0, atol=1e-18)
+        p0, e0, st_p, st_q = out["p0"], out["euler_t"], out["adam_p0"], out["adam_pose"]

@@ -1,7 +1,7 @@
-"""Build a libpa.so variant with extra -D macros into variants/<name>/libpa.so (A/B timing; load it
-with PA_LIB_PATH=variants/<name>/libpa.so).  Usage: python tools/build_variant.py name -DMACRO=V ..."""
+"""Build a libpa.so variant with extra -D macros into variants/<name>/libpa.so (A/B timing of compile-time
+kernel parameters; load it with PA_LIB_PATH=variants/<name>/libpa.so).
+Usage: python tools/build_variant.py name -DMACRO=V ..."""
 import os
-import subprocess
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -9,7 +9,4 @@ from paper_2604_09643_b200 import build as b  # noqa: E402
 
 name, defs = sys.argv[1], sys.argv[2:]
 out = os.path.join(b.ROOT, "variants", name)
-os.makedirs(out, exist_ok=True)
-cmd = [b.NVCC, *b.FLAGS, *defs, "-I", os.path.join(b.ROOT, "include"), "-o", os.path.join(out, "libpa.so"), *b.SRC]
-subprocess.check_call(cmd)
-print(os.path.join(out, "libpa.so"))
+print(b.build(force=True, defs=defs, lib=os.path.join(out, "libpa.so"), objdir=os.path.join(out, "obj")))
