@@ -26,19 +26,28 @@ sys.path.insert(0, ROOT)
 
 METRIC = "forward+adjoint voxel·element·sample updates/s; s per SfM iteration @1/2/4/8"
 UNIT = "updates/s"
-# Algorithmic FP32 lane-ops per in-window update: forward 4 + 0.5
-# amortised setup; fused adjoint + pose 8 + 1 LDS (amortised setup included).
-OPS_FWD = 4.5
-OPS_ADJ = 8.5
 N_SM = 148
 LANES = 128
-# kernel families (f3): algorithmic ops per in-window update and the pipe that bounds them.
+# Roofline basis: ALGORITHMIC lane-ops per (voxel, element) pair of the kernel that runs, counted
+# from its arithmetic (FP32 ops, packed ops as 2, MUFU, integer ops of the algorithm, loads / shared-memory
+# atomics as 1; loop control, addressing and spills not counted), against 148 SM x 128 lanes x clock (the
+# FP32-pipe peak = the issue peak of 4 warp-instr/clk/SM x 32 lanes).  Pairs = updates / W, W = 2 kappa sigma /
+# (c dt) (in-window samples per pair).  The direct kernels (exp / power-law families, Gaussian fallback) walk the
+# window: the survey's per-update basis x W.
+OPS_PAIR = {
+    "k_fwd_dep": 87.0,            # K1d: geometry 29 + 6-channel deposit arithmetic 39 + 7 ATOMS / 7 bias / 3 address
+    "k_adjoint_tay2_8": 73.5,     # K2c, 32-B records: geometry 23.5 + series & moments 35 + gradient 7.5 + reduction 7.5
+    "k_adjoint_tay2_12": 85.5,    # K2c, 48-B records (short windows): synthetic division 27 instead of 15
+    "k_adjoint_svd": 82.5,        # K2s: geometry 23.5 + rank-R basis evaluation 44 + gradient 7.5 + reduction 7.5
+}
+OPS_UPDATE_DIRECT = {"fwd": 4.5, "adj": 8.5}  # recurrence walk, FP32 lane-ops per in-window update
+# kernel families (f3): the direct kernels and the pipe that bounds them
 #   exp: E = min(A K_i, B/K_i) -> 2 FMUL + 1 MIN + D + FFMA (+0.5 setup) forward; adjoint + pose adds
 #        g E, |D| and three sums (SE, SD, SX)
 #   pow: MUFU-bound: lg2 + ex2 per update forward, + ex2(-lg2 x) for the pose sum; 16 XU lanes/SM
 FAMILIES = {
-    "gauss": dict(fwd=OPS_FWD, adj=OPS_ADJ, lanes=LANES, unit="T FP32-lane-op/s", pipe="128 FP32 lanes"),
-    "exp": dict(fwd=5.5, adj=9.5, lanes=LANES, unit="T FP32-lane-op/s", pipe="128 FP32 lanes"),
+    "gauss": dict(fwd=4.5, adj=8.5, lanes=LANES, unit="T lane-op/s", pipe="128 lanes (FP32 pipe = issue peak)"),
+    "exp": dict(fwd=5.5, adj=9.5, lanes=LANES, unit="T lane-op/s", pipe="128 lanes (FP32 pipe = issue peak)"),
     "pow": dict(fwd=2.0, adj=3.0, lanes=16, unit="T MUFU-op/s", pipe="16 MUFU (XU) lanes"),
 }
 
@@ -106,35 +115,72 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_sample(w, p0, poses, target_s=12.0):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: frame 0, the first
-    E_s elements: forward + adjoint + element gradient.  Returns (updates/s, cores, sample string)."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(w, p0, poses, rows=None, sub=128, frame=0):
+    """The bounded oracle sample of a workload: frame `frame`, the first `rows` elements (default 4 x the host's
+    cores, so the oracle's (frame, element)-parallel loops use every core), on the central sub^3 voxel
+    sub-volume; forward + adjoint + element gradient (the GPU's two passes), exact in-window count n.
+    Returns (run, n, description); run() executes the sample once."""
     import oracle
 
     oracle.build()
-    E_s = 1
-    tmpl = w.tmpl
-    cot = None
-    # grow the element count until the sample is ~target_s of CPU work
-    while True:
-        t0 = time.perf_counter()
-        sel = tmpl[:E_s]
-        pz = poses[:1]
-        y = oracle.forward(w.grid, w.acq, sel, pz, p0)
-        cot = np.random.default_rng(0).normal(size=y.shape)
-        oracle.adjoint(w.grid, w.acq, sel, pz, cot)
-        oracle.elem_grad(w.grid, w.acq, sel, pz, p0, cot)
-        dt = time.perf_counter() - t0
-        n, _ = oracle.count(w.grid, w.acq, sel, pz)
-        if dt * 2 > target_s or E_s * 2 > w.E:
-            break
-        E_s *= 2
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return 2.0 * n / dt, cores, f"frame 0, elements 0..{E_s - 1} of {w.E}: forward + adjoint + element gradient ({2 * n:.3e} updates, {dt:.1f} s)"
+    cores = os.cpu_count() or 1
+    rows = min(w.E, rows or 4 * cores)
+    g = dict(w.grid)
+    lo = [max(0, (g[k] - sub) // 2) for k in ("nx", "ny", "nz")]
+    n3 = [min(sub, g[k]) for k in ("nx", "ny", "nz")]
+    sg = dict(nx=n3[0], ny=n3[1], nz=n3[2], pitch=g["pitch"],
+              origin=[g["origin"][i] + g["pitch"] * lo[i] for i in range(3)])
+    sp = np.ascontiguousarray(p0[lo[2]:lo[2] + n3[2], lo[1]:lo[1] + n3[1], lo[0]:lo[0] + n3[0]])
+    tm, pz = w.tmpl[:rows], poses[frame:frame + 1]
+    n, _ = oracle.count(sg, w.acq, tm, pz)
+    cot = np.random.default_rng(0).normal(size=(1, rows, w.acq["nt"]))
+
+    def run():
+        oracle.forward(sg, w.acq, tm, pz, sp)
+        oracle.adjoint(sg, w.acq, tm, pz, cot)
+        oracle.elem_grad(sg, w.acq, tm, pz, sp, cot)
+
+    desc = (f"frame {frame}, elements 0..{rows - 1} of {w.E} ({rows} (frame, element) rows), central "
+            f"{n3[0]}x{n3[1]}x{n3[2]} sub-volume: forward + adjoint + element gradient, {2 * n:.3e} counted updates")
+    return run, n, desc
+
+
+def cpu_oracle_sample(w, p0, poses):
+    """cpu_baseline: the fp64 oracle (as it stands) on all host cores and on 1 thread, on a bounded sample of
+    the workload (~10-20 s).  Returns the cpu_baseline dict."""
+    import oracle
+
+    cores = os.cpu_count() or 1
+    run, n, desc = oracle_sample(w, p0, poses)
+    oracle.set_threads(cores)
+    t0 = time.perf_counter()
+    run()
+    dt = time.perf_counter() - t0
+    # 1-thread rate on 1/cores of the rows (same per-row work)
+    run1, n1, desc1 = oracle_sample(w, p0, poses, rows=max(1, 4))
+    oracle.set_threads(1)
+    t1 = time.perf_counter()
+    run1()
+    dt1 = time.perf_counter() - t1
+    oracle.set_threads(cores)
+    return {"value": 2.0 * n / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc + f" ({dt:.1f} s)",
+            "single_thread": {"value": 2.0 * n1 / dt1, "unit": UNIT, "sample": desc1 + f" ({dt1:.1f} s)"},
+            "cpu": cpu_model()}
 
 
 def run_reference(args):
-    """--impl reference: the fp64 oracle on host cores, each step a bounded sample (rank 0 only)."""
+    """--impl reference: the fp64 oracle on all host cores, each step a bounded sample of the same workload
+    (rank 0 only; the sample is sized to ~8 s so that --steps 20 --warmup 5 ends within a few minutes)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -145,39 +191,29 @@ def run_reference(args):
     w.acq = gen.family_acq(w.acq, args.kernel, args.nu)
     p0 = gen.phantom(w)
     poses = w.poses_true()
-    # size the per-step sample once (about 10-20 s of CPU work)
-    E_s = 1
-    while True:
-        t0 = time.perf_counter()
-        y = oracle.forward(w.grid, w.acq, w.tmpl[:E_s], poses[:1], p0)
-        dt = time.perf_counter() - t0
-        if dt * 3 * 2 > 15.0 or E_s * 2 > w.E:
-            break
-        E_s *= 2
-    sel, pz = w.tmpl[:E_s], poses[:1]
-    n, _ = oracle.count(w.grid, w.acq, sel, pz)
-    cot = np.random.default_rng(0).normal(size=(1, E_s, w.acq["nt"]))
-
-    def step():
-        y = oracle.forward(w.grid, w.acq, sel, pz, p0)
-        oracle.adjoint(w.grid, w.acq, sel, pz, cot)
-        oracle.elem_grad(w.grid, w.acq, sel, pz, p0, cot)
-        return y
-
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    sub = 128
+    run, n, desc = oracle_sample(w, p0, poses, sub=sub)
+    t0 = time.perf_counter()
+    run()
+    if time.perf_counter() - t0 > 12.0:  # keep the whole run within minutes
+        sub = 96
+        run, n, desc = oracle_sample(w, p0, poses, sub=sub)
     for _ in range(args.warmup):
-        step()
+        run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        step()
+        run()
     dt = (time.perf_counter() - t0) / max(args.steps, 1)
     value = 2.0 * n / dt
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    sample = f"frame 0, elements 0..{E_s - 1} of {w.E}: forward + adjoint + element gradient per step"
+    sample = desc + " per step"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": describe(w), "kernel": args.kernel, "sample": sample},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -226,16 +262,20 @@ def main():
     w = gen.workload(args.config, frames=args.frames)
     w.acq = gen.family_acq(w.acq, args.kernel, args.nu)
     p_true = gen.phantom(w).astype(np.float32)
-    frames = shard_frames(w.F, world, rank)
-    Fl = len(frames)
     T = lambda a: torch.tensor(np.asarray(a, dtype=np.float32), device=dev)  # noqa: E731
     tmpl = T(w.tmpl)
+    e_all = gen.perturb_euler(w.euler_true, 1.0, 0.5, seed=w.seed + 100)
+    # frames by greedy longest-processing-time on the exact per-frame in-window counts of the initial poses
+    # (every rank computes the same counts, so the partition needs no communication)
+    _, per_frame = ctx.count(w.grid, w.acq, tmpl, T(gen.poses_from_euler(e_all)))
+    frames = shard_frames(w.F, world, rank, cost=per_frame if world > 1 else None)
+    Fl = len(frames)
     poses_true = T(w.poses_true()[frames])
     meas = ctx.forward(w.grid, w.acq, tmpl, poses_true, T(p_true))           # synthetic measurements
-    e_init = gen.perturb_euler(w.euler_true, 1.0, 0.5, seed=w.seed + 100)[frames]
+    e_init = e_all[frames]
     p_init = np.full(p_true.shape, 0.05, dtype=np.float32)
     nvox = p_true.size
-    n_local, _ = ctx.count(w.grid, w.acq, tmpl, poses_true)                 # exact in-window count
+    n_local = int(per_frame[frames].sum())                                   # exact in-window count
     cnt = torch.tensor([float(n_local)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(cnt)
@@ -301,7 +341,7 @@ def main():
         meas_d = torch.empty_like(meas)
         h2d = meas_h.numel() * 4 + p_h.numel() * 4 + e_h.numel() * 4
         d2h = out_p.numel() * 4 + out_e.numel() * 4 + out_l.numel() * 4
-        k = 1
+        k = 3  # >= 3 steps: the copies (~10 ms) resolve against seconds of compute
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -328,79 +368,107 @@ def main():
         dist.destroy_process_group()
         return
     clocks = clk.summary()
-    # roofline of the dominant kernel (adjoint+pose): FP32 lane-ops / s vs 148 SM x 128 lanes x clock
+    # roofline of the dominant kernel: algorithmic lane-ops per pair (OPS_PAIR) x pairs / its live time, vs
+    # 148 SM x 128 lanes x clock; the per-rank share of the work (frames are LPT-balanced)
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
         peaks = json.load(fh)
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    fam = FAMILIES[args.kernel]
-    ops_fwd, ops_adj, lanes = fam["fwd"], fam["adj"], fam["lanes"]
-    peak = N_SM * lanes * f_max / 1e12
-    U_local_max = U / world  # frames are balanced; per-GPU roofline uses the per-rank share
-    adj_achieved = U_local_max * ops_adj / (ams / 1e3) / 1e12 if ams > 0 else None
-    fwd_achieved = U_local_max * ops_fwd / (fms / 1e3) / 1e12 if fms > 0 else None
-    fwd_frac = fwd_achieved / peak if fwd_achieved else None
-    adj_frac = adj_achieved / peak if adj_achieved else None
     f_meas = clocks["sm_mhz"] * 1e6 if clocks.get("sm_mhz") else None
-    gauss = args.kernel == "gauss"
-    # the kernels this geometry ran with (host-only plan query; env overrides included)
+    fam = FAMILIES[args.kernel]
+    from paper_2604_09643_b200 import build as pa_build
     from paper_2604_09643_b200._pa import plan_info
-    plan = plan_info(w.grid, w.acq, w.E)
-    fwd_name = ("k_fwd_dep (K1d, deposit-form forward + fused loss/cotangent)" if plan["fwd_deposit"]
-                else "k_forward (K1, direct forward + fused loss/cotangent)")
-    adj_name = ("k_adj_svd_filter + k_adjoint_svd (K2s, rank-R-basis adjoint + pose gradient)" if plan["adj_svd"]
-                else "k_adj_filter + k_adjoint_tay2 (K2a/K2c, moment-filter adjoint + pose gradient)" if plan["adj_taylor"]
-                else "k_adjoint (K2, direct adjoint + pose gradient)")
-    k_fwd = {"kernel": fwd_name, "achieved": fwd_achieved, "frac": fwd_frac, "ops_per_update": ops_fwd, "ms_per_step": fms}
-    k_adj = {"kernel": adj_name, "achieved": adj_achieved, "frac": adj_frac, "ops_per_update": ops_adj, "ms_per_step": ams}
+    plan = plan_info(w.grid, w.acq, w.E)  # host-only: the kernels this geometry runs
+    W = 2.0 * w.acq["kappa"] * w.acq["sigma"] / (w.acq["c"] * w.acq["dt"])  # in-window samples per pair
+    U_rank = float(n_local)  # updates per pass on this rank (rank 0 prints; LPT keeps ranks within a frame)
+    if plan["fwd_deposit"]:
+        fwd_name, fwd_ops = "k_fwd_dep (K1d, deposit-form forward + fused loss/cotangent)", OPS_PAIR["k_fwd_dep"] / W
+    else:
+        fwd_name, fwd_ops = "k_forward (K1, direct forward + fused loss/cotangent)", fam["fwd"]
+    if plan["adj_kernel"] == 2:
+        adj_name, adj_ops = "k_adj_svd_filter + k_adjoint_svd (K2s, rank-R-basis adjoint + pose gradient)", OPS_PAIR["k_adjoint_svd"] / W
+    elif plan["adj_kernel"] == 1:
+        nf = 8 if plan["tay_order"] == 5 else 12
+        adj_name = f"k_adj_filter + k_adjoint_tay2 (K2a/K2c, moment-filter adjoint + pose gradient, {4 * nf}-B records)"
+        adj_ops = OPS_PAIR[f"k_adjoint_tay2_{nf}"] / W
+    else:
+        adj_name, adj_ops = "k_adjoint (K2, direct adjoint + pose gradient)", fam["adj"]
+    lanes = fam["lanes"] if not (plan["fwd_deposit"] or plan["adj_kernel"]) else LANES
+    peak = N_SM * lanes * f_max / 1e12
+
+    def kinfo(name, ops, ms_):
+        ach = U_rank * ops / (ms_ / 1e3) / 1e12 if ms_ > 0 else None
+        return {"kernel": name, "achieved": ach, "frac": ach / peak if ach else None, "ops_per_update": ops,
+                "ops_per_pair": ops * W, "ms_per_step": ms_,
+                "frac_at_measured_clock": (ach * 1e12 / (N_SM * lanes * f_meas)) if (ach and f_meas) else None}
+
+    k_fwd, k_adj = kinfo(fwd_name, fwd_ops, fms), kinfo(adj_name, adj_ops, ams)
     dom, other = (k_fwd, k_adj) if fms >= ams else (k_adj, k_fwd)
-    # measured DRAM bytes per launch (ncu, default C4 command; profiles/r1_traffic_c4.json) — only for
-    # the workload it was measured on
+    # hardware-side check of the same kernels: warp instructions per update from an ncu capture of THIS build
+    # (profiles/*_issue_c4.json stamped with libpa's source hash; a capture of another build is refused)
+    issue, issue_note = None, None
+    src_hash = pa_build.source_hash()
+    caps = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_issue_c4.json"))
+    for fname in reversed(caps):
+        try:
+            with open(os.path.join(ROOT, "profiles", fname)) as fh:
+                iss = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        if iss.get("libpa_hash") != src_hash:
+            issue_note = f"no ncu capture of this build (libpa {src_hash}); latest {fname} is of {iss.get('libpa_hash')}"
+            continue
+        if args.config == "c4" and args.kernel == "gauss":
+            ipk = N_SM * 4 * f_max / 1e12
+            issue = {"unit": "T warp-instr/s", "peak": ipk, "source": f"profiles/{fname} (libpa {src_hash})"}
+            for key, kk in (("forward", k_fwd), ("adjoint", k_adj)):
+                ipu = iss[key]["warp_inst_per_update"]
+                ach = U_rank * ipu / (kk["ms_per_step"] / 1e3) / 1e12
+                issue[key] = {"achieved": ach, "frac": ach / ipk, "warp_inst_per_update": ipu,
+                              "lane_instr_per_pair": 32 * ipu * W}
+            issue["frac"] = issue["adjoint" if dom is k_adj else "forward"]["frac"]
+            issue_note = None
+        break
+    # measured DRAM bytes per launch (ncu launch list of the default C4 command, same build)
     traffic, traffic_note = None, None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic_c4.json")) as fh:
-            tr = json.load(fh)
-        if args.config == "c4" and gauss and Fl == 400:
+    for fname in sorted((f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_traffic_c4.json")),
+                        reverse=True):
+        try:
+            with open(os.path.join(ROOT, "profiles", fname)) as fh:
+                tr = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        if tr.get("libpa_hash") == src_hash and args.config == "c4" and args.kernel == "gauss" and world == 1:
             t = tr["forward" if dom is k_fwd else "adjoint"]
             traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
             traffic_note = tr.get("note")
-    except (OSError, KeyError, ValueError):
-        traffic = None
-    # hardware-side check of the same kernel: warp instructions it issues per in-window update (ncu
-    # smsp__inst_executed.sum / exact updates of the captured launch, profiles/r1_issue_c4.json) x this
-    # run's updates / its live kernel time, against the issue peak 148 SM x 4 warp-instr/clk x sm_max
-    issue = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_issue_c4.json")) as fh:
-            iss = json.load(fh)
-        if args.config == "c4" and gauss:
-            key = "forward" if dom is k_fwd else "adjoint"
-            ipu = iss[key]["warp_inst_per_update"]
-            t_s = dom["ms_per_step"] / 1e3
-            ach = U_local_max * ipu / t_s / 1e12
-            ipk = N_SM * 4 * f_max / 1e12
-            issue = {"achieved": ach, "peak": ipk, "unit": "T warp-instr/s", "frac": ach / ipk,
-                     "warp_inst_per_update": ipu, "source": iss[key]["source"]}
-    except (OSError, KeyError, ValueError):
-        issue = None
+        break
     roofline = {"bound": "alu", "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
-                "unit": fam["unit"], "frac": dom["frac"], "traffic": traffic, "traffic_unit": "bytes/launch",
-                "peak_basis": f"148 SM x {fam['pipe']} x sm_max {f_max / 1e6:.0f} MHz (MEASURED_PEAKS.json)",
-                "ops_per_update": dom["ops_per_update"], "kernel_ms_per_step": dom["ms_per_step"],
+                "unit": fam["unit"] if lanes != LANES else "T lane-op/s", "frac": dom["frac"], "traffic": traffic,
+                "traffic_unit": "bytes/launch",
+                "peak_basis": f"148 SM x {lanes} lanes x sm_max {f_max / 1e6:.0f} MHz (MEASURED_PEAKS.json): the FP32-pipe "
+                              f"peak = the issue peak (4 warp-instr/clk/SM x 32 lanes)",
+                "ops_basis": "algorithmic lane-ops per (voxel, element) pair of the running kernel (DESIGN.md §7) / "
+                             f"W = {W:.2f} in-window samples per pair",
+                "ops_per_update": dom["ops_per_update"], "ops_per_pair": dom["ops_per_pair"],
+                "kernel_ms_per_step": dom["ms_per_step"],
                 "kernel_share_of_step": dom["ms_per_step"] / ms if ms > 0 else None,
-                "frac_at_measured_clock": (dom["achieved"] * 1e12 / (N_SM * lanes * f_meas)) if (dom["achieved"] and f_meas) else None,
-                "other_kernel": other,
-                "step_frac": (U_local_max * (ops_fwd + ops_adj) / (ms / 1e3) / 1e12) / peak if ms > 0 else None,
-                "traffic_note": traffic_note, "issue": issue}
+                "frac_at_measured_clock": dom["frac_at_measured_clock"], "other_kernel": other,
+                "step_frac": (U_rank * (fwd_ops + adj_ops) / (ms / 1e3) / 1e12) / peak if ms > 0 else None,
+                "traffic_note": traffic_note, "issue": issue, "issue_note": issue_note,
+                "dense_equivalent": {"value": value * w.acq["nt"] / W, "unit": "voxel·element·sample terms/s",
+                                     "note": f"secondary figure: the same work counted on all N_t = {w.acq['nt']} samples "
+                                             f"per pair, the paper's O(N_s N_d N_t) framing (P:347) = value x N_t / W"}}
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, cores, sample = cpu_oracle_sample(w, p_true.astype(np.float64), w.poses_true())
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = cpu_oracle_sample(w, p_true.astype(np.float64), w.poses_true())
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "s_per_iteration": ms / 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded vascular phantom, freehand sweep; meas = forward at true poses)",
         "config": {"workload": describe(w), "kernel": args.kernel, "frames_per_rank": Fl, "updates_per_pass": U,
-                   "parallelism": f"frame-sharded x{world}, NCCL all-reduce of dL/dp0",
+                   "parallelism": f"frame-sharded x{world} (LPT on exact per-frame counts), NCCL all-reduce of dL/dp0",
+                   "plan": {k: plan[k] for k in ("lmin", "fwd_deposit", "dep_rank", "adj_kernel", "tay_order")},
+                   "libpa_hash": src_hash,
                    "l2": "inputs larger than L2 (meas + cotangent per step) and a 256 MiB L2 flush before every timed step"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": n_launch,

@@ -88,6 +88,15 @@ def _p(x):
     return x.ctypes.data_as(ctypes.c_void_p) if x is not None else None
 
 
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's loops (bench.py's cpu_baseline: the 1-thread and all-core rates)."""
+    _load().oracle_set_threads(ctypes.c_int32(int(n)))
+
+
+def threads() -> int:
+    return int(_load().oracle_get_threads())
+
+
 def place(tmpl, poses):
     tmpl, poses = _d(tmpl), _d(poses)
     E, F = tmpl.shape[0], poses.shape[0]

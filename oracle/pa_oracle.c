@@ -31,6 +31,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <omp.h>
 
 typedef struct {
     int32_t nx, ny, nz;
@@ -140,6 +141,10 @@ static double dkern_dr(const og_acq *a, double r, int j)
     double D = r - a->c * (a->t0 + (double)j * a->dt);
     return kfun(a, D) / (2.0 * r) * ((1.0 + dlogk_times_D(a, D)) - D / r);
 }
+
+/* OpenMP threads of the oracle's parallel loops (the cpu_baseline's 1-thread and all-core rates). */
+void oracle_set_threads(int32_t n) { omp_set_num_threads(n > 0 ? n : 1); }
+int32_t oracle_get_threads(void) { return omp_get_max_threads(); }
 
 /* ---------------------------------------------------------------------------
  * a2: forward radiation (Eq. gpu_forward_model; Eq. 1)

@@ -23,6 +23,18 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", *ARCH, "-lineinfo", "-ftz=true", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
 
 
+def source_hash() -> str:
+    """sha256 (16 hex) of every source libpa is built from: stamps ncu captures (profiles/) so bench.py can
+    refuse counters measured on another build."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for p in sorted(DEPS):
+        with open(p, "rb") as fh:
+            h.update(os.path.basename(p).encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
 def stale(lib: str = LIB) -> bool:
     if not os.path.exists(lib):
         return True

@@ -7,23 +7,25 @@
 namespace pa {
 
 namespace {
-template <int M, bool POSE, bool ADJ>
+template <int NF, bool POSE, bool ADJ>
 pa_status launch_tay_t(pa_ctx *ctx, const Plan &pl, const float *poses, const float *tmpl, const float *p0,
                        const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry, cudaStream_t st)
 {
-    using T = TayCfg<M>;
-    const int E = pl.g.E, F = pl.g.F, NJ = pl.g.nt + pl.g.lmin;
-    const size_t per_frame = (size_t)E * NJ * T::NF * sizeof(float);
+    using T = TayCfg<NF>;
+    const int E = pl.g.E, F = pl.g.F, E4 = (E + 3) & ~3;
+    const int njp = pl.g.nt + pl.g.lmin + 2 * pl.tay_pad;  // zero-padded record row
+    const size_t per_frame = (size_t)E * njp * T::NF * sizeof(float);
     int Fc = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t(48) << 20) / per_frame));
     auto smem_of = [&](int fc) {
-        return ((size_t)E * 12 * 2 + (size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
+        return (size_t)2 * E4 * sizeof(AncT) +
+               ((size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
     };
     while (Fc > 1 && smem_of(Fc) > 113 * 1024) --Fc;
     Fc = std::min(Fc, std::max(1, 65535 / E));  // K2a grid.y = Fc E
     Fc = std::min(Fc, F > 0 ? F : 1);
     const size_t smem = smem_of(Fc);
     if (smem > 227 * 1024) return fail(PA_EUNSUPPORTED, "E=%d too large for the adjoint kernel's shared memory", E);
-    auto kern = k_adjoint_tay2<M, POSE, ADJ>;
+    auto kern = k_adjoint_tay2<NF, POSE, ADJ>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
@@ -41,23 +43,24 @@ pa_status launch_tay_t(pa_ctx *ctx, const Plan &pl, const float *poses, const fl
     for (int f0 = 0; f0 < F; f0 += Fc) {
         const int fn = std::min(Fc, F - f0);
         ++g_nlaunch;
-        k_adj_filter<M><<<dim3((NJ + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.tf, cot, f0, fn, Fg);
+        k_adj_filter<NF><<<dim3((njp + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.tf, cot, f0, fn, njp, Fg);
         CUDA_TRY(cudaGetLastError());
         ++g_nlaunch;
-        kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.tc, poses, tmpl, p0, cot, Fg, grad_p0, partial, f0, fn);
+        kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.tc, poses, tmpl, p0, Fg, grad_p0, partial, f0, fn, njp,
+                                           pl.tay_pad, pl.tay_sentinel);
         CUDA_TRY(cudaGetLastError());
     }
     return PA_OK;
 }
 
-template <int M>
+template <int NF>
 pa_status launch_tay_m(pa_ctx *ctx, const Plan &pl, bool pose, bool adj, const float *poses, const float *tmpl,
                        const float *p0, const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry,
                        cudaStream_t st)
 {
-    if (pose && adj) return launch_tay_t<M, true, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    if (pose) return launch_tay_t<M, true, false>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    return launch_tay_t<M, false, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    if (pose && adj) return launch_tay_t<NF, true, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    if (pose) return launch_tay_t<NF, true, false>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    return launch_tay_t<NF, false, true>(ctx, pl, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
 }
 }  // namespace
 
@@ -65,14 +68,9 @@ pa_status launch_adjoint_tay(pa_ctx *ctx, const Plan &pl, bool pose, bool adj, c
                              const float *p0, const float *cot, float *grad_p0, float *partial, AdjLaunch &L, bool dry,
                              cudaStream_t st)
 {
-    switch (pl.tay_M) {
-    case 4: return launch_tay_m<4>(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    case 5: return launch_tay_m<5>(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    case 6: return launch_tay_m<6>(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    case 7: return launch_tay_m<7>(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    case 8: return launch_tay_m<8>(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    default: return fail(PA_EUNSUPPORTED, "no moment-filter adjoint for Taylor order %d", pl.tay_M);
-    }
+    if (pl.tay_NF == 8) return launch_tay_m<8>(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    if (pl.tay_NF == 12) return launch_tay_m<12>(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    return fail(PA_EUNSUPPORTED, "no moment-filter adjoint for record size %d", pl.tay_NF);
 }
 
 }  // namespace pa

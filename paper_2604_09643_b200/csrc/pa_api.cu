@@ -45,8 +45,11 @@ inline bool aligned4(const void *p) { return p != nullptr && (reinterpret_cast<u
 constexpr int FAST_LMIN = 12;
 
 // Moment-filter constants (K2a/K2c, pa_kernels.cuh) and the bound on the Taylor remainder of
-// e^{dl k}, |dl| <= (a/s)^2/2 (+2%), relative to sum_k C'_k |k|^n, n = 0..2: the smallest order
-// M in [4, 8] whose bound is <= 4e-7 (below the direct sum's fp32 rounding, L 2^-24).
+// e^{dl k}, |dl| <= (a/s)^2/2 (+2%), relative to sum_k C'_k |k|^n.  The record holds H_p = F_p/p!,
+// p < NPS = NF - 1, so S0, S1, S2 run to orders NPS-1, NPS-2, NPS-3: the 32-B record (NF = 8: orders
+// 6/5/4) when the bounds hold — S0, S1 <= 4e-7 (below the direct sum's fp32 rounding, L 2^-24), the pose
+// moment S2 <= 1e-5 (as K2s's pose moment) — else the 48-B record (NF = 12: orders 10/9/8).  The taps
+// carry the 1/2 of D/(2r).
 void make_tay(Plan &pl, int lmin, double a, double sig)
 {
     const int MA = (lmin + 1) / 2;
@@ -56,45 +59,55 @@ void make_tay(Plan &pl, int lmin, double a, double sig)
     std::memset(&pl.tf, 0, sizeof pl.tf);
     pl.tc.lam0 = (float)lam0;
     pl.tc.lam_s = (float)as2;
+    pl.tc.c_a = (float)(-2.0 * a / (sig * sig));
+    pl.tc.c_aa = (float)(2.0 * a * a / (sig * sig));
     const int kt = lmin - MA;
-    pl.tc.Ckt = (float)std::exp(-(double)kt * kt * a * a / (2.0 * sig * sig));
-    for (int m = 0; m < 8; ++m) pl.tc.inv[m] = (float)(1.0 / (m + 1));
+    pl.tf.gx = (float)(0.5 * std::exp(-(double)kt * kt * a * a / (2.0 * sig * sig)));
     const double dl = 0.5 * as2 * a * 1.02;
-    auto bound = [&](int M) {
+    auto bound = [&](int M, int n) {  // remainder of the order-M series of moment n, relative to sum |terms|
         double fact = 1.0;
         for (int i = 2; i <= M + 1; ++i) fact *= i;
-        double worst = 0.0;
-        for (int n = 0; n < 3; ++n) {
-            double num = 0.0, den = 0.0;
-            for (int t = 0; t <= lmin; ++t) {
-                const double k = t - MA;
-                const double cp = std::exp(-k * k * a * a / (2.0 * sig * sig)) * std::exp(lam0 * k);
-                const double x = dl * std::fabs(k);
-                num += cp * std::pow(std::fabs(k), n) * std::pow(x, M + 1) / fact * std::exp(x);
-                den += cp * std::pow(std::fabs(k), n);
-            }
-            worst = std::max(worst, num / den);
+        double num = 0.0, den = 0.0;
+        for (int t = 0; t <= lmin; ++t) {
+            const double k = t - MA;
+            const double cp = std::exp(-k * k * a * a / (2.0 * sig * sig)) * std::exp(lam0 * k);
+            const double x = dl * std::fabs(k);
+            num += cp * std::pow(std::fabs(k), n) * std::pow(x, M + 1) / fact * std::exp(x);
+            den += cp * std::pow(std::fabs(k), n);
         }
-        return worst;
+        return num / den;
     };
     pl.tay_ok = false;
-    pl.tay_M = 8;
+    pl.tay_NF = 12;
     pl.tay_err = 1.0;
-    for (int M = 4; M <= 8; ++M) {
-        const double b = bound(M);
-        pl.tay_M = M;
-        pl.tay_err = b;
-        if (b <= 4e-7) {
+    for (int NF : {8, 12}) {
+        const int NPS = NF - 1;
+        const double b = std::max(bound(NPS - 1, 0), bound(NPS - 2, 1)), b2 = bound(NPS - 3, 2);
+        pl.tay_NF = NF;
+        pl.tay_err = std::max(b, b2 / 25.0);  // reported on the adjoint's scale (pose bound 1e-5 = 25 x 4e-7)
+        if (b <= 4e-7 && b2 <= 1e-5) {
             pl.tay_ok = true;
             break;
         }
     }
-    const int NP = pl.tay_M + 3;
+    const int NP = pl.tay_NF - 1;
     for (int t = 0; t < lmin; ++t) {
         const double k = t - MA;
         const double cp = std::exp(-k * k * a * a / (2.0 * sig * sig)) * std::exp(lam0 * k);
-        for (int p = 0; p < NP; ++p) pl.tf.H[t * NP + p] = (float)(cp * std::pow(k, p));
+        double fact = 1.0;
+        for (int p = 0; p < NP; ++p) {
+            if (p > 0) fact *= p;
+            pl.tf.H[t * NP + p] = (float)(0.5 * cp * std::pow(k, p) / fact);
+        }
     }
+    // zero padding of the record rows (K2c reads without bounds checks): a non-culled (tile, element)
+    // window starts within (2 rt + 4a)/a + 1 positions of the row; the sentinel of a culled one lands in
+    // [0, 2 rt/a + 3]
+    const int pad = (int)std::ceil(2.0 * pl.g.rt_d / a) + 16;
+    pl.tf.padl = pad;
+    pl.tay_pad = pad;
+    pl.tay_sentinel = -(int)std::floor((-pl.g.rt_d * 1.001 - 0.5 * a - pl.g.ksig_d) / a) + 1;
+    pl.g.njp_m1 = (unsigned)(pl.g.nt + lmin + 2 * pad - 1);
 }
 
 // Separable factorisation of the forward pulse for the deposit-form forward K1d (pa_kernels.cuh):
@@ -458,7 +471,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     }
     // Gaussian fast path (runtime window length L_min in [FAST_LMIN, PA_LMAX]): K1d, K2a/K2c, K2s
     pl.tay_ok = pl.dep_ok = false;
-    pl.tay_M = 0;
+    pl.tay_NF = 0;
     pl.tay_err = pl.dep_err = pl.svd_derr = 1.0;
     pl.dep_R = 0;
     pl.dep_nw = 0;
@@ -476,9 +489,9 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     if (policy & PA_POLICY_ADJ_DIRECT) pl.adj = ADJ_DIRECT;
     else if ((policy & PA_POLICY_ADJ_SVD) && svd_avail) pl.adj = ADJ_SVD;
     else if ((policy & PA_POLICY_ADJ_TAYLOR) && tay_avail) pl.adj = ADJ_TAY;
-    // default: the Taylor form, except where it needs 48-B filter records (M >= 6, short windows) and the
+    // default: the Taylor form, except where it needs 48-B filter records (short windows) and the
     // rank-R basis is accurate enough (K2s measured 5% faster for the C5 class)
-    else if (svd_avail && (!tay_avail || pl.tay_M >= 6)) pl.adj = ADJ_SVD;
+    else if (svd_avail && (!tay_avail || pl.tay_NF > 8)) pl.adj = ADJ_SVD;
     else if (tay_avail) pl.adj = ADJ_TAY;
     else pl.adj = ADJ_DIRECT;
     if ((!pl.fwd_dep || pl.adj == ADJ_DIRECT) && pl.klass < 0)
@@ -1365,7 +1378,7 @@ static void fill_info(const Plan &pl, pa_plan_info *out)
     out->dep_warps = pl.dep_nw;
     out->dep_err = pl.dep_err;
     out->adj_taylor = (pl.fam == KF_GAUSS && pl.tay_ok && !(pl.policy & PA_POLICY_ADJ_DIRECT)) ? 1 : 0;
-    out->tay_order = pl.tay_M;
+    out->tay_order = pl.tay_NF - 3;  // order of the adjoint moment S1
     out->tay_err = pl.tay_err;
     out->adj_svd = pl.adj == ADJ_SVD ? 1 : 0;
     out->svd_derr = pl.svd_derr;

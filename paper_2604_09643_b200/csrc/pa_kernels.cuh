@@ -46,6 +46,7 @@ struct Geo {
     float s2, inv_s2, rt;
     int mF, mA;                 // recurrence centres (forward cluster window / adjoint pair window)
     int lmin;                   // L_min = floor(2 kappa sigma / (c dt)): window length (L in {lmin, lmin+1})
+    unsigned njp_m1;            // K2c: last record index of a zero-padded filter row
     float ls, nu;               // exponential: log2(e)/s; power law: nu   (kernel families, R23)
 };
 
@@ -995,46 +996,60 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
 // exactly as the direct kernel.  K2a computes F for a frame chunk (L2-resident); K2c (below) replaces
 // the per-voxel L-sample walk by one filter-record load and three M-term Horner evaluations.
 // ============================================================================================
-// Series order M of the Taylor form (a template parameter: it sizes the filter records); the window
-// length L_min is a runtime value (Geo::lmin), up to PA_LMAX.
+// The window length L_min is a runtime value (Geo::lmin), up to PA_LMAX; the record size NF is a
+// template parameter.
+//
+// The moments as one polynomial: with H_p = F_p / p!, P(x) = sum_{p<NPS} H_p x^p gives
+//   S0 = P(dl),  S1 = P'(dl),  S2 = P''(dl)
+// (the Taylor series of S_n is sum_m dl^m/m! F_{n+m}), evaluated together by Horner with synthetic
+// division — S0, S1, S2 to orders NPS-1, NPS-2, NPS-3 from NPS stored values.
+// Filter record of a position (NF floats, one 256-bit load for NF = 8): H_0 .. H_{NPS-1}, NPS = NF - 1,
+// and in the last slot the cotangent sample at the position scaled by C_k(k_t)/2 — the window's optional
+// last tap — so a pair needs exactly one load.  Orders for NF = 8: 6 / 5 / 4; NF = 12 (short windows):
+// 10 / 9 / 8.  The host bounds the remainders: S0, S1 <= 4e-7, the pose moment S2 <= 1e-5 (as K2s's).
+// All filters carry the factor 1/2 of D/(2r).  Rows are zero-padded by PADL / PADR positions on both
+// sides, so every pair of a non-culled (tile, element) — and every pair of a culled one, through a
+// sentinel anchor — addresses a valid position: no per-pair bounds checks (windows outside [0, nt)
+// read zeros).
 constexpr int PA_LMAX = 160;  // longest window (L_min) of the Gaussian fast path (K1d, K2a/K2c, K2s)
-template <int M_>
+template <int NF_>
 struct TayCfg {
-    static constexpr int M = M_;
-    static constexpr int NP = M + 3;                                    // F_0 .. F_{M+2}
-    static constexpr int NF = (NP + 3) & ~3;                            // floats per j (16-B rows)
+    static constexpr int NF = NF_;       // floats per record (32 / 48 B)
+    static constexpr int NPS = NF - 1;   // H_0 .. H_{NPS-1} stored
 };
-constexpr int TAY_MAXNP = 11;  // M <= 8
+constexpr int TAY_MAXNP = 11;  // NF <= 12
 
 struct TayFilt {               // K2a: the filter taps
-    float H[PA_LMAX * TAY_MAXNP];  // H[t][p] = C'_k k^p, k = t - MA, t in [0, L_min), p in [0, NP)
+    float H[PA_LMAX * TAY_MAXNP];  // H[t][p] = C'_k k^p / (2 p!), k = t - MA, t in [0, L_min), p in [0, NPS)
+    float gx;                      // C_k(k_t) / 2 at the extra tap k_t = L_min - MA
+    int padl;                      // leading zero positions of a row
 };
 struct TayConst {              // K2c: the series constants
     float lam0;        // series centre (natural units)
     float lam_s;       // a / s^2: lam = lam_s D_m
-    float Ckt;         // C_k at the extra tap k_t = L_min - MA
-    float inv[8];      // 1/(m+1)
+    float c_a;         // -2 a / s^2   (pose moment Bq / s^2)
+    float c_aa;        // 2 a^2 / s^2  (S2 = 2 x the synthetic-division d2)
 };
 
-template <int M>
+template <int NF>
 __global__ void __launch_bounds__(256) k_adj_filter(Geo g, TayFilt tf, const float *__restrict__ cot, int f0, int fn,
-                                                    float *__restrict__ Fg)
+                                                    int njp, float *__restrict__ Fg)
 {
-    using T = TayCfg<M>;
+    using T = TayCfg<NF>;
     __shared__ float s[256 + PA_LMAX];
     const int lmin = g.lmin;
-    const int NJ = g.nt + lmin;
     const int row = blockIdx.y;  // chunk-local row (f - f0) E + e
-    const int jj0 = blockIdx.x * 256;
+    const int jp0 = blockIdx.x * 256;
+    const int jj0 = jp0 - tf.padl;  // position jj = jp - PADL; j_m = jj + MA - L_min
     const float *gr = cot + ((size_t)f0 * g.E + row) * g.nt;
-    // j_m = jj + MA - L_min; the taps k in [-MA, L_min - MA) read samples jj - L_min + t, t = k + MA
+    // the taps k in [-MA, L_min - MA) read samples jj - L_min + t, t = k + MA; the last tap sample jj
     for (int t = threadIdx.x; t < 256 + lmin; t += 256) {
         const int j = jj0 - lmin + t;
         s[t] = (j >= 0 && j < g.nt) ? __ldg(gr + j) : 0.0f;
     }
     __syncthreads();
-    const int jj = jj0 + threadIdx.x;
-    if (jj >= NJ) return;
+    const int jp = jp0 + threadIdx.x;
+    if (jp >= njp) return;
     float acc[T::NF];
 #pragma unroll
     for (int p = 0; p < T::NF; ++p) acc[p] = 0.0f;
@@ -1042,9 +1057,10 @@ __global__ void __launch_bounds__(256) k_adj_filter(Geo g, TayFilt tf, const flo
     for (int t = 0; t < lmin; ++t) {
         const float v = s[threadIdx.x + t];
 #pragma unroll
-        for (int p = 0; p < T::NP; ++p) acc[p] = __fmaf_rn(v, tf.H[t * T::NP + p], acc[p]);
+        for (int p = 0; p < T::NPS; ++p) acc[p] = __fmaf_rn(v, tf.H[t * T::NPS + p], acc[p]);
     }
-    float4 *o = reinterpret_cast<float4 *>(Fg + ((size_t)row * NJ + jj) * T::NF);
+    acc[T::NF - 1] = s[threadIdx.x + lmin] * tf.gx;  // the last tap's sample g[jj] C_k(k_t) / 2
+    float4 *o = reinterpret_cast<float4 *>(Fg + ((size_t)row * njp + jp) * T::NF);
 #pragma unroll
     for (int q = 0; q < T::NF / 4; ++q) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
 }
@@ -1095,9 +1111,6 @@ struct DepConst {
 #endif
 #ifndef PA_DEP_MAP
 #define PA_DEP_MAP 2  // lane -> voxel map: 2 = two z-adjacent tiles per warp slot (default); 1 = one tile, 2x4x1 per lane; 0 = 2x2x2 cluster
-#endif
-#ifndef PA_DEP_XPRED
-#define PA_DEP_XPRED 0  // 1: the last-tap deposit only by the lanes that have it (a branch)
 #endif
 // |deposit| <= 2^NB with NW warps x PA_DEP_TPR tiles x 256 voxels adding to a word per round: sums < 2^30
 constexpr int dep_ilog2(int x) { return x <= 1 ? 0 : 1 + dep_ilog2(x / 2); }
@@ -1168,19 +1181,6 @@ __device__ __forceinline__ void fwd_epilogue(const Geo &g, const float *y, int f
     if (threadIdx.x == 0) rowloss[fe] = masked ? 0.0 : -COV / (sdy * sds);
 }
 
-// ceil(x) for |x| < 2^22 on the FP32 pipe (round-to-nearest by the 1.5*2^23 shifter, then +1 when
-// below x): bit-identical to ceilf, without the FRND/F2I conversion unit.
-__device__ __forceinline__ float ceil_alu(float x, int &xi)
-{
-    const float sh = __fadd_rn(x, 12582912.0f);
-    float r = __fsub_rn(sh, 12582912.0f);
-    int ri = __float_as_int(sh) - 0x4B400000;
-    const bool up = r < x;
-    r = up ? __fadd_rn(r, 1.0f) : r;
-    xi = up ? ri + 1 : ri;
-    return r;
-}
-
 // Unpredicated shared-memory integer add (ATOMS.ADD, no return value) at addr + OFF: a predicated
 // red is turned into a branch per atomic by ptxas, so lanes without a deposit add 0 to a per-lane
 // dummy word instead.
@@ -1205,8 +1205,11 @@ __device__ __forceinline__ void red_s32(unsigned addr, int v)
     asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
 }
 
+#ifndef PA_DEP_MINB
+#define PA_DEP_MINB 3  // resident CTAs per SM of the 8-warp K1d (<= 80 registers, no spills; 2: 128 registers, 4.5% slower at C4)
+#endif
 template <int RK, int NW, int NG>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, DepConst dc, const float *__restrict__ poses,
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(Geo g, DepConst dc, const float *__restrict__ poses,
                                                                        const float *__restrict__ tmpl,
                                                                        const float *__restrict__ p0,
                                                                        const unsigned *__restrict__ pmax_bits,
@@ -1355,7 +1358,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                 const float posA = (float)(A.JA + LMIN);
                 const float2 tCA = f2(__fmaf_rn(A.CA, dc.tA, dc.tC));
                 // two voxels (vx = 0, 1) per pass in packed fp32x2 (FFMA2/FMUL2/FADD2: half the issue
-                // slots); every scalar step below is the same operation as pair<LMIN>() (R17)
+                // slots); every scalar step below is the same operation as pair() (R17)
+                const int pbase = A.JA + LMIN - 0x4B400000;  // position = pbase + bits(ceil shifter)
 #pragma unroll
                 for (int v = 0; v < 8; v += 2) {
                     const float2 Pv = make_float2(P[v], P[v + 1]);
@@ -1370,17 +1374,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                     const float2 bse = __fadd2_rn(drel, f2(A.CA));
                     const float2 xlo = __fmul2_rn(__fadd2_rn(bse, f2(-g.ksig)), f2(g.inv_a));
                     const float2 xhi = __fmul2_rn(__fadd2_rn(bse, f2(g.ksig)), f2(g.inv_a));
-                    // ceil(xlo) on the FP32 pipe (bit-identical to ceilf)
-                    const float2 sh = __fadd2_rn(xlo, f2(12582912.0f));
-                    float2 clof = __fadd2_rn(sh, f2(-12582912.0f));
-                    const bool upx = clof.x < xlo.x, upy = clof.y < xlo.y;
-                    clof.x = upx ? clof.x + 1.0f : clof.x;
-                    clof.y = upy ? clof.y + 1.0f : clof.y;
-                    const int clox = __float_as_int(sh.x) - 0x4B400000 + (upx ? 1 : 0);
-                    const int cloy = __float_as_int(sh.y) - 0x4B400000 + (upy ? 1 : 0);
+                    // ceil(xlo) = the round-up sum with the 1.5 2^23 shifter (exact for |xlo| < 2^22; == ceilf)
+                    const float shx = __fadd_ru(xlo.x, 12582912.0f), shy = __fadd_ru(xlo.y, 12582912.0f);
+                    const float2 clof = __fadd2_rn(make_float2(shx, shy), f2(-12582912.0f));
                     const float2 cl2 = __fadd2_rn(clof, f2((float)LMIN));
                     const bool Lxx = xhi.x >= cl2.x, Lxy = xhi.y >= cl2.y;  // floor(xhi) - clo + 1 >= LMIN + 1
-                    const int posx = A.JA + LMIN + clox, posy = A.JA + LMIN + cloy;  // j_m + OFF = jlo + LMIN
+                    const int posx = pbase + __float_as_int(shx), posy = pbase + __float_as_int(shy);  // j_m + OFF = jlo + LMIN
                     const bool vax = live && Pv.x != 0.0f && (unsigned)posx < (unsigned)NJ;
                     const bool vay = live && Pv.y != 0.0f && (unsigned)posy < (unsigned)NJ;
                     // t = (D_m - Dc)/Dw, D_m = bse - clo a - MA a
@@ -1392,34 +1391,31 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                     float2 ct = __fmul2_rn(__fmul2_rn(__fmul2_rn(Pv, f2(invP)), rlo), inv_r);
                     ct.x = vax ? ct.x : 0.0f;
                     ct.y = vay ? ct.y : 0.0f;
-                    // c t^i s^k products shared by all channels
-                    const float2 c1 = __fmul2_rn(ct, s2), c2 = __fmul2_rn(c1, s2), c3 = __fmul2_rn(c2, s2);
-                    const float2 o0 = __fmul2_rn(ct, t), o1 = __fmul2_rn(o0, s2), o2 = __fmul2_rn(o1, s2), o3 = __fmul2_rn(o2, s2);
+                    const float2 o0 = __fmul2_rn(ct, t);  // odd channels: c t phi_m(t) = (c t) (c0 + s c1 + s^2 c2 + s^3 c3)
                     // a lane without a deposit (ct = 0: every word 0) adds to its dummy words
                     const unsigned sax = vax ? qbase + ((unsigned)posx & nrm) * (CS * 4) : dbase;
                     const unsigned say = vay ? qbase + ((unsigned)posy & nrm) * (CS * 4) : dbase;
+                    // phi_m by Horner in s = t^2 (3 FFMA2), then x (c or c t) with the 1.5 2^23 shifter riding in
+                    // the last FFMA2: each deposit rounds to an integer (quantisation <= 2 units on a channel <= 8%
+                    // of the trace)
+                    auto poly = [&](int m) {
+                        return __ffma2_rn(__ffma2_rn(__ffma2_rn(dc.cf2[m][3], s2, dc.cf2[m][2]), s2, dc.cf2[m][1]), s2, dc.cf2[m][0]);
+                    };
+                    {  // channel 0: two words, |x| <= 2^NB0 = hi 2^10 + lo, quantum far below fp32 rounding
+                        const float2 xm = __fmul2_rn(poly(0), ct);
+                        const float2 hs = __ffma2_rn(xm, f2(1.0f / 1024.0f), f2(12582912.0f));
+                        const float2 ls = __fadd2_rn(__ffma2_rn(__fadd2_rn(hs, f2(-12582912.0f)), f2(-1024.0f), xm), f2(12582912.0f));
+                        red_s32<0>(sax, __float_as_int(hs.x) - 0x4B400000);
+                        red_s32<0>(say, __float_as_int(hs.y) - 0x4B400000);
+                        red_s32<4 * (R + 1)>(sax, __float_as_int(ls.x) - 0x4B400000);
+                        red_s32<4 * (R + 1)>(say, __float_as_int(ls.y) - 0x4B400000);
+                    }
                     auto chan = [&](auto mc) {
                         constexpr int m = decltype(mc)::value;
-                        const float2 a0 = (m & 1) ? o0 : ct, a1 = (m & 1) ? o1 : c1, a2 = (m & 1) ? o2 : c2,
-                                     a3 = (m & 1) ? o3 : c3;
-                        if constexpr (m == 0) {
-                            // two words: |x| <= 2^NB0 = hi 2^10 + lo, quantum far below fp32 rounding
-                            const float2 xm = __ffma2_rn(a3, dc.cf2[m][3], __ffma2_rn(a2, dc.cf2[m][2], __ffma2_rn(a1, dc.cf2[m][1], __fmul2_rn(a0, dc.cf2[m][0]))));
-                            const float2 hs = __ffma2_rn(xm, f2(1.0f / 1024.0f), f2(12582912.0f));
-                            const float2 ls = __fadd2_rn(__ffma2_rn(__fadd2_rn(hs, f2(-12582912.0f)), f2(-1024.0f), xm), f2(12582912.0f));
-                            red_s32<0>(sax, __float_as_int(hs.x) - 0x4B400000);
-                            red_s32<0>(say, __float_as_int(hs.y) - 0x4B400000);
-                            red_s32<4 * (R + 1)>(sax, __float_as_int(ls.x) - 0x4B400000);
-                            red_s32<4 * (R + 1)>(say, __float_as_int(ls.y) - 0x4B400000);
-                        } else {
-                            // the 1.5 2^23 shifter rides in the first FFMA: each step rounds to an integer
-                            // (quantisation <= 2 units on a channel <= 8% of the trace)
-                            const float2 xm = __ffma2_rn(a3, dc.cf2[m][3], __ffma2_rn(a2, dc.cf2[m][2], __ffma2_rn(a1, dc.cf2[m][1], __ffma2_rn(a0, dc.cf2[m][0], f2(12582912.0f)))));
-                            red_s32<4 * m>(sax, __float_as_int(xm.x) - 0x4B400000);
-                            red_s32<4 * m>(say, __float_as_int(xm.y) - 0x4B400000);
-                        }
+                        const float2 xm = __ffma2_rn(poly(m), (m & 1) ? o0 : ct, f2(12582912.0f));
+                        red_s32<4 * m>(sax, __float_as_int(xm.x) - 0x4B400000);
+                        red_s32<4 * m>(say, __float_as_int(xm.y) - 0x4B400000);
                     };
-                    chan(std::integral_constant<int, 0>{});
                     chan(std::integral_constant<int, 1>{});
                     chan(std::integral_constant<int, 2>{});
                     chan(std::integral_constant<int, 3>{});
@@ -1427,18 +1423,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
                     if constexpr (R > 5) chan(std::integral_constant<int, 5>{});
                     if constexpr (R > 6) chan(std::integral_constant<int, 6>{});
                     static_assert(R >= 5 && R <= 7, "rank 5, 6 or 7");
-                    {  // X: the optional last tap (L = LMIN + 1), a cubic in t
+                    {  // X: the optional last tap (L = LMIN + 1), a cubic in t by Horner
                         const float2 cx = make_float2(Lxx ? ct.x : 0.0f, Lxy ? ct.y : 0.0f);
-                        const float2 ox = make_float2(Lxx ? o0.x : 0.0f, Lxy ? o0.y : 0.0f);
-                        const float2 xm = __ffma2_rn(__fmul2_rn(ox, s2), dc.cf2[R][3], __ffma2_rn(__fmul2_rn(cx, s2), dc.cf2[R][2], __ffma2_rn(ox, dc.cf2[R][1], __ffma2_rn(cx, dc.cf2[R][0], f2(12582912.0f)))));
-#if PA_DEP_XPRED
-                        // only the lanes whose window has the last tap take part (branch)
-                        if (vax && Lxx) red_s32<4 * R>(sax, __float_as_int(xm.x) - 0x4B400000);
-                        if (vay && Lxy) red_s32<4 * R>(say, __float_as_int(xm.y) - 0x4B400000);
-#else
+                        const float2 px = __ffma2_rn(__ffma2_rn(__ffma2_rn(dc.cf2[R][3], t, dc.cf2[R][2]), t, dc.cf2[R][1]), t, dc.cf2[R][0]);
+                        const float2 xm = __ffma2_rn(px, cx, f2(12582912.0f));
                         red_s32<4 * R>(sax, __float_as_int(xm.x) - 0x4B400000);
                         red_s32<4 * R>(say, __float_as_int(xm.y) - 0x4B400000);
-#endif
                     }
                 }
             }
@@ -1497,34 +1487,54 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_fwd_dep(Geo g, Dep
 // ============================================================================================
 // K2c — the moment-filter adjoint (a4 + a5) with two voxels per thread in packed fp32x2.
 //
-// Per (voxel, element): the window of pair() (every step bit-identical, ceil on the FP32 pipe; L_min
-// is the runtime Geo::lmin), the Taylor moments S_n = sum_m dl^m/m! F_{n+m}[j_m]
-// from the L2-resident per-row filters, the exact optional last tap, A1 = u_m (D_m S0 - a S1)
-// and Bq = u_m ((D_m^2 - s^2) S0 - 2 a D_m S1 + a^2 S2).  A thread owns voxels z and z + 2 of an
-// 8x8x4 anchor tile (a CTA = two tiles stacked in z, 128 threads each), so the geometry, the
-// series and the gradient terms of the two voxels run as FFMA2/FMUL2/FADD2, the anchor is read
-// once for both, and their element-gradient terms are summed before the warp reduction.
+// Per (voxel, element): the window of pair() (every step bit-identical; ceil by a round-up add of the
+// 1.5 2^23 shifter; L_min is the runtime Geo::lmin), the Taylor moments S_n = sum_m dl^m/m! F_{n+m}[j_m]
+// from the L2-resident per-row filter records (one 256-bit load per voxel, the last tap included),
+// A1 = u_m (D_m S0 - a S1) and Bq / s^2 = u_m ((D_m^2/s^2 - 1) S0 - (2a/s^2) D_m S1 + (a^2/s^2) S2) (the
+// filters carry the 1/2 of D/(2r)).  A thread owns voxels z and z + 2 of an 8x8x4 anchor tile (a CTA =
+// two tiles stacked in z, 128 threads each), so the geometry, the series and the gradient terms of the
+// two voxels run as FFMA2/FMUL2/FADD2, the anchor is read once for both, and their element-gradient
+// terms are summed before the warp reduction.  No per-pair validity logic: zero-padded filter rows, a
+// sentinel anchor for culled / padding elements, amplitude 0 for voxels outside the grid.
 // ============================================================================================
+struct AncT {  // anchor of K2c / K2s in shared memory (8 words: two 128-bit loads)
+    float dx, dy, dz, rho, rho2, CA;
+    int JAp;   // JA + L_min + PADL: the record index of the window is JAp + clo
+    int pad;
+};
+
+// the shared anchor of (tile, element), or the sentinel of a culled / padding element whose record
+// index lands in the leading zero padding of the row
+__device__ __forceinline__ AncT make_anct(const Geo &g, const Anc &A, bool culled, int padl, int sentinel)
+{
+    AncT s;
+    s.dx = A.dx;
+    s.dy = A.dy;
+    s.dz = A.dz;
+    s.rho = A.rho;
+    s.rho2 = A.rho2;
+    s.CA = A.CA;
+    s.JAp = culled ? sentinel : A.JA + g.lmin + padl;
+    s.pad = 0;
+    return s;
+}
+
 template <int NF>
 struct Tay2A {
-    float Fa[NF], Fb[NF];  // filter values of voxel a (.x) and voxel b (.y), straight from the loads
+    float Fa[NF], Fb[NF];  // records of voxel a (.x) and voxel b (.y), straight from the loads
     float2 Dm, inv_r, dz;
     float dx, dy;
-    float2 gx;  // cotangent at the optional last tap (0 if absent)
-    bool va, vb;
+    bool La, Lb;  // the window has the last tap (L = L_min + 1)
 };
 
 template <int NF>
-__device__ __forceinline__ Tay2A<NF> tay2_stage_a(const Geo &g, const AncS *anc, int e, int E, bool ina,
-                                                                bool inb, float ex, float ey, float2 ez, float2 e2,
-                                                                const float *__restrict__ Frow,
-                                                                const float *__restrict__ crow, int NJ)
+__device__ __forceinline__ Tay2A<NF> tay2_stage_a(const Geo &g, const AncT *anc, int e, float ex2x, float ey2x,
+                                                  float2 ez2x, float2 e2, float2 ez, const float *__restrict__ Frow)
 {
-    const int LMIN = g.lmin, MA = g.mA;  // runtime window length and centre
     Tay2A<NF> o;
-    const int ec = min(e, E - 1);
-    const AncS sa = anc[ec];
-    const float2 num = __ffma2_rn(f2(sa.dx2), f2(ex), __ffma2_rn(f2(sa.dy2), f2(ey), __ffma2_rn(f2(sa.dz2), ez, e2)));
+    const AncT sa = anc[e];
+    // num = 2 d.delta + |delta|^2 exactly as pair(): fma(2dx, ex, ...) == fma(dx, 2ex, ...) (exact doubling)
+    const float2 num = __ffma2_rn(f2(sa.dx), f2(ex2x), __ffma2_rn(f2(sa.dy), f2(ey2x), __ffma2_rn(f2(sa.dz), ez2x, e2)));
     const float2 r2 = __fadd2_rn(f2(sa.rho2), num);
     const float2 inv_r = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
     const float2 den = __fadd2_rn(__fmul2_rn(r2, inv_r), f2(sa.rho));
@@ -1532,102 +1542,106 @@ __device__ __forceinline__ Tay2A<NF> tay2_stage_a(const Geo &g, const AncS *anc,
     const float2 bse = __fadd2_rn(drel, f2(sa.CA));
     const float2 xlo = __fmul2_rn(__fadd2_rn(bse, f2(-g.ksig)), f2(g.inv_a));
     const float2 xhi = __fmul2_rn(__fadd2_rn(bse, f2(g.ksig)), f2(g.inv_a));
-    const float2 sh = __fadd2_rn(xlo, f2(12582912.0f));
-    float2 clof = __fadd2_rn(sh, f2(-12582912.0f));
-    const bool upx = clof.x < xlo.x, upy = clof.y < xlo.y;
-    clof.x = upx ? clof.x + 1.0f : clof.x;
-    clof.y = upy ? clof.y + 1.0f : clof.y;
-    const int jla = sa.JA + __float_as_int(sh.x) - 0x4B400000 + (upx ? 1 : 0);
-    const int jlb = sa.JA + __float_as_int(sh.y) - 0x4B400000 + (upy ? 1 : 0);
-    const float2 cl2 = __fadd2_rn(clof, f2((float)LMIN));
-    const bool Lxa = xhi.x >= cl2.x, Lxb = xhi.y >= cl2.y;  // L = LMIN + 1
-    const bool ok = e < E && !sa.cull;
-    o.va = ok && ina && jla <= g.nt - 1 && jla + LMIN + (Lxa ? 0 : -1) >= 0;
-    o.vb = ok && inb && jlb <= g.nt - 1 && jlb + LMIN + (Lxb ? 0 : -1) >= 0;
-    const int jja = o.va ? jla + LMIN : 0, jjb = o.vb ? jlb + LMIN : 0;  // j_m - (MA - LMIN)
-    // Frow: this element's filter row
+    // ceil(xlo) = the round-up sum with the 1.5 2^23 shifter (exact for |xlo| < 2^22; == ceilf)
+    const float sha = __fadd_ru(xlo.x, 12582912.0f), shb = __fadd_ru(xlo.y, 12582912.0f);
+    const float2 clof = __fadd2_rn(make_float2(sha, shb), f2(-12582912.0f));
+    // record indices; the unsigned clamp only guards memory against non-finite (degenerate, R10) geometry
+    const unsigned ja = min((unsigned)(sa.JAp + (__float_as_int(sha) - 0x4B400000)), g.njp_m1);
+    const unsigned jb = min((unsigned)(sa.JAp + (__float_as_int(shb) - 0x4B400000)), g.njp_m1);
+    const float2 cl2 = __fadd2_rn(clof, f2((float)g.lmin));
+    o.La = xhi.x >= cl2.x;  // floor(xhi) - clo + 1 >= L_min + 1
+    o.Lb = xhi.y >= cl2.y;
     if constexpr (NF == 8) {  // one 256-bit load per voxel (32-B records)
-        ldg256(Frow + jja * NF, o.Fa);
-        ldg256(Frow + jjb * NF, o.Fb);
+        ldg256(Frow + (size_t)ja * NF, o.Fa);
+        ldg256(Frow + (size_t)jb * NF, o.Fb);
     } else {  // 48-B records: 128-bit loads
 #pragma unroll
         for (int r = 0; r < NF / 4; ++r) {
-            const float4 u4 = __ldg(reinterpret_cast<const float4 *>(Frow + jja * NF) + r);
-            const float4 w4 = __ldg(reinterpret_cast<const float4 *>(Frow + jjb * NF) + r);
+            const float4 u4 = __ldg(reinterpret_cast<const float4 *>(Frow + (size_t)ja * NF) + r);
+            const float4 w4 = __ldg(reinterpret_cast<const float4 *>(Frow + (size_t)jb * NF) + r);
             o.Fa[4 * r] = u4.x; o.Fa[4 * r + 1] = u4.y; o.Fa[4 * r + 2] = u4.z; o.Fa[4 * r + 3] = u4.w;
             o.Fb[4 * r] = w4.x; o.Fb[4 * r + 1] = w4.y; o.Fb[4 * r + 2] = w4.z; o.Fb[4 * r + 3] = w4.w;
         }
     }
-    o.Dm = __fadd2_rn(__ffma2_rn(clof, f2(-g.af), bse), f2(-(float)MA * g.af));
+    o.Dm = __fadd2_rn(__ffma2_rn(clof, f2(-g.af), bse), f2(-(float)g.mA * g.af));
     o.inv_r = inv_r;
-    o.dx = sa.dx;
-    o.dy = sa.dy;
+    o.dx = sa.dx + 0.5f * ex2x;  // d + delta (x, y shared by the two voxels)
+    o.dy = sa.dy + 0.5f * ey2x;
     o.dz = __fadd2_rn(f2(sa.dz), ez);
-    const int jxa = jla + LMIN, jxb = jlb + LMIN;
-    const bool xa = o.va && Lxa && jxa >= 0 && jxa < g.nt, xb = o.vb && Lxb && jxb >= 0 && jxb < g.nt;
-    o.gx = make_float2(xa ? __ldg(crow + jxa) : 0.0f, xb ? __ldg(crow + jxb) : 0.0f);  // crow: this element's row
     return o;
 }
 
-template <int M, bool POSE>
-__device__ __forceinline__ void tay2_stage_b(const Geo &g, const TayConst &tc, const Tay2A<TayCfg<M>::NF> &a,
-                                             float2 &A1, float2 &Bq)
+// A1 / 2 and Bq / (2 s^2) of the two voxels
+template <int NF, bool POSE>
+__device__ __forceinline__ void tay2_stage_b(const Geo &g, const TayConst &tc, const Tay2A<NF> &a, float2 &A1,
+                                             float2 &Bq)
 {
-    const int KT = g.lmin - g.mA;  // the optional last tap k_t = L_min - MA
+    constexpr int NPS = TayCfg<NF>::NPS;
+    const float KT = (float)(g.lmin - g.mA);  // the optional last tap k_t = L_min - MA
     const float2 Dm = a.Dm;
     const float2 dl = __ffma2_rn(f2(tc.lam_s), Dm, f2(-tc.lam0));
-    float2 qm[M];
+    // P, P', P''/2 at dl by Horner with synthetic division, in scalar FFMAs straight on the loaded
+    // registers (packing the two voxels' values would cost a register move per value)
+    float ba = a.Fa[NPS - 1], bb = a.Fb[NPS - 1], d1a = 0.0f, d1b = 0.0f, d2a = 0.0f, d2b = 0.0f;
 #pragma unroll
-    for (int m = 0; m < M; ++m) qm[m] = __fmul2_rn(dl, f2(tc.inv[m]));
-    // the series in scalar FFMAs straight on the loaded registers (packing the two voxels' filter
-    // values would cost a register move per value)
-    float2 S[3];
-#pragma unroll
-    for (int n = 0; n < (POSE ? 3 : 2); ++n) {
-        float ta = a.Fa[n + M], tb = a.Fb[n + M];
-#pragma unroll
-        for (int m = M - 1; m >= 0; --m) {
-            ta = __fmaf_rn(ta, qm[m].x, a.Fa[n + m]);
-            tb = __fmaf_rn(tb, qm[m].y, a.Fb[n + m]);
+    for (int p = NPS - 2; p >= 0; --p) {
+        if (POSE) {
+            if (p <= NPS - 4) {
+                d2a = __fmaf_rn(d2a, dl.x, d1a);
+                d2b = __fmaf_rn(d2b, dl.y, d1b);
+            } else if (p == NPS - 3) {
+                d2a = d1a;
+                d2b = d1b;
+            }
         }
-        S[n] = make_float2(ta, tb);
+        if (p <= NPS - 3) {
+            d1a = __fmaf_rn(d1a, dl.x, ba);
+            d1b = __fmaf_rn(d1b, dl.y, bb);
+        } else {
+            d1a = ba;
+            d1b = bb;
+        }
+        ba = __fmaf_rn(ba, dl.x, a.Fa[p]);
+        bb = __fmaf_rn(bb, dl.y, a.Fb[p]);
     }
-    const float2 ea = __fmul2_rn(Dm, f2(g.two_a_k2 * (float)KT));
-    const float2 w = __fmul2_rn(__fmul2_rn(a.gx, f2(tc.Ckt)), make_float2(ex2(ea.x), ex2(ea.y)));
+    float2 S[3] = {make_float2(ba, bb), make_float2(d1a, d1b), make_float2(d2a, d2b)};  // S[2] = S2 / 2
+    // the last tap (record slot NF - 1 = g C_k(k_t) / 2), in the window iff L = L_min + 1
+    const float2 ea = __fmul2_rn(Dm, f2(g.two_a_k2 * KT));
+    const float2 gx = make_float2(a.La ? a.Fa[NF - 1] : 0.0f, a.Lb ? a.Fb[NF - 1] : 0.0f);
+    const float2 w = __fmul2_rn(gx, make_float2(ex2(ea.x), ex2(ea.y)));
     S[0] = __fadd2_rn(S[0], w);
-    S[1] = __ffma2_rn(w, f2((float)KT), S[1]);
+    S[1] = __ffma2_rn(w, f2(KT), S[1]);
     const float2 q = __fmul2_rn(Dm, Dm);
-    const float2 um = make_float2(ex2(-g.k2 * q.x), ex2(-g.k2 * q.y));
+    const float2 kq = __fmul2_rn(f2(-g.k2), q);
+    const float2 um = make_float2(ex2(kq.x), ex2(kq.y));
     A1 = __fmul2_rn(um, __ffma2_rn(f2(-g.af), S[1], __fmul2_rn(Dm, S[0])));
-    if (!a.va) A1.x = 0.0f;
-    if (!a.vb) A1.y = 0.0f;
     Bq = f2(0.0f);
     if (POSE) {
-        S[2] = __ffma2_rn(w, f2((float)(KT * KT)), S[2]);
-        // (D^2 - s^2) S0 - 2 a D S1 + a^2 S2
-        const float2 b = __ffma2_rn(f2(g.af * g.af), S[2],
-                                    __ffma2_rn(__fmul2_rn(f2(-2.0f * g.af), Dm), S[1], __fmul2_rn(__fadd2_rn(q, f2(-g.s2)), S[0])));
+        S[2] = __ffma2_rn(w, f2(0.5f * KT * KT), S[2]);
+        // (D^2/s^2 - 1) S0 - (2a/s^2) D S1 + (a^2/s^2) S2, with S[2] = S2 / 2 and c_aa = 2 a^2/s^2
+        const float2 b = __ffma2_rn(f2(tc.c_aa), S[2],
+                                    __ffma2_rn(__fmul2_rn(f2(tc.c_a), Dm), S[1], __fmul2_rn(__ffma2_rn(q, f2(g.inv_s2), f2(-1.0f)), S[0])));
         Bq = __fmul2_rn(um, b);
-        if (!a.va) Bq.x = 0.0f;
-        if (!a.vb) Bq.y = 0.0f;
     }
 }
 
-template <int M, bool POSE, bool ADJ>
-__global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst tc, const float *__restrict__ poses,
+#ifndef PA_ADJ_MINB
+#define PA_ADJ_MINB 2  // resident CTAs per SM of K2c
+#endif
+template <int NF, bool POSE, bool ADJ>
+__global__ void __launch_bounds__(ADJ_THREADS, PA_ADJ_MINB) k_adjoint_tay2(Geo g, TayConst tc, const float *__restrict__ poses,
                                                                 const float *__restrict__ tmpl,
                                                                 const float *__restrict__ p0,
-                                                                const float *__restrict__ cot,
                                                                 const float *__restrict__ Fg,
                                                                 float *__restrict__ grad_p0,
-                                                                float *__restrict__ partial, int f0, int fn)
+                                                                float *__restrict__ partial, int f0, int fn, int njp,
+                                                                int padl, int sentinel)
 {
-    using T = TayCfg<M>;
-    constexpr int NF = T::NF;
     extern __shared__ float sm[];
-    const int E = g.E, F = g.F, NJ = g.nt + g.lmin;
-    AncS *anc = reinterpret_cast<AncS *>(sm);             // [2][E]: the two tiles of the CTA
-    float *wred = reinterpret_cast<float *>(anc + 2 * E);  // [8][E][3]
+    const int E = g.E, F = g.F;
+    const int E4 = (E + 3) & ~3;                           // elements padded to the unroll of 4 (sentinels)
+    AncT *anc = reinterpret_cast<AncT *>(sm);             // [2][E4]: the two tiles of the CTA
+    float *wred = reinterpret_cast<float *>(anc + 2 * E4); // [8][E][3]
     float *gacc = wred + (ADJ_THREADS / 32) * E * 3;       // [fn][E][3]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int half = tid >> 7, u = tid & 127;
@@ -1637,7 +1651,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
     const float2 ez = make_float2(((float)lzp - 0.5f * (TZ - 1)) * g.hf, ((float)(lzp + 2) - 0.5f * (TZ - 1)) * g.hf);
     // e2 exactly as pair(): fma(ex, ex, fma(ey, ey, ez * ez))
     const float2 e2 = __ffma2_rn(f2(ex), f2(ex), __ffma2_rn(f2(ey), f2(ey), __fmul2_rn(ez, ez)));
-    const AncS *anch = anc + half * E;
+    const float ex2x = 2.0f * ex, ey2x = 2.0f * ey;
+    const float2 ez2x = __fmul2_rn(f2(2.0f), ez);
+    const AncT *anch = anc + half * E4;
     const int ntzp = (g.ntz + 1) >> 1, ntp = g.ntx * g.nty * ntzp;
 
     if (POSE) {
@@ -1649,59 +1665,61 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint_tay2(Geo g, TayConst
         const int ix = TX * tx + lx, iy = TY * ty + ly, iza = TZ * tz + lzp, izb = iza + 2;
         const bool ina = ix < g.nx && iy < g.ny && iza < g.nz, inb = ix < g.nx && iy < g.ny && izb < g.nz;
         const size_t ka = ((size_t)iza * g.ny + iy) * g.nx + ix, kb = ka + 2 * (size_t)g.nx * g.ny;
+        // amplitude 0 outside the grid: those voxels add nothing to the element gradient
         const float2 P = make_float2((POSE && ina) ? __ldg(p0 + ka) : 0.0f, (POSE && inb) ? __ldg(p0 + kb) : 0.0f);
         float2 z = f2(0.0f);
         for (int fl = 0; fl < fn; ++fl) {
             const int f = f0 + fl;
             __syncthreads();  // previous frame's anchors / wred consumed
-            for (int q = tid; q < 2 * E; q += ADJ_THREADS) {
-                const int hh = q / E, e = q - hh * E;
-                double x[3];
-                elem_pos(poses, tmpl, f, e, x);
+            for (int q = tid; q < 2 * E4; q += ADJ_THREADS) {
+                const int hh = q / E4, e = q - hh * E4;
                 const int tzh = 2 * tzp + hh;
-                const Anc A = make_anchor(g, x, tx, ty, tzh < g.ntz ? tzh : 0);
-                AncS sa;
-                sa.dx2 = A.dx2; sa.dy2 = A.dy2; sa.dz2 = A.dz2;
-                sa.dx = A.dx; sa.dy = A.dy; sa.dz = A.dz;
-                sa.rho = A.rho; sa.rho2 = A.rho2; sa.CA = A.CA;
-                sa.JA = A.JA; sa.cull = A.cull || tzh >= g.ntz; sa.jseg = 0;
-                anc[q] = sa;
+                Anc A;
+                bool culled = true;
+                if (e < E) {
+                    double x[3];
+                    elem_pos(poses, tmpl, f, e, x);
+                    A = make_anchor(g, x, tx, ty, tzh < g.ntz ? tzh : 0);
+                    culled = A.cull || tzh >= g.ntz;
+                } else {
+                    A.dx = A.dy = A.dz = A.rho = A.rho2 = A.CA = 0.0f;
+                    A.rho2 = 1.0f;  // finite geometry for the padding sentinels
+                    A.rho = 1.0f;
+                    A.JA = 0;
+                }
+                anc[q] = make_anct(g, A, culled, padl, sentinel);
             }
             __syncthreads();
-            // per-element rows advanced incrementally (element e+1 of stage A; clamped to E-1)
-            const float *Frow = Fg + (size_t)fl * E * NJ * NF;
-            const float *crow = cot + (size_t)f * E * g.nt;
-            const size_t fstep = (size_t)NJ * NF;
-            Tay2A<NF> cur = tay2_stage_a<NF>(g, anch, 0, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
+            // per-element record rows advanced incrementally (stage A runs one element ahead; rows past
+            // E - 1 stay on the last row, their sentinel anchors read its zero padding)
+            const float *Frow = Fg + (size_t)fl * E * njp * NF;
+            const size_t fstep = (size_t)njp * NF;
+            Tay2A<NF> cur = tay2_stage_a<NF>(g, anch, 0, ex2x, ey2x, ez2x, e2, ez, Frow);
 #pragma unroll 1
             for (int e0 = 0; e0 < E; e0 += 4) {
                 float G[4][3];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int e = e0 + q;
-                    if (e + 1 < E) {
-                        Frow += fstep;
-                        crow += g.nt;
-                    }
-                    const Tay2A<NF> nxt = tay2_stage_a<NF>(g, anch, e + 1, E, ina, inb, ex, ey, ez, e2, Frow, crow, NJ);
+                    if (e + 1 < E) Frow += fstep;
+                    const Tay2A<NF> nxt = tay2_stage_a<NF>(g, anch, min(e + 1, E4 - 1), ex2x, ey2x, ez2x, e2, ez, Frow);
                     float2 A1, Bq;
-                    tay2_stage_b<M, POSE>(g, tc, cur, A1, Bq);
+                    tay2_stage_b<NF, POSE>(g, tc, cur, A1, Bq);
                     const float2 ir = cur.inv_r;
-                    const float2 hir = __fmul2_rn(f2(0.5f), ir);
-                    if (ADJ) z = __ffma2_rn(A1, hir, z);
+                    if (ADJ) z = __ffma2_rn(A1, ir, z);
                     if (POSE) {
-                        // dL/dr = P/(2r) (-Bq/s^2 - A1/r);  G += -dL/dr (d + delta)/r   (x - y_k = -(d + delta))
-                        const float2 dL = __fmul2_rn(__fmul2_rn(P, hir), __ffma2_rn(f2(-g.inv_s2), Bq, __fmul2_rn(__fmul2_rn(f2(-1.0f), A1), ir)));
-                        const float2 sc = __fmul2_rn(__fmul2_rn(f2(-1.0f), dL), ir);
+                        // dL/dr = P/(2r) (-Bq/s^2 - A1/r);  G += -dL/dr (d + delta)/r  (x - y_k = -(d + delta)):
+                        // with the halved moments, -dL/dr / r = P ir^2 (Bq'/s^2 + A1' ir)
+                        const float2 sc = __fmul2_rn(__fmul2_rn(P, __fmul2_rn(ir, ir)), __ffma2_rn(A1, ir, Bq));
                         const float sxy = sc.x + sc.y;  // both voxels share x and y
-                        G[q][0] = sxy * (cur.dx + ex);
-                        G[q][1] = sxy * (cur.dy + ey);
-                        G[q][2] = sc.x * cur.dz.x + sc.y * cur.dz.y;
+                        G[q][0] = sxy * cur.dx;
+                        G[q][1] = sxy * cur.dy;
+                        G[q][2] = __fmaf_rn(sc.x, cur.dz.x, sc.y * cur.dz.y);
                     }
                     cur = nxt;
                 }
                 if (POSE) {
-                    // transposed warp reduction of 4 elements x 3 components (as k_adjoint)
+                    // transposed warp reduction of 4 elements x 3 components
                     const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
                     float r6[6];
 #pragma unroll

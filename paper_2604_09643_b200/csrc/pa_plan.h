@@ -37,7 +37,9 @@ struct Plan {
     TayFilt tf;       // K2a filter taps
     TayConst tc;      // K2c series constants
     bool tay_ok;      // Taylor remainder below the bound for this geometry (K2a/K2c available)
-    int tay_M;        // its series order
+    int tay_NF;       // its record size (8 or 12 floats; TayCfg)
+    int tay_pad;      // zero positions on each side of a K2a record row
+    int tay_sentinel; // record index base of a culled (tile, element) in K2c (lands in the leading padding)
     double tay_err;   // host bound on the remainder (relative to sum |terms|)
     DepConst dc;      // deposit-form forward constants (Gaussian)
     SvdConst sv;      // the same factorisation for the adjoint K2s (unscaled)

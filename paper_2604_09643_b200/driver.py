@@ -51,7 +51,13 @@ def upsample(p: torch.Tensor, grid_to: dict) -> torch.Tensor:
 
 
 def run_pyramid(ctx, levels, tmpl: np.ndarray, meas: torch.Tensor, euler_init: np.ndarray, *, lr_trans=2e-2,
-                check_every=10, p_init=0.05, allreduce=None, outlier_k=6.0, log=None) -> DriverResult:
+                check_every=10, p_init=0.05, allreduce=None, outlier_k=6.0, log=None, pose_loss="mse",
+                p_start: torch.Tensor | None = None, pose_frames: np.ndarray | None = None) -> DriverResult:
+    """pose_loss "mse": one pa_step per iteration updates p0 and the poses from the MSE cotangent (R12);
+    "nc": the paper's split (P:85 MSE for P_c, P:92 / P:113 NC for the poses) — after the warm-up,
+    iterations alternate a p0 step (MSE, poses frozen) and a pose step (NC, masked rows out of the loss,
+    p0 frozen).  p_start: initial volume (e.g. Stage 1's reference map); pose_frames: bool [F], frames whose
+    pose is optimised (the others, e.g. tracked "Pose A" frames, stay fixed)."""
     dev = meas.device
     T = lambda a: torch.tensor(np.asarray(a, dtype=np.float32), device=dev)  # noqa: E731
     F, E = euler_init.shape[0], tmpl.shape[0]
@@ -68,7 +74,9 @@ def run_pyramid(ctx, levels, tmpl: np.ndarray, meas: torch.Tensor, euler_init: n
     for li, L in enumerate(levels):
         g = L.grid
         if p is None:
-            p = torch.full((g["nz"], g["ny"], g["nx"]), p_init, device=dev)
+            p = p_start.clone() if p_start is not None else torch.full((g["nz"], g["ny"], g["nx"]), p_init, device=dev)
+            if p.shape != (g["nz"], g["ny"], g["nx"]):
+                p = upsample(p, g)
         else:
             p = upsample(p, g)
         nv = p.numel()
@@ -77,19 +85,34 @@ def run_pyramid(ctx, levels, tmpl: np.ndarray, meas: torch.Tensor, euler_init: n
         gbuf = torch.empty(nv, device=dev)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tot_ms = 0.0
+        n_p = n_q = 0  # Adam step counters of p0 and of the poses
+        frozen = None if pose_frames is None else torch.as_tensor(~np.asarray(pose_frames, bool), device=dev)
         for it in range(L.iters):
-            cfg = dict(lr_p0=L.lr_p0, lr_trans=lr_trans, lr_rot=lr_trans / radius, step=it + 1, loss_kind=0,
-                       update_p0=1, update_pose=int(it >= L.pose_warmup))
+            pose_on = it >= L.pose_warmup
+            if pose_loss == "nc" and pose_on and (it - L.pose_warmup) % 2 == 1:
+                n_q += 1  # pose step: NC (Eq. 3/4), p0 frozen
+                cfg = dict(lr_p0=0.0, lr_trans=lr_trans, lr_rot=lr_trans / radius, step=n_q, loss_kind=1,
+                           update_p0=0, update_pose=1)
+            elif pose_loss == "nc":
+                n_p += 1  # p0 step: MSE (Eq. 2), poses frozen
+                cfg = dict(lr_p0=L.lr_p0, lr_trans=0.0, lr_rot=0.0, step=n_p, loss_kind=0, update_p0=1, update_pose=0)
+            else:
+                n_p += 1
+                cfg = dict(lr_p0=L.lr_p0, lr_trans=lr_trans, lr_rot=lr_trans / radius, step=n_p, loss_kind=0,
+                           update_p0=1, update_pose=int(pose_on))
+            e_keep = eu.clone() if (frozen is not None and cfg["update_pose"]) else None
             ev0.record()
             ctx.step(g, L.acq, tm, meas, p, eu, adam_p, adam_q, gbuf, loss, cfg, row_mask=mask, allreduce=allreduce,
                      row_loss=rl)
+            if e_keep is not None:  # tracked frames keep their poses
+                eu[frozen] = e_keep[frozen]
             ev1.record()
             torch.cuda.synchronize()
             tot_ms += ev0.elapsed_time(ev1)
-            res.history.append((li, it, float(loss[1])))
+            res.history.append((li, it, float(loss[1]), int(cfg["loss_kind"])))
             if log:
                 log(li, it, float(loss[1]))
-            if (it + 1) % check_every == 0 and it >= L.pose_warmup:
+            if (it + 1) % check_every == 0 and it >= L.pose_warmup and cfg["loss_kind"] == 0:
                 e = eu.cpu().numpy().astype(np.float64)
                 bad = rigid.trajectory_outliers(e, tmpl, k=outlier_k)
                 fl = rl.sum(1).cpu().numpy().astype(np.float64)
@@ -100,6 +123,8 @@ def run_pyramid(ctx, levels, tmpl: np.ndarray, meas: torch.Tensor, euler_init: n
                 flagged_prev = bad.copy()
                 masked_until[repeat] = it + check_every  # inconsistent twice: out of the loss for a period
                 bad &= ~repeat
+                if frozen is not None:
+                    bad &= np.asarray(pose_frames, bool)
                 if bad.any():
                     e2 = rigid.reinit_from_neighbours(e, bad)
                     eu.copy_(T(e2))

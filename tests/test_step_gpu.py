@@ -137,7 +137,7 @@ def test_allreduce_callback_inside_pa_step(ctx):
              dict(cfg, update_p0=1, step=2), allreduce=double)
     torch.cuda.synchronize()
     want, _, _ = oracle.adam(f64(p0).ravel(), np.zeros(nv), f64(v0), 2.0 * g_np, lr=1e-2, t=2, clamp=0.0)
-    assert rel(p3.double().cpu().numpy().ravel() - f64(p0).ravel(), want - f64(p0).ravel()) <= 1e-5
+    assert rel(p3.double().cpu().numpy().ravel() - f64(p0).ravel(), want - f64(p0).ravel()) <= 1e-4  # fp32 ulp(p0) / update
     not_doubled, _, _ = oracle.adam(f64(p0).ravel(), np.zeros(nv), f64(v0), g_np, lr=1e-2, t=2, clamp=0.0)
     assert rel(want - f64(p0).ravel(), not_doubled - f64(p0).ravel()) > 0.1  # the check can tell them apart
 

@@ -48,6 +48,9 @@ out = {"forward": {"kernel": "pa::k_fwd_dep (K1d), 1 launch per step", "dram_rea
        "source": f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, "
                  f"python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e (C4, 400 frames); medians per launch, the adjoint "
                  f"summed over its per-step chunks ({os.path.basename(src)})"}
+sys.path.insert(0, ROOT)
+from paper_2604_09643_b200 import build as _b  # noqa: E402
+out["libpa_hash"] = _b.source_hash()  # bench.py uses these bytes only for the same build
 out["note"] = (f"DRAM bytes per pass (ncu, default C4): forward {fr / 1e9:.1f} GB read + {fw / 1e9:.2f} GB written per "
                f"{ft / 1e3:.2f} s launch; adjoint {ar / 1e9:.1f} GB + {aw / 1e9:.1f} GB per {at / 1e3:.2f} s pass "
                f"({(fr + fw) / ft / 1e6:.1f} / {(ar + aw) / at / 1e6:.1f} GB/s, <0.5% of HBM): both passes are "

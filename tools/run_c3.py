@@ -1,6 +1,16 @@
 """BASELINE config 3 end to end: coarse-to-fine joint p0 + 6-DoF pose optimisation, 200 frames,
 128^3 (sigma 0.4) -> 256^3 (sigma 0.2) pyramid, rigid-body outlier rejection.  Prints one JSON line.
-  python tools/run_c3.py [--frames 200] [--iters 20 20]"""
+
+  python tools/run_c3.py [--frames 200] [--iters 20 20]            # r1 driver: joint MSE, glitch frames
+  python tools/run_c3.py --chain [--frames 200] [--iters 20 20]    # the paper's chain (Alg. 1):
+      Stage 1  reference map from the tracked frames (every 4th: "Pose A", known poses), coarse level, MSE;
+      Stage 2  every 8th element of every other frame ("Pose B") localised on that map (NC, Top-K, Adam
+               through decreasing sigma);
+      Stage 3  modified RANSAC (edge pre-check) + Kabsch per frame;
+      Stage 4  inlier-masked NC fine-tuning of (theta, t);
+      Stage 5  joint reconstruction over all frames, 128^3 -> 256^3 pyramid, p0 steps (MSE) alternating
+               with NC pose steps of the Pose-B frames.
+"""
 import argparse
 import json
 import math
@@ -13,12 +23,13 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_09643_b200 import Context, gen  # noqa: E402
-from paper_2604_09643_b200.driver import Level, element_errors, run_pyramid  # noqa: E402
+from paper_2604_09643_b200.driver import Level, element_errors, pose_errors, run_pyramid  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=200)
 ap.add_argument("--iters", type=int, nargs=2, default=[20, 20])
 ap.add_argument("--glitch", type=float, default=0.1)
+ap.add_argument("--chain", action="store_true")
 args = ap.parse_args()
 import __graft_entry__  # noqa: E402
 
@@ -37,21 +48,76 @@ ng = int(round(args.glitch * F))
 glitch = rng.choice(np.arange(2, F - 2), ng, replace=False)
 e0[glitch, :3] += rng.choice([-1, 1], size=(ng, 3)) * math.radians(5.0)
 e0[glitch, 3:] += rng.choice([-1, 1], size=(ng, 3)) * 3.0
-err0 = element_errors(e0, wf.euler_true, wf.tmpl)
+
+if not args.chain:
+    err0 = element_errors(e0, wf.euler_true, wf.tmpl)
+    setup_s = time.time() - t0
+    res = run_pyramid(ctx, [Level(wc.grid, wc.acq, args.iters[0], lr_p0=2e-2, pose_warmup=5),
+                            Level(wf.grid, wf.acq, args.iters[1], lr_p0=1e-2, pose_warmup=2)],
+                      wf.tmpl, meas, e0, lr_trans=2e-2, check_every=5)
+    err1 = element_errors(res.euler_t, wf.euler_true, wf.tmpl)
+    flagged = sorted(set(i for ev in res.reinit_events for i in ev[2]))
+    print(json.dumps({
+        "config": "c3: 128^3@0.4 (sigma 0.4) -> 256^3@0.2 (sigma 0.2), %d frames, 128-el linear, 2048 samples" % F,
+        "s_per_iteration": {"coarse": res.ms_per_iter[0] / 1e3, "fine": res.ms_per_iter[1] / 1e3},
+        "iters": args.iters, "setup_s": setup_s,
+        "loss_first_last": {"coarse": [res.history[0][2], [h for h in res.history if h[0] == 0][-1][2]],
+                            "fine": [[h for h in res.history if h[0] == 1][0][2], res.history[-1][2]]},
+        "elem_err_mm": {"init_mean": float(err0.mean()), "init_glitch_mean": float(err0[glitch].mean()),
+                        "final_mean": float(err1.mean()), "final_max": float(err1.max()),
+                        "final_glitch_max": float(err1[glitch].max())},
+        "glitch_frames": int(ng), "glitch_found": int(len(set(glitch.tolist()) & set(flagged))),
+        "flagged": len(flagged)}))
+    sys.exit(0)
+
+from paper_2604_09643_b200.pipeline import calibrate_frames, candidate_offsets  # noqa: E402
+
+known = np.arange(F) % 4 == 0            # Pose A: tracked frames
+B = np.nonzero(~known)[0]
+e_init = np.where(known[:, None], wf.euler_true, e0)  # tracked frames at their true poses
 setup_s = time.time() - t0
-res = run_pyramid(ctx, [Level(wc.grid, wc.acq, args.iters[0], lr_p0=2e-2, pose_warmup=5),
-                        Level(wf.grid, wf.acq, args.iters[1], lr_p0=1e-2, pose_warmup=2)],
-                  wf.tmpl, meas, e0, lr_trans=2e-2, check_every=5)
-err1 = element_errors(res.euler_t, wf.euler_true, wf.tmpl)
-flagged = sorted(set(i for ev in res.reinit_events for i in ev[2]))
-print(json.dumps({
-    "config": "c3: 128^3@0.4 (sigma 0.4) -> 256^3@0.2 (sigma 0.2), %d frames, 128-el linear, 2048 samples" % F,
-    "s_per_iteration": {"coarse": res.ms_per_iter[0] / 1e3, "fine": res.ms_per_iter[1] / 1e3},
-    "iters": args.iters, "setup_s": setup_s,
-    "loss_first_last": {"coarse": [res.history[0][2], [h for h in res.history if h[0] == 0][-1][2]],
-                        "fine": [[h for h in res.history if h[0] == 1][0][2], res.history[-1][2]]},
-    "elem_err_mm": {"init_mean": float(err0.mean()), "init_glitch_mean": float(err0[glitch].mean()),
-                    "final_mean": float(err1.mean()), "final_max": float(err1.max()),
-                    "final_glitch_max": float(err1[glitch].max())},
-    "glitch_frames": int(ng), "glitch_found": int(len(set(glitch.tolist()) & set(flagged))),
-    "flagged": len(flagged)}))
+out = {"config": "c3 chain: 128^3@0.4 -> 256^3@0.2, %d frames (%d tracked 'Pose A', %d 'Pose B'), 128-el linear, "
+                 "2048 samples" % (F, known.sum(), len(B)), "setup_s": setup_s}
+
+
+def errs(e):
+    el = element_errors(e, wf.euler_true, wf.tmpl)[B]
+    rot, tr = pose_errors(e, wf.euler_true)
+    return {"elem_mean_mm": float(el.mean()), "elem_median_mm": float(np.median(el)), "elem_max_mm": float(el.max()),
+            "trans_median_mm": float(np.median(tr[B])), "rot_median_deg": float(np.median(rot[B]))}
+
+
+out["init"] = errs(e_init)
+# ---- Stage 1: reference map from the tracked frames (coarse level, MSE, poses fixed)
+t1 = time.time()
+kidx = torch.as_tensor(np.nonzero(known)[0], device="cuda")
+r1 = run_pyramid(ctx, [Level(wc.grid, wc.acq, args.iters[0], lr_p0=2e-2, pose_warmup=10 ** 9)], wf.tmpl,
+                 meas[kidx].contiguous(), wf.euler_true[known], check_every=10 ** 9)
+torch.cuda.synchronize()
+out["stage1"] = {"s": time.time() - t1, "s_per_iteration": r1.ms_per_iter[0] / 1e3, "iters": args.iters[0]}
+p_ref = r1.p0
+# ---- Stages 2-4 on the Pose-B frames (coarse map; sigma 0.8 -> 0.4 on the 0.4 mm grid)
+acq_c2 = dict(wc.acq, sigma=0.8)
+bidx = torch.as_tensor(B, device="cuda")
+cal = calibrate_frames(ctx, wc.grid, [acq_c2, wc.acq], p_ref, meas[bidx].contiguous(), wf.tmpl, e_init[B],
+                       offsets=candidate_offsets(1.0, 0.5), topk=2, loc_iters=20, loc_lr=0.05, ransac_thr=0.6,
+                       edge_tol=0.8, ransac_iters=300, ft_iters=15, ft_lr=1e-2, elems=np.arange(0, wf.E, 8))
+e4 = e_init.copy()
+e4[B] = cal.euler_t
+e3 = e_init.copy()
+e3[B] = cal.euler_ransac
+out["stage2"] = {"s": cal.stage_s["stage2"], "sensors": int(len(B) * len(np.arange(0, wf.E, 8)))}
+out["stage3"] = {"s": cal.stage_s["stage3"], "inlier_frac": float(cal.inliers[:, ::8].mean()), "errors": errs(e3)}
+out["stage4"] = {"s": cal.stage_s["stage4"], "s_per_iteration": cal.stage4_ms_per_iter / 1e3, "errors": errs(e4)}
+# ---- Stage 5: joint reconstruction over all frames, pyramid, NC pose steps for Pose B
+t5 = time.time()
+r5 = run_pyramid(ctx, [Level(wc.grid, wc.acq, args.iters[0], lr_p0=2e-2, pose_warmup=2),
+                       Level(wf.grid, wf.acq, args.iters[1], lr_p0=1e-2, pose_warmup=2)],
+                 wf.tmpl, meas, e4, lr_trans=5e-3, check_every=10, p_start=p_ref, pose_frames=~known, pose_loss="nc")
+torch.cuda.synchronize()
+out["stage5"] = {"s": time.time() - t5, "s_per_iteration": {"coarse": r5.ms_per_iter[0] / 1e3, "fine": r5.ms_per_iter[1] / 1e3},
+                 "iters": args.iters, "errors": errs(r5.euler_t),
+                 "loss_first_last_fine_mse": [[h[2] for h in r5.history if h[0] == 1 and h[3] == 0][0],
+                                              [h[2] for h in r5.history if h[0] == 1 and h[3] == 0][-1]]}
+out["glitch_frames_in_B"] = int(np.isin(glitch, B).sum())
+print(json.dumps(out))
