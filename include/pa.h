@@ -57,7 +57,7 @@ typedef enum {
     PA_ECUDA = 4,         /* a CUDA call or launch failed                                     */
     PA_ENOMEM = 5,        /* workspace allocation failed                                      */
     PA_EUNSUPPORTED = 6   /* geometry outside every kernel (see pa_get_plan_info): the Gaussian
-                             kernel runs any L_min = floor(2 kappa sigma/(c dt)) in [12, 160]
+                             kernel runs any L_min = floor(2 kappa sigma/(c dt)) in [21, 256]
                              (nt + L_min row accumulators permitting); the exponential and
                              power-law families L_min in {26, 53, 106} (compiled direct classes) */
 } pa_status;

@@ -482,7 +482,8 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
         make_dep(pl, wmin, a, sig);
     }
     // the kernels this geometry runs (policy bits force / prefer alternatives; pa.h PA_POLICY_*)
-    const bool dep_avail = fast && pl.dep_ok && pl.dep_nw > 0;
+    // K1d: 32-bit in-plane offsets (nx ny < 2^30)
+    const bool dep_avail = fast && pl.dep_ok && pl.dep_nw > 0 && (long long)g.nx * g.ny < (1ll << 30);
     const bool svd_avail = fast && pl.dep_ok && pl.svd_derr <= 1e-5;
     const bool tay_avail = fast && pl.tay_ok;
     pl.fwd_dep = dep_avail && !(policy & PA_POLICY_FWD_DIRECT);
@@ -499,7 +500,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
                     "no kernel for this geometry: L_min=%d (2 kappa sigma/(c dt)=%.4f), kernel family %d, %s; the direct "
                     "kernels are compiled for L_min in {53, 26, 106} (cluster spread %d, tile span %d, segment %d)",
                     wmin, K2, pl.fam,
-                    !fast ? "outside the Gaussian fast path (Gaussian kernel, 12 <= L_min <= 160)"
+                    !fast ? "outside the Gaussian fast path (Gaussian kernel, 21 <= L_min <= 256)"
                           : (!pl.fwd_dep ? "the deposit forward is unavailable or not selected"
                                          : "the moment-filter adjoints are unavailable or not selected"),
                     o_need, span_need, seg_need);

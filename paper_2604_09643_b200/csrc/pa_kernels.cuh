@@ -1011,7 +1011,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
 // sides, so every pair of a non-culled (tile, element) — and every pair of a culled one, through a
 // sentinel anchor — addresses a valid position: no per-pair bounds checks (windows outside [0, nt)
 // read zeros).
-constexpr int PA_LMAX = 160;  // longest window (L_min) of the Gaussian fast path (K1d, K2a/K2c, K2s)
+constexpr int PA_LMAX = 256;  // longest window (L_min) of the Gaussian fast path (K1d, K2a/K2c, K2s)
 template <int NF_>
 struct TayCfg {
     static constexpr int NF = NF_;       // floats per record (32 / 48 B)
@@ -1315,16 +1315,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
         if (PAIR) hh_ ^= 1;
         return tx < g.ntx && ty < g.nty && tz < g.ntz;
     };
-    const size_t sy = (size_t)g.nx, sz = (size_t)g.nx * g.ny;  // 64-bit offsets: volumes of >= 2^31 voxels
-    // the lane's 2x2x2 voxel amplitudes of a tile (0 outside the grid)
+    // the lane's voxel amplitudes of a tile (0 outside the grid): one 64-bit base per tile (volumes of
+    // >= 2^31 voxels), 32-bit in-tile offsets (a z-plane of < 2^30 voxels, checked on the host), the tile's
+    // edge tests once
+    const int sy = g.nx, sz = g.nx * g.ny;
     auto load_p = [&](int tx, int ty, int tz, int hh, bool ok, float P[8]) {
         const int ix0 = TX * tx + bx, iy0 = TY * ty + by + 4 * hh, iz0 = TZ * tz + bz;
         const bool ok0 = ok && ix0 < g.nx && iy0 < g.ny && iz0 < g.nz;
-        const float *pb = p0 + (ok0 ? ((size_t)iz0 * sz + (size_t)iy0 * sy + (size_t)ix0) : (size_t)0);
+        const bool okx1 = ix0 + 1 < g.nx, okz1 = iz0 + 1 < g.nz;
+        const int ny_left = g.ny - iy0;  // rows of the lane's y run inside the grid
+        const float *pb = p0 + (ok0 ? ((size_t)iz0 * (size_t)sz + (size_t)(iy0 * sy + ix0)) : (size_t)0);
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
             const int vx = v & 1, vy = dyv(v), vz = dzv(v);
-            const bool in = ok0 && ix0 + vx < g.nx && iy0 + vy < g.ny && iz0 + vz < g.nz;
+            const bool in = ok0 && (vx == 0 || okx1) && vy < ny_left && (vz == 0 || okz1);
             P[v] = in ? __ldg(pb + (vx + vy * sy + vz * sz)) : 0.0f;
         }
     };
@@ -1380,8 +1384,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
                     const float2 cl2 = __fadd2_rn(clof, f2((float)LMIN));
                     const bool Lxx = xhi.x >= cl2.x, Lxy = xhi.y >= cl2.y;  // floor(xhi) - clo + 1 >= LMIN + 1
                     const int posx = pbase + __float_as_int(shx), posy = pbase + __float_as_int(shy);  // j_m + OFF = jlo + LMIN
-                    const bool vax = live && Pv.x != 0.0f && (unsigned)posx < (unsigned)NJ;
-                    const bool vay = live && Pv.y != 0.0f && (unsigned)posy < (unsigned)NJ;
+                    // (a zero amplitude deposits zeros: no test; a window outside the row deposits nowhere)
+                    const bool vax = live && (unsigned)posx < (unsigned)NJ;
+                    const bool vay = live && (unsigned)posy < (unsigned)NJ;
                     // t = (D_m - Dc)/Dw, D_m = bse - clo a - MA a
                     const float2 t = __ffma2_rn(clof, f2(-dc.tB), __ffma2_rn(drel, f2(dc.tA), tCA));
                     const float2 s2 = __fmul2_rn(t, t);

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2604_09643_b200 import Context, gen  # noqa: E402
+from paper_2604_09643_b200 import Context, gen, rigid  # noqa: E402
 from paper_2604_09643_b200.driver import Level, element_errors, pose_errors, run_pyramid  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -81,13 +81,26 @@ out = {"config": "c3 chain: 128^3@0.4 -> 256^3@0.2, %d frames (%d tracked 'Pose 
 
 
 def errs(e):
+    """Pose-B errors: element positions (mm; a linear array's roll about its own axis is unobservable, R15, so
+    the full rotation error is not reported), the array-axis direction (deg) and the translation (mm)."""
     el = element_errors(e, wf.euler_true, wf.tmpl)[B]
-    rot, tr = pose_errors(e, wf.euler_true)
-    return {"elem_mean_mm": float(el.mean()), "elem_median_mm": float(np.median(el)), "elem_max_mm": float(el.max()),
-            "trans_median_mm": float(np.median(tr[B])), "rot_median_deg": float(np.median(rot[B]))}
+    _, tr = pose_errors(e, wf.euler_true)
+    ax = wf.tmpl[-1] - wf.tmpl[0]
+    ax = ax / np.linalg.norm(ax)
+    ang = [math.degrees(math.acos(min(1.0, abs(float((rigid.euler_to_R(e[f, :3]) @ ax) @ (rigid.euler_to_R(wf.euler_true[f, :3]) @ ax))))))
+           for f in B]
+    return {"elem_mean_mm": float(el.mean()), "elem_median_mm": float(np.median(el)), "elem_p95_mm": float(np.percentile(el, 95)),
+            "elem_max_mm": float(el.max()), "frames_over_0.5mm": int((el > 0.5).sum()),
+            "trans_median_mm": float(np.median(tr[B])), "axis_median_deg": float(np.median(ang))}
 
 
 out["init"] = errs(e_init)
+# geometric-consistency check of the freehand sweep before localisation (R22): frames whose guessed pose leaves
+# the local trajectory fit of their neighbours (glitches) are rigidly re-initialised from them
+bad0 = rigid.trajectory_outliers(e_init, wf.tmpl) & ~known
+e_init = rigid.reinit_from_neighbours(e_init, bad0)
+out["consistency_check"] = {"flagged": int(bad0.sum()), "glitch_flagged": int(np.isin(glitch, np.nonzero(bad0)[0]).sum()),
+                            "errors": errs(e_init)}
 # ---- Stage 1: reference map from the tracked frames (coarse level, MSE, poses fixed)
 t1 = time.time()
 kidx = torch.as_tensor(np.nonzero(known)[0], device="cuda")
@@ -106,9 +119,24 @@ e4 = e_init.copy()
 e4[B] = cal.euler_t
 e3 = e_init.copy()
 e3[B] = cal.euler_ransac
+# frames whose RANSAC consensus is weak (< half of the localised elements) or whose calibrated pose leaves the
+# sweep: re-initialised from their neighbours and calibrated again
+weak = np.zeros(F, bool)
+weak[B] = cal.inliers[:, ::8].mean(1) < 0.5
+weak |= rigid.trajectory_outliers(e4, wf.tmpl) & ~known
+n_retry = int(weak.sum())
+if n_retry:
+    e_r = rigid.reinit_from_neighbours(e4, weak)
+    widx = np.nonzero(weak)[0]
+    cal2 = calibrate_frames(ctx, wc.grid, [acq_c2, wc.acq], p_ref, meas[torch.as_tensor(widx, device="cuda")].contiguous(),
+                            wf.tmpl, e_r[widx], offsets=candidate_offsets(1.5, 0.5), topk=2, loc_iters=20, loc_lr=0.05,
+                            ransac_thr=0.6, edge_tol=0.8, ransac_iters=300, ft_iters=15, ft_lr=1e-2,
+                            elems=np.arange(0, wf.E, 8))
+    e4[widx] = cal2.euler_t
 out["stage2"] = {"s": cal.stage_s["stage2"], "sensors": int(len(B) * len(np.arange(0, wf.E, 8)))}
 out["stage3"] = {"s": cal.stage_s["stage3"], "inlier_frac": float(cal.inliers[:, ::8].mean()), "errors": errs(e3)}
-out["stage4"] = {"s": cal.stage_s["stage4"], "s_per_iteration": cal.stage4_ms_per_iter / 1e3, "errors": errs(e4)}
+out["stage4"] = {"s": cal.stage_s["stage4"], "s_per_iteration": cal.stage4_ms_per_iter / 1e3, "retried_frames": n_retry,
+                 "errors": errs(e4)}
 # ---- Stage 5: joint reconstruction over all frames, pyramid, NC pose steps for Pose B
 t5 = time.time()
 r5 = run_pyramid(ctx, [Level(wc.grid, wc.acq, args.iters[0], lr_p0=2e-2, pose_warmup=2),
