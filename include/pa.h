@@ -59,7 +59,8 @@ typedef enum {
     PA_EUNSUPPORTED = 6   /* geometry outside every kernel (see pa_get_plan_info): the Gaussian
                              kernel runs any L_min = floor(2 kappa sigma/(c dt)) in [21, 256]
                              (nt + L_min row accumulators permitting); the exponential and
-                             power-law families L_min in {26, 53, 106} (compiled direct classes) */
+                             power-law families (direct kernels) L_min + cluster spread <= 128
+                             (spread = floor(sqrt(3) pitch/(c dt)) + 2) and L_min < 160      */
 } pa_status;
 
 /* Voxel grid.  Voxel (i,j,l) centre = origin + pitch*(i,j,l); p0[l][j][i]. */
@@ -249,7 +250,8 @@ typedef struct {
     int32_t dep_groups;  /* K1d: round-accumulator copies (2 when pitch < 4 c dt, else 1)         */
     int32_t dep_ring;    /* K1d: positions of the round-accumulator ring (= nt + L_min: no ring)  */
     int32_t adj_kernel;  /* the adjoint that runs: 0 direct K2, 1 moment-filter K2a+K2c, 2 K2s     */
-    int32_t direct_class;/* L_min of the direct kernels' compiled class (K1/K2), 0 if none fits    */
+    int32_t direct_class;/* direct kernels (K1/K2): L_min of the compiled class, or -capacity of the
+                            runtime class (L_min + cluster spread <= capacity), 0 if none fits     */
 } pa_plan_info;
 pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out);
 /* The same for a context (its pa_set_policy applied). */

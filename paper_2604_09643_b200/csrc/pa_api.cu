@@ -430,18 +430,28 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     const int o_need = (int)std::floor(std::sqrt(3.0) * g.h / a) + 2;
     const int span_need = (int)std::ceil(2.0 * g.rt_d / a) + 2;  // max lane window-base spread in a tile
     const int seg_need = (int)std::ceil(2.0 * g.rt_d / a) + 5 + (wmin + 1);
-    // direct kernels (K1/K2): a compiled class must match L_min and hold the geometry's spreads
+    // direct kernels (K1/K2): a compiled class that matches L_min and holds the geometry's spreads, else the
+    // smallest runtime class whose register window holds L_min + OMAX (R26)
     pl.klass = -1;
+    int k_lmin = wmin, k_omax = o_need;
     for (int k = 0; k < kNumClasses; ++k) {
         const Klass &c = kClasses[k];
         if (c.lmin == wmin && o_need <= c.omax && span_need <= c.span && seg_need <= c.seg) {
             pl.klass = k;
+            k_omax = c.omax;
             break;
         }
     }
+    if (pl.klass < 0 && wmin + 1 <= ADJ_LCAP)
+        for (int k = 0; k < kNumRtClasses; ++k)
+            if (wmin + o_need <= kRtClasses[k].rc && span_need <= kRtClasses[k].span) {
+                pl.klass = KLASS_RT + k;
+                break;
+            }
+    g.omax = k_omax;
+    g.seg = seg_need;
     if (pl.klass >= 0) {
-        const Klass &c = kClasses[pl.klass];
-        g.mF = ((c.lmin + c.omax) / 2) & ~1;  // == FwdMid<LMIN,OMAX>::m
+        g.mF = ((k_lmin + k_omax) / 2) & ~1;  // == the kernel's centre step M
         const double be = a * a / (2.0 * sig * sig);
         const double as = a / sig;  // exponential family: K_i = exp((i - m) a / s)
         for (int k = 0; k < 64; ++k) {
@@ -455,7 +465,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
             }
             pl.fc.I2[k] = make_float2((float)(-2 * k), (float)(-2 * k - 1));
         }
-        for (int i = 0; i < 128; ++i) {
+        for (int i = 0; i < ADJ_LCAP; ++i) {
             const double ka = i - g.mA;
             if (pl.fam == PA_KERNEL_EXP) {
                 pl.ac.C0[i] = (float)std::exp(ka * as);
@@ -498,7 +508,8 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     if ((!pl.fwd_dep || pl.adj == ADJ_DIRECT) && pl.klass < 0)
         return fail(PA_EUNSUPPORTED,
                     "no kernel for this geometry: L_min=%d (2 kappa sigma/(c dt)=%.4f), kernel family %d, %s; the direct "
-                    "kernels are compiled for L_min in {53, 26, 106} (cluster spread %d, tile span %d, segment %d)",
+                    "kernels need L_min + cluster spread <= 128, L_min < 160 and a tile span <= 128 (cluster spread %d, "
+                    "tile span %d, segment %d)",
                     wmin, K2, pl.fam,
                     !fast ? "outside the Gaussian fast path (Gaussian kernel, 21 <= L_min <= 256)"
                           : (!pl.fwd_dep ? "the deposit forward is unavailable or not selected"
@@ -1386,7 +1397,7 @@ static void fill_info(const Plan &pl, pa_plan_info *out)
     out->dep_groups = pl.dep_g;
     out->dep_ring = pl.dc.nr;
     out->adj_kernel = pl.adj;
-    out->direct_class = pl.klass >= 0 ? kClasses[pl.klass].lmin : 0;
+    out->direct_class = pl.klass < 0 ? 0 : (pl.klass >= KLASS_RT ? -kRtClasses[pl.klass - KLASS_RT].rc : kClasses[pl.klass].lmin);
 }
 
 pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out)

@@ -47,6 +47,7 @@ struct Geo {
     int mF, mA;                 // recurrence centres (forward cluster window / adjoint pair window)
     int lmin;                   // L_min = floor(2 kappa sigma / (c dt)): window length (L in {lmin, lmin+1})
     unsigned njp_m1;            // K2c: last record index of a zero-padded filter row
+    int omax, seg;              // direct kernels of a runtime class: cluster window-base spread, segment length
     float ls, nu;               // exponential: log2(e)/s; power law: nu   (kernel families, R23)
 };
 
@@ -63,10 +64,11 @@ struct FwdConst {
     float2 I2[64];   // (-2k, -2k-1): step indices for packed D_i = D_J - i a
     float2 X2[64];   // exp: (1/K_2k, 1/K_2k+1)
 };
+constexpr int ADJ_LCAP = 160;  // longest window (L_min + 1) of the direct adjoint K2
 struct AdjConst {
-    float C0[128];  // Gaussian: C_i about the pair-window centre mA;  exp: K_i
-    float C1[128];  // Gaussian: C_i (i - mA);                           exp: 1/K_i
-    float C2[128];  // Gaussian: C_i (i - mA)^2
+    float C0[ADJ_LCAP];  // Gaussian: C_i about the pair-window centre mA;  exp: K_i
+    float C1[ADJ_LCAP];  // Gaussian: C_i (i - mA);                           exp: 1/K_i
+    float C2[ADJ_LCAP];  // Gaussian: C_i (i - mA)^2
 };
 
 struct Anc {
@@ -150,9 +152,9 @@ struct Pair {
     int L;        // window length, clamped to [LMIN, LMIN+1]
 };
 
-// The single definition of a (voxel, element) pair's window used by every kernel (R17).
-template <int LMIN>
-__device__ __forceinline__ Pair pair(const Geo &g, const Anc &A, float ex, float ey, float ez, float e2)
+// The single definition of a (voxel, element) pair's window used by every kernel (R17); LMIN is the
+// window length L_min (a compile-time constant in the compiled classes, folded by the compiler).
+__device__ __forceinline__ Pair pair(const Geo &g, const Anc &A, float ex, float ey, float ez, float e2, int LMIN)
 {
     float num = __fmaf_rn(A.dx2, ex, __fmaf_rn(A.dy2, ey, __fmaf_rn(A.dz2, ez, e2)));
     float r2 = __fadd_rn(A.rho2, num);
@@ -218,26 +220,22 @@ __device__ __forceinline__ int warp_max(int v)
 // and the 4 warp traces are summed in fixed order at the end.  Epilogue optionally fuses
 // the MSE / NC cotangent (a3) so the trace is never written.
 // ============================================================================================
-template <int LMIN, int OMAX, int SPAN>
+// LMIN = 0: a runtime class — L_min, OMAX and the centre step come from Geo (lmin, omax, mF) and RC is
+// the register-window capacity (>= L_min + OMAX); the loops below are written over the whole capacity
+// with bounds tests that fold away for the compiled classes.
+template <int LMIN, int OMAX, int SPAN, int RC = LMIN + OMAX>
 struct FwdCfg {
-    static constexpr int R = LMIN + OMAX;
+    static constexpr int R = RC;
     static constexpr int NCOL = R + SPAN;   // columns of the flush buffer (window + tile spread)
     static constexpr int NPH = PA_FWD_PHASES;         // flush phases (rows per phase = 32 / NPH)
     static constexpr int ROWS = 32 / NPH;
     static constexpr int CSTR = ROWS + 4;              // column stride (floats): rows + skew, 16-B aligned
-    static constexpr int PADL = LMIN + 2;
+    static constexpr int PADL = (LMIN > 0 ? LMIN : RC) + 2;
     static __host__ __device__ int trace_len(int nt) { return PADL + nt + NCOL + 1; }
     static __host__ __device__ int warp_floats(int nt) { return ((trace_len(nt) + 3) & ~3) + NCOL * CSTR; }
 };
 
 enum { FWD_TRACE = 0, FWD_MSE = 1, FWD_NC = 2 };
-
-// Centre step of the forward register window, m = round(L_min/2 + (OMAX-1)/2) — the host sets
-// Geo::mF to the same value (checked in make_plan).
-template <int LMIN, int OMAX>
-struct FwdMid {
-    static constexpr int m = ((LMIN + OMAX) / 2) & ~1;  // even: packed (i, i+1) pairs stay register-pair aligned
-};
 
 // K(D) evaluated directly (slow paths)
 template <int FAM>
@@ -274,7 +272,7 @@ __device__ __forceinline__ float fam_val1(const Geo &g, const FwdConst &fc, int 
     }
 }
 
-template <int LMIN, int OMAX, int SPAN, int FAM>
+template <int LMIN_, int OMAX_, int SPAN, int FAM, int RC = LMIN_ + OMAX_>
 __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <= 64) ? 3 : 2) k_forward(Geo g, FwdConst fc, const float *__restrict__ poses,
                                                             const float *__restrict__ tmpl,
                                                             const float *__restrict__ p0, float *__restrict__ out,
@@ -282,8 +280,15 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
                                                             const uint8_t *__restrict__ row_mask,
                                                             double *__restrict__ rowloss)
 {
-    using C = FwdCfg<LMIN, OMAX, SPAN>;
+    using C = FwdCfg<LMIN_, OMAX_, SPAN, RC>;
     constexpr int R = C::R;
+    // window length, cluster spread and recurrence centre: compile-time in the compiled classes, from the
+    // plan in a runtime class (LMIN_ = 0)
+    const int LMIN = LMIN_ > 0 ? LMIN_ : g.lmin;
+    const int OMAX = OMAX_ > 0 ? OMAX_ : g.omax;
+    const int M = LMIN_ > 0 ? (((LMIN_ + OMAX_) / 2) & ~1) : g.mF;  // centre step (even), host Geo::mF
+    const int UPE = M + 2 * ((LMIN - M) / 2);  // upward packed pairs: [M, UPE)
+    const int DNE = 2 * (OMAX / 2);            // downward packed pairs: [DNE, M)
     extern __shared__ float sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int TL = (C::trace_len(g.nt) + 3) & ~3;
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
             const float eyq = ((float)(2 * cy + qy) - 0.5f * (TY - 1)) * g.hf;
             const float ezq = ((float)(2 * cz + qz) - 0.5f * (TZ - 1)) * g.hf;
             const float e2q = __fmaf_rn(exq, exq, __fmaf_rn(eyq, eyq, __fmul_rn(ezq, ezq)));
-            J = pair<LMIN>(g, A, exq, eyq, ezq, e2q).jlo;
+            J = pair(g, A, exq, eyq, ezq, e2q, LMIN).jlo;
         }
         J = max(J, -(LMIN + 1));  // windows ending before 0 contribute nothing
         const bool any = J <= g.nt - 1;
@@ -363,10 +368,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
         const float2 af2 = make_float2(g.af, g.af);
         // steps [OMAX-1, LMIN) are in-window for every voxel of the cluster: there the recurrence
         // runs packed on (i, i+1) pairs (FFMA2/FMUL2); the OMAX-1 head and the tail steps are
-        // scalar and predicated.
-        constexpr int M = FwdMid<LMIN, OMAX>::m;
-        constexpr int UPE = M + 2 * ((LMIN - M) / 2);   // upward packed pairs: [M, UPE)
-        constexpr int DNE = 2 * ((OMAX - 1 + 1) / 2);   // downward packed pairs: [DNE, M)
+        // scalar and predicated.  Every loop runs over the register window with static indices; its
+        // bounds tests fold away in a compiled class and are warp-uniform branches in a runtime class.
         // NV voxels per pass (independent recurrence chains, ILP NV); the recurrence runs
         // centre-out from step M
         constexpr int NV = PA_FWD_NV;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
                 const float ex = ex0 + (float)vx * g.hf;
                 const float ey = ((float)(2 * cy + vy) - 0.5f * (TY - 1)) * g.hf;
                 const float ez = ((float)(2 * cz + vz) - 0.5f * (TZ - 1)) * g.hf;
-                const Pair pv = pair<LMIN>(g, A, ex, ey, ez, __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez))));
+                const Pair pv = pair(g, A, ex, ey, ez, __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez))), LMIN);
                 const bool in = bx + vx < g.nx && by + vy < g.ny && bz + vz < g.nz;
                 float c = (in && pv.jlo <= g.nt - 1 && pv.jlo + pv.L - 1 >= 0) ? P[v] * 0.5f * pv.inv_r : 0.0f;
                 int o = pv.jlo - J;
@@ -418,7 +421,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
             if constexpr (FAM == KF_GAUSS) {
                 // -- upward, packed
 #pragma unroll
-                for (int i = M; i < UPE; i += 2) {
+                for (int i = 0; i < R - 1; i += 2) {
+                    if (i < M) continue;
+                    if (i >= UPE) break;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) {
                         const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
@@ -439,7 +444,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
 #pragma unroll
                 for (int q = 0; q < NV; ++q) us[q] = u2[q].x;
 #pragma unroll
-                for (int i = UPE; i < R; ++i) {
+                for (int i = 0; i < R; ++i) {
+                    if (i < UPE) continue;
                     if (i >= tail_end) break;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) {
@@ -452,7 +458,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
 #pragma unroll
                 for (int q = 0; q < NV; ++q) u2[q] = make_float2(um[q] * q2[q].x, um[q] * qq[q]);
 #pragma unroll
-                for (int i = M - 2; i >= DNE; i -= 2) {
+                for (int i = R - 2 - (R & 1); i >= 0; i -= 2) {
+                    if (i > M - 2) continue;
+                    if (i < DNE) break;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) {
                         const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
@@ -466,7 +474,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
 #pragma unroll
                 for (int q = 0; q < NV; ++q) us[q] = u2[q].y;
 #pragma unroll
-                for (int i = DNE - 1; i >= 0; --i) {
+                for (int i = R - 1; i >= 0; --i) {
+                    if (i >= DNE) continue;
                     if (i < head_beg) break;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) {
@@ -479,7 +488,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
                 // exponential / power law: no recurrence state; packed where every voxel of the
                 // pass is in-window, scalar and predicated at the edges (warp-uniform exits)
 #pragma unroll
-                for (int i = DNE; i + 1 < UPE; i += 2) {
+                for (int i = 0; i < R - 1; i += 2) {
+                    if (i < DNE) continue;
+                    if (i + 1 >= UPE) break;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) {
                         const float2 D = __ffma2_rn(fc.I2[i >> 1], af2, DJ2[q]);
@@ -495,7 +506,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
                 const int tail_end = (int)__reduce_max_sync(0xffffffffu, (unsigned)mx);
                 const int head_beg = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
 #pragma unroll
-                for (int i = UPE; i < R; ++i) {
+                for (int i = 0; i < R; ++i) {
+                    if (i < UPE) continue;
                     if (i >= tail_end) break;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) {
@@ -505,7 +517,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
                     }
                 }
 #pragma unroll
-                for (int i = DNE - 1; i >= 0; --i) {
+                for (int i = R - 1; i >= 0; --i) {
+                    if (i >= DNE) continue;
                     if (i < head_beg) break;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) {
@@ -577,7 +590,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, (PA_FWD_PHASES == 2 && SPAN <=
                         const float ex = ((float)(2 * cx + vx) - 0.5f * (TX - 1)) * g.hf;
                         const float ey = ((float)(2 * cy + vy) - 0.5f * (TY - 1)) * g.hf;
                         const float ez = ((float)(2 * cz + vz) - 0.5f * (TZ - 1)) * g.hf;
-                        const Pair pv = pair<LMIN>(g, A, ex, ey, ez, __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez))));
+                        const Pair pv = pair(g, A, ex, ey, ez, __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez))), LMIN);
                         const float cv = P[v] * 0.5f * pv.inv_r;
                         for (int i = 0; i < pv.L; ++i) {
                             const int j = pv.jlo + i;
@@ -676,25 +689,23 @@ struct AdjCfg {
     }
 };
 
-// Centre step of the adjoint pair window (host Geo::mA must equal it, set in make_plan).
-template <int LMIN>
-struct AdjMid {
-    static constexpr int m = (LMIN + 1) / 2;
-};
-
 struct AncS {  // anchor as stored in shared memory (12 words)
     float dx2, dy2, dz2, dx, dy, dz, rho, rho2, CA;
     int JA, cull, jseg;
 };
 
-template <int LMIN, int SEG, bool POSE, bool ADJ, int FAM>
+// LMIN_ = 0: a runtime class (L_min = Geo::lmin, the segment length Geo::seg).
+template <int LMIN_, int SEG_, bool POSE, bool ADJ, int FAM>
 __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, const float *__restrict__ poses,
                                                            const float *__restrict__ tmpl,
                                                            const float *__restrict__ p0,
                                                            const float *__restrict__ cot, float *__restrict__ grad_p0,
                                                            float *__restrict__ partial, int Fc)
 {
-    constexpr int LMAX = LMIN + 1;
+    const int LMIN = LMIN_ > 0 ? LMIN_ : g.lmin;
+    const int SEG = SEG_ > 0 ? SEG_ : g.seg;
+    const int LMAX = LMIN + 1;
+    constexpr int UNR = LMIN_ > 0 ? 128 : 4;  // full unroll in a compiled class
     extern __shared__ float sm[];
     const int E = g.E, F = g.F;
     float *seg = sm;
@@ -768,15 +779,15 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                         Aa.rho = sa.rho; Aa.rho2 = sa.rho2; Aa.CA = sa.CA; Aa.JA = sa.JA; Aa.cull = 0;
                         Ab.dx2 = sb.dx2; Ab.dy2 = sb.dy2; Ab.dz2 = sb.dz2; Ab.dx = sb.dx; Ab.dy = sb.dy; Ab.dz = sb.dz;
                         Ab.rho = sb.rho; Ab.rho2 = sb.rho2; Ab.CA = sb.CA; Ab.JA = sb.JA; Ab.cull = 0;
-                        const Pair pa = pair<LMIN>(g, Aa, ex, ey, ez, e2);
-                        const Pair pb = pair<LMIN>(g, Ab, ex, ey, ez, e2);
+                        const Pair pa = pair(g, Aa, ex, ey, ez, e2, LMIN);
+                        const Pair pb = pair(g, Ab, ex, ey, ez, e2, LMIN);
                         const bool va = inside && !sa.cull && pa.jlo <= g.nt - 1 && pa.jlo + pa.L - 1 >= 0;
                         const bool vb = inside && hb && !sb.cull && pb.jlo <= g.nt - 1 && pb.jlo + pb.L - 1 >= 0;
                         const int offa = va ? min(max(pa.jlo - sa.jseg, 0), SEG - LMAX) : 0;
                         const int offb = vb ? min(max(pb.jlo - sb.jseg, 0), SEG - LMAX) : 0;
                         const float *gsa = seg + ea * SEG + offa;
                         const float *gsb = seg + (hb ? eb : ea) * SEG + offb;
-                        constexpr int MA = AdjMid<LMIN>::m;
+                        const int MA = (LMIN + 1) / 2;  // == Geo::mA
                         const float Dma = __fmaf_rn(-(float)(pa.jlo - sa.JA), g.af, __fadd_rn(pa.drel, sa.CA)) - (float)MA * g.af;
                         const float Dmb = __fmaf_rn(-(float)(pb.jlo - sb.JA), g.af, __fadd_rn(pb.drel, sb.CA)) - (float)MA * g.af;
                         // A1 = sum g D K (adjoint);  A2 = sum g (K + D K') (pose, d/dr of D K)
@@ -794,7 +805,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                             //   sum c_k x^k = b, sum k c_k x^k = x d1, sum k^2 c_k x^k = x d1 + 2 x^2 d2.
                             const float2 z2 = make_float2(0.f, 0.f);
                             float2 bu = z2, d1u = z2, d2u = z2, bd = z2, d1d = z2, d2d = z2;
-#pragma unroll
+#pragma unroll UNR
                             for (int i = LMAX - 1; i >= MA; --i) {
                                 float2 c = __fmul2_rn(make_float2(gsa[i], gsb[i]), make_float2(ac.C0[i], ac.C0[i]));
                                 if (i >= LMIN) {
@@ -805,7 +816,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                                 d1u = __ffma2_rn(d1u, pu, bu);
                                 bu = __ffma2_rn(bu, pu, c);
                             }
-#pragma unroll
+#pragma unroll UNR
                             for (int i = 0; i <= MA; ++i) {  // k = MA - i; the k = 0 step (i = MA) adds 0
                                 const float2 c = i < MA ? __fmul2_rn(make_float2(gsa[i], gsb[i]),
                                                                      make_float2(ac.C0[i], ac.C0[i]))
@@ -827,7 +838,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
 #else
                             float2 S0 = make_float2(0.f, 0.f), S1 = S0, S2 = S0;  // sum g E k^n, k = i - MA
                             float2 u = um;
-#pragma unroll
+#pragma unroll UNR
                             for (int i = MA; i < LMAX; ++i) {
                                 float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), u);
                                 if (i >= LMIN) {
@@ -840,7 +851,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                                 u = __fmul2_rn(u, pu);
                             }
                             u = __fmul2_rn(um, pd);
-#pragma unroll
+#pragma unroll UNR
                             for (int i = MA - 1; i >= 0; --i) {
                                 const float2 t = __fmul2_rn(make_float2(gsa[i], gsb[i]), u);
                                 S0 = __ffma2_rn(t, make_float2(ac.C0[i], ac.C0[i]), S0);
@@ -871,7 +882,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
                                 Be = make_float2(ex2(la), ex2(lb));
                             }
                             float2 SE = make_float2(0.f, 0.f), SD = SE, SX = SE;
-#pragma unroll
+#pragma unroll UNR
                             for (int i = 0; i < LMAX; ++i) {
                                 const float2 D = __ffma2_rn(make_float2((float)(MA - i), (float)(MA - i)), af2, Dm2);
                                 float2 Kv;

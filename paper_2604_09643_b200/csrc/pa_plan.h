@@ -28,6 +28,16 @@ struct Klass {
 };
 constexpr Klass kClasses[] = {{53, 11, 58, 128}, {26, 6, 30, 64}, {106, 21, 114, 256}};
 constexpr int kNumClasses = (int)(sizeof kClasses / sizeof kClasses[0]);
+// Runtime classes of the direct kernels (r2, R26): L_min, the cluster spread OMAX and the recurrence centre
+// come from the plan; K1 holds a register window of capacity rc >= L_min + OMAX and a flush buffer for a
+// tile span <= span; K2 stages segments of the plan's length (L_min + 1 <= ADJ_LCAP).  Plan::klass =
+// KLASS_RT + index.
+struct RtKlass {
+    int rc, span;
+};
+constexpr RtKlass kRtClasses[] = {{48, 80}, {80, 96}, {128, 128}};
+constexpr int kNumRtClasses = (int)(sizeof kRtClasses / sizeof kRtClasses[0]);
+constexpr int KLASS_RT = 100;
 
 // kernel-selection policy of a context (pa_set_policy; PA_POLICY_* in pa.h)
 struct Plan {

@@ -144,3 +144,29 @@ def test_family_argument_errors(ctx):
         with pytest.raises(PAError) as ei:
             ctx.forward(grid, acq, T(tmpl), T(poses), p0)
         assert ei.value.status == PA_EINVAL, bad
+
+
+# runtime classes of the direct kernels (r2, R26): window lengths outside {26, 53, 106}, and the Gaussian
+# forced onto the direct kernels at a general acquisition
+RT_CASES = [("exp", 0.0, 0.075, 10.0, 0.2, 40), ("pow", 1.5, 0.0375, 20.0, 0.2, 40), ("exp", 0.0, 0.125, 10.0, 0.2, 66),
+            ("pow", 0.8, 0.15, 10.0, 0.2, 80), ("exp", 0.0, 0.07, 10.0, 0.1, 37), ("gauss", 0.0, 0.25, 5.0, 0.2, 66)]
+
+
+@pytest.mark.parametrize("kernel,nu,s,kappa,pitch,lmin", RT_CASES)
+def test_runtime_direct_classes(ctx, record_parity, kernel, nu, s, kappa, pitch, lmin):
+    """Ragged multi-tile grid, several frames, windows clipped at both ends, on a runtime class of K1/K2."""
+    from paper_2604_09643_b200 import plan_info
+
+    grid = gen.make_grid((21, 17, 13), pitch)
+    acq = dict(gen.make_acq(700, 0.2, t0=1.0), sigma=s, kappa=kappa, kernel=kernel, nu=nu)
+    tmpl, poses = random_scene(41, grid, E=4, F=2, standoff=2.0)
+    p0 = gen.random_volume(grid, 42)
+    cot = gen.random_cotangent((2, 4, 700), seed=43)
+    if kernel == "gauss":
+        ctx.set_policy(["fwd_direct", "adj_direct"])
+    try:
+        info = ctx.plan_info(grid32(grid), acq32(acq), 4)
+        assert info["lmin"] == lmin and info["direct_class"] < 0 and info["fwd_deposit"] == 0 and info["adj_kernel"] == 0, info
+        check(record_parity, f"rt-{kernel}{nu}-L{lmin}", run_all(ctx, grid, acq, tmpl, poses, p0, cot))
+    finally:
+        ctx.set_policy("default")
