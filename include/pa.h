@@ -57,10 +57,11 @@ typedef enum {
     PA_ECUDA = 4,         /* a CUDA call or launch failed                                     */
     PA_ENOMEM = 5,        /* workspace allocation failed                                      */
     PA_EUNSUPPORTED = 6   /* geometry outside every kernel (see pa_get_plan_info): the Gaussian
-                             kernel runs any L_min = floor(2 kappa sigma/(c dt)) in [21, 256]
-                             (nt + L_min row accumulators permitting); the exponential and
-                             power-law families (direct kernels) L_min + cluster spread <= 128
-                             (spread = floor(sqrt(3) pitch/(c dt)) + 2) and L_min < 160      */
+                             fast path runs any L_min = floor(2 kappa sigma/(c dt)) in [21, 256]
+                             (nt + L_min row accumulators permitting); the direct kernels (the
+                             exponential and power-law families; shorter Gaussian windows) run
+                             spread <= L_min < 160 with L_min + spread <= 128, spread =
+                             floor(sqrt(3) pitch/(c dt)) + 2                                  */
 } pa_status;
 
 /* Voxel grid.  Voxel (i,j,l) centre = origin + pitch*(i,j,l); p0[l][j][i]. */

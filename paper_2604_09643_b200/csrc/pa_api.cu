@@ -442,7 +442,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
             break;
         }
     }
-    if (pl.klass < 0 && wmin + 1 <= ADJ_LCAP)
+    if (pl.klass < 0 && wmin + 1 <= ADJ_LCAP && wmin >= o_need)  // the recurrence centre lies inside the window
         for (int k = 0; k < kNumRtClasses; ++k)
             if (wmin + o_need <= kRtClasses[k].rc && span_need <= kRtClasses[k].span) {
                 pl.klass = KLASS_RT + k;
@@ -508,7 +508,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     if ((!pl.fwd_dep || pl.adj == ADJ_DIRECT) && pl.klass < 0)
         return fail(PA_EUNSUPPORTED,
                     "no kernel for this geometry: L_min=%d (2 kappa sigma/(c dt)=%.4f), kernel family %d, %s; the direct "
-                    "kernels need L_min + cluster spread <= 128, L_min < 160 and a tile span <= 128 (cluster spread %d, "
+                    "kernels need spread <= L_min, L_min + cluster spread <= 128, L_min < 160 and a tile span <= 128 (cluster spread %d, "
                     "tile span %d, segment %d)",
                     wmin, K2, pl.fam,
                     !fast ? "outside the Gaussian fast path (Gaussian kernel, 21 <= L_min <= 256)"

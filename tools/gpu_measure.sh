@@ -13,12 +13,12 @@ if [ "$MODE" = tests ]; then
   PARITY_OUT=$O/${TAG}_parity.json timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/${TAG}_gpu_tests.txt 2>&1
   echo "pytest rc=$?"; tail -3 $O/${TAG}_gpu_tests.txt
 fi
-timeout 900 python bench.py --steps 3 --warmup 3 > $O/${TAG}_bench_c4.json 2> $O/${TAG}_bench_c4.err
-echo "bench rc=$?"; tail -c 300 $O/${TAG}_bench_c4.json
 timeout 900 python tools/issue_capture.py run $TAG > $O/${TAG}_issue.log 2>&1 && \
   timeout 300 python tools/issue_capture.py parse $O/${TAG}_issue_c4.csv $TAG >> $O/${TAG}_issue.log 2>&1
 echo "issue rc=$?"; tail -2 $O/${TAG}_issue.log
 cp profiles/${TAG}_issue_c4.json $O/ 2>/dev/null
+timeout 900 python bench.py --steps 3 --warmup 3 > $O/${TAG}_bench_c4.json 2> $O/${TAG}_bench_c4.err
+echo "bench rc=$?"; tail -c 300 $O/${TAG}_bench_c4.json
 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $O/${TAG}_launches_c4.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > $O/${TAG}_launch_bench.json 2>&1
 echo "launches rc=$?"
