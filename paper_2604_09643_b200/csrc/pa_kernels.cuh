@@ -2115,15 +2115,18 @@ __device__ __forceinline__ void tgv_fields(const TgvArgs &t, const float *__rest
 #pragma unroll
         for (int b = 0; b < 3; ++b) D[a][b] = (__ldg(w + b * nv + k + off[a]) - wv[b]) * t.inv_h;
     }
-    ng = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + t.eps * t.eps);
-    const float ig = 1.0f / ng;
+    // |v|_eps and 1/|v|_eps from one MUFU.RSQ (no IEEE sqrt / division sequences)
+    const float sg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + t.eps * t.eps;
+    const float ig = rsqrtf(sg);
+    ng = sg * ig;
     n[0] = g[0] * ig;
     n[1] = g[1] * ig;
     n[2] = g[2] * ig;
     const float exx = D[0][0], eyy = D[1][1], ezz = D[2][2];
     const float exy = 0.5f * (D[0][1] + D[1][0]), exz = 0.5f * (D[0][2] + D[2][0]), eyz = 0.5f * (D[1][2] + D[2][1]);
-    ne = sqrtf(exx * exx + eyy * eyy + ezz * ezz + 2.0f * (exy * exy + exz * exz + eyz * eyz) + t.eps * t.eps);
-    const float ie = 1.0f / ne;
+    const float se = exx * exx + eyy * eyy + ezz * ezz + 2.0f * (exy * exy + exz * exz + eyz * eyz) + t.eps * t.eps;
+    const float ie = rsqrtf(se);
+    ne = se * ie;
     m[0] = exx * ie;
     m[1] = eyy * ie;
     m[2] = ezz * ie;
@@ -2139,35 +2142,75 @@ __device__ __forceinline__ float msym(const float m[6], int a, int b)
     return s == 1 ? m[3] : (s == 2 ? m[4] : m[5]);
 }
 
-// 2.5-D streaming version: a CTA owns a 32 x 8 column of (x, y) and walks z through a slab;
-// the dphi fields (n: 3, m: 6) of each point are computed ONCE into a shared-memory plane
-// (with the x-1 / y-1 halo), the previous plane is kept, and the gradient of plane z is a
-// gather from planes z and z-1.  One thread per point of the 33 x 9 halo plane (297 of 320
-// threads; the last 23 only join barriers and the sum), so a plane fills in one pass; the
-// 32 x 8 threads with i, j >= 1 also own an output voxel.  (Loading a plane's inputs one plane
-// ahead, into registers, measured slower: 72 registers cost a resident CTA, 0.30 vs 0.28 ms at 256^3.)
+// 2.5-D streaming version: a CTA owns a 32 x 8 column of (x, y) and walks z through a slab.  Thread q
+// owns the raw point (x0 - 1 + q % 34, y0 - 1 + q / 34) of a 34 x 10 region and streams its z column in
+// registers: the values (P, w_x, w_y, w_z) of plane z + 1 are loaded one iteration ahead and those of
+// plane z + 2 issued before the current plane's work, so every value is read from global memory once per
+// CTA and its latency hides behind a plane of compute.  Per plane: the raw values of plane z go to a
+// shared plane (for the x + 1 / y + 1 neighbours of the fields), the 33 x 9 halo points compute the dphi
+// fields (n: 3, m: 6) from that plane and their own plane-(z + 1) registers, and the gradient of plane z is
+// a gather from field planes z and z - 1 (previous plane kept).
 constexpr int TGV_BX = 32, TGV_BY = 8, TGV_ZS = 32;
-constexpr int TGV_NT = ((TGV_BX + 1) * (TGV_BY + 1) + 31) / 32 * 32;
+constexpr int TGV_RX = TGV_BX + 2, TGV_RY = TGV_BY + 2;               // raw region 34 x 10
+constexpr int TGV_NT = (TGV_RX * TGV_RY + 31) / 32 * 32;              // 352 threads
 
 __global__ void __launch_bounds__(TGV_NT) k_tgv(TgvArgs t, const float *__restrict__ P,
                                                 const float *__restrict__ w, float *__restrict__ gP,
                                                 float *__restrict__ gw, double *__restrict__ part)
 {
     constexpr int PX = TGV_BX + 1, PY = TGV_BY + 1, NF = 9, NWT = TGV_NT / 32;
-    __shared__ float fld[2][NF][PY][PX];  // plane buffers: n0..2, m0..5 at (x - 1 .. x + 31, y - 1 .. y + 7)
-    const int i = threadIdx.x % PX, j = threadIdx.x / PX;  // this thread's halo-plane point
+    __shared__ float fld[2][NF][PY][PX];     // field planes: n0..2, m0..5 at (x - 1 .. x + 31, y - 1 .. y + 7)
+    __shared__ float raw[4][TGV_RY][TGV_RX];  // raw plane z: P, w_x, w_y, w_z at (x - 1 .. x + 32, y - 1 .. y + 8)
+    const int i = threadIdx.x % TGV_RX, j = threadIdx.x / TGV_RX;  // this thread's raw point
     const int x0 = blockIdx.x * TGV_BX, y0 = blockIdx.y * TGV_BY, z0 = blockIdx.z * TGV_ZS;
     const int x = x0 - 1 + i, y = y0 - 1 + j;
-    const bool pt = threadIdx.x < PX * PY;
-    const bool own = pt && i >= 1 && j >= 1;  // owns output voxel (x, y) and the value term of (x, y)
-    const int sz = t.nx * t.ny, nv = sz * t.nz;  // 3 nv < 2^31 (launch_tgv)
+    const bool rp = threadIdx.x < TGV_RX * TGV_RY;           // a raw point
+    const bool pt = rp && i < PX && j < PY;                  // a halo point (computes fields)
+    const bool own = pt && i >= 1 && j >= 1;                 // owns output voxel (x, y) and its value term
+    const int sz = t.nx * t.ny, nv = sz * t.nz;              // 3 nv < 2^31 (launch_tgv)
+    const bool inxy = rp && x >= 0 && y >= 0 && x < t.nx && y < t.ny;
+    const int kxy = inxy ? y * t.nx + x : 0;
     double val = 0.0;
+    auto ld = [&](int z, float v[4]) {  // this column's raw values at plane z (0 outside the volume)
+        const bool ok = inxy && z >= 0 && z < t.nz;
+        const int k = z * sz + kxy;
+        v[0] = ok ? __ldg(P + k) : 0.0f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[1 + c] = ok ? __ldg(w + c * nv + k) : 0.0f;
+    };
+    float cz[4] = {}, c1[4] = {}, c2[4] = {};  // the column at planes z, z + 1, z + 2
+    // fields at this halo point of plane z from raw plane z (shared) and the column's plane z + 1
     auto fill = [&](int buf, int z, bool count) {
         if (!pt) return;
         float n[3] = {0.f, 0.f, 0.f}, m[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (tgv_in(t, x, y, z)) {
-            float ng, ne;
-            tgv_fields(t, P, w, x, y, z, n, m, ng, ne);
+            const float p = cz[0];
+            const float pn[3] = {raw[0][j][i + 1], raw[0][j + 1][i], c1[0]};
+            float D[3][3], g[3];
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                D[0][b] = (raw[1 + b][j][i + 1] - cz[1 + b]) * t.inv_h;
+                D[1][b] = (raw[1 + b][j + 1][i] - cz[1 + b]) * t.inv_h;
+                D[2][b] = (c1[1 + b] - cz[1 + b]) * t.inv_h;
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) g[a] = (pn[a] - p) * t.inv_h - cz[1 + a];
+            // |v|_eps and 1/|v|_eps from one MUFU.RSQ
+            const float sg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + t.eps * t.eps;
+            const float ig = rsqrtf(sg), ng = sg * ig;
+            n[0] = g[0] * ig;
+            n[1] = g[1] * ig;
+            n[2] = g[2] * ig;
+            const float exx = D[0][0], eyy = D[1][1], ezz = D[2][2];
+            const float exy = 0.5f * (D[0][1] + D[1][0]), exz = 0.5f * (D[0][2] + D[2][0]), eyz = 0.5f * (D[1][2] + D[2][1]);
+            const float se = exx * exx + eyy * eyy + ezz * ezz + 2.0f * (exy * exy + exz * exz + eyz * eyz) + t.eps * t.eps;
+            const float ie = rsqrtf(se), ne = se * ie;
+            m[0] = exx * ie;
+            m[1] = eyy * ie;
+            m[2] = ezz * ie;
+            m[3] = exy * ie;
+            m[4] = exz * ie;
+            m[5] = eyz * ie;
             // the value is counted once, by the owner of the interior point (i, j >= 1) in its own slab
             if (own && count) val += (double)t.a1 * (ng - t.eps) + (double)t.a0 * (ne - t.eps);
         }
@@ -2176,10 +2219,31 @@ __global__ void __launch_bounds__(TGV_NT) k_tgv(TgvArgs t, const float *__restri
 #pragma unroll
         for (int f = 0; f < 6; ++f) fld[buf][3 + f][j][i] = m[f];
     };
+    auto stage = [&]() {  // this column's plane-z values into the shared raw plane
+        if (rp) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) raw[c][j][i] = cz[c];
+        }
+    };
     const int zend = min(z0 + TGV_ZS, t.nz);
-    fill(0, z0 - 1, false);  // the plane below the slab: fields only (its value belongs to the slab below)
+    // prologue: the plane below the slab (fields only: its value belongs to the slab below)
+    ld(z0 - 1, cz);
+    ld(z0, c1);
+    ld(z0 + 1, c2);
+    stage();
+    __syncthreads();
+    fill(0, z0 - 1, false);
     int cur = 1;
     for (int z = z0; z < zend; ++z) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            cz[c] = c1[c];
+            c1[c] = c2[c];
+        }
+        ld(z + 2, c2);   // two planes ahead: in flight during this plane
+        __syncthreads();  // raw plane z - 1 consumed (fill of z - 1 done by every thread)
+        stage();
+        __syncthreads();
         fill(cur, z, true);
         __syncthreads();
         if (own && x < t.nx && y < t.ny) {
@@ -2210,7 +2274,6 @@ __global__ void __launch_bounds__(TGV_NT) k_tgv(TgvArgs t, const float *__restri
 #pragma unroll
             for (int d = 0; d < 3; ++d) gw[d * nv + k] = t.gs * gwv[d];
         }
-        __syncthreads();
         cur ^= 1;
     }
     // fixed-order block sum: shuffle tree per warp, then the warp partials in order

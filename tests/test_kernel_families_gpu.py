@@ -150,7 +150,7 @@ def test_family_argument_errors(ctx):
 # forced onto the direct kernels at a general acquisition
 RT_CASES = [("exp", 0.0, 0.075, 10.0, 0.2, 40), ("pow", 1.5, 0.0375, 20.0, 0.2, 40), ("exp", 0.0, 0.125, 10.0, 0.2, 66),
             ("pow", 0.8, 0.15, 10.0, 0.2, 80), ("exp", 0.0, 0.07, 10.0, 0.1, 37), ("gauss", 0.0, 0.25, 5.0, 0.2, 66),
-            ("gauss", 0.0, 0.06, 5.0, 0.1, 16), ("gauss", 0.0, 0.05, 5.0, 0.2, 13)]
+            ("gauss", 0.0, 0.061, 5.0, 0.1, 16), ("gauss", 0.0, 0.05, 5.0, 0.2, 13)]
 
 
 @pytest.mark.parametrize("kernel,nu,s,kappa,pitch,lmin", RT_CASES)

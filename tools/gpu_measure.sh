@@ -17,11 +17,14 @@ timeout 900 python tools/issue_capture.py run $TAG > $O/${TAG}_issue.log 2>&1 &&
   timeout 300 python tools/issue_capture.py parse $O/${TAG}_issue_c4.csv $TAG >> $O/${TAG}_issue.log 2>&1
 echo "issue rc=$?"; tail -2 $O/${TAG}_issue.log
 cp profiles/${TAG}_issue_c4.json $O/ 2>/dev/null
-timeout 900 python bench.py --steps 3 --warmup 3 > $O/${TAG}_bench_c4.json 2> $O/${TAG}_bench_c4.err
-echo "bench rc=$?"; tail -c 300 $O/${TAG}_bench_c4.json
 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $O/${TAG}_launches_c4.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > $O/${TAG}_launch_bench.json 2>&1
 echo "launches rc=$?"
+STEP_MS=$(python -c "import json,sys; print(json.loads(open('$O/${TAG}_launch_bench.json').read().strip().splitlines()[-1])['ms_per_step'])" 2>/dev/null || echo 0)
+python tools/launch_profile.py $O/${TAG}_launches_c4.csv $TAG $STEP_MS > $O/${TAG}_launch_profile.log 2>&1; echo "launch profile rc=$?"
+cp profiles/${TAG}_traffic_c4.json profiles/${TAG}_launches_c4.md $O/ 2>/dev/null
+timeout 900 python bench.py --steps 3 --warmup 3 > $O/${TAG}_bench_c4.json 2> $O/${TAG}_bench_c4.err
+echo "bench rc=$?"; tail -c 300 $O/${TAG}_bench_c4.json
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_adjoint_tay2 -s 1 -c 1 \
   -o $O/${TAG}_k2c python tools/profile_step.py c4 16 1 > $O/${TAG}_ncu_k2c.log 2>&1
 echo "ncu k2c rc=$?"
