@@ -1192,6 +1192,8 @@ __device__ __forceinline__ void fwd_epilogue(const Geo &g, const float *y, int f
     if (threadIdx.x == 0) rowloss[fe] = masked ? 0.0 : -COV / (sdy * sds);
 }
 
+// (Pairs of channels as one 64-bit shared-memory add — red.shared.add.u64, exact with a borrow-aware split —
+// measured 2.9x slower on B200: 368 vs 126 ms per 16 C4 frames.  Not taken.)
 // Unpredicated shared-memory integer add (ATOMS.ADD, no return value) at addr + OFF: a predicated
 // red is turned into a branch per atomic by ptxas, so lanes without a deposit add 0 to a per-lane
 // dummy word instead.
@@ -2151,10 +2153,11 @@ __device__ __forceinline__ float msym(const float m[6], int a, int b)
 // fields (n: 3, m: 6) from that plane and their own plane-(z + 1) registers, and the gradient of plane z is
 // a gather from field planes z and z - 1 (previous plane kept).
 constexpr int TGV_BX = 32, TGV_BY = 8, TGV_ZS = 32;
+constexpr int TGV_MINB = 4;  // 4 CTAs/SM (<= 46 registers): 0.22 vs 0.24 ms at 256^3 with 3 (52 registers)
 constexpr int TGV_RX = TGV_BX + 2, TGV_RY = TGV_BY + 2;               // raw region 34 x 10
 constexpr int TGV_NT = (TGV_RX * TGV_RY + 31) / 32 * 32;              // 352 threads
 
-__global__ void __launch_bounds__(TGV_NT) k_tgv(TgvArgs t, const float *__restrict__ P,
+__global__ void __launch_bounds__(TGV_NT, TGV_MINB) k_tgv(TgvArgs t, const float *__restrict__ P,
                                                 const float *__restrict__ w, float *__restrict__ gP,
                                                 float *__restrict__ gw, double *__restrict__ part)
 {
