@@ -36,8 +36,10 @@
  *     (no floating-point atomics: the forward's shared-memory deposits are fixed-point
  *     integer additions, which are associative; all floating-point reductions in fixed order).
  *   - Errors: the status code; pa_last_error() returns a thread-local message.
- *   - A pa_ctx owns only internal workspace (pose-gradient partials, scratch); use one
- *     context per stream.  Calls on different contexts may run concurrently.
+ *   - A pa_ctx owns only internal workspace (pose-gradient partials, scratch) and a cache of the
+ *     last geometry's plan (its host-side factorisation, ~20-40 ms, is recomputed only when the
+ *     grid, acquisition, E or policy change); use one context per stream.  Calls on different
+ *     contexts may run concurrently.
  */
 #ifndef PA_H
 #define PA_H

@@ -830,6 +830,12 @@ struct pa_ctx {
     bool ev_fwd = false, ev_adj = false;
     bool chk_pending = false;             // a pa_step verdict is in flight / not yet read
     int chk_E = 1;                        // elements of that step (to decode the verdict)
+    // the last plan (its host factorisation / Taylor bounds take ~20-40 ms): reused while the geometry,
+    // acquisition, E and policy are unchanged
+    Plan plan;
+    pa_grid plan_grid{};
+    pa_acq plan_acq{};
+    int plan_E = -1, plan_policy = -1;
 };
 
 namespace pa {
@@ -900,6 +906,26 @@ pa_status ws_reserve(pa_ctx *ctx, size_t bytes)
         return fail(PA_ENOMEM, "workspace allocation of %zu bytes failed", b);
     }
     ctx->ws_bytes = b;
+    return PA_OK;
+}
+
+// make_plan through the context's cache (same validation, same result; only the host work is saved)
+pa_status plan_for(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, int E, int F, Plan &pl)
+{
+    if (grid && acq && ctx->plan_E == E && ctx->plan_policy == ctx->policy &&
+        std::memcmp(&ctx->plan_grid, grid, sizeof *grid) == 0 && std::memcmp(&ctx->plan_acq, acq, sizeof *acq) == 0) {
+        if (F < 0) return fail(PA_ESHAPE, "F must be >= 0");
+        pl = ctx->plan;
+        pl.g.F = F;
+        return PA_OK;
+    }
+    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
+    if (s) return s;
+    ctx->plan = pl;
+    ctx->plan_grid = *grid;
+    ctx->plan_acq = *acq;
+    ctx->plan_E = E;
+    ctx->plan_policy = ctx->policy;
     return PA_OK;
 }
 
@@ -1097,7 +1123,7 @@ pa_status pa_forward(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
+    pa_status s = plan_for(ctx, grid, acq, E, F, pl);
     if (s) return s;
     if (F == 0) return PA_OK;
     if ((s = check_ptrs({tmpl, poses, p0, traces}))) return s;
@@ -1116,7 +1142,7 @@ pa_status pa_adjoint(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const 
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
+    pa_status s = plan_for(ctx, grid, acq, E, F, pl);
     if (s) return s;
     if ((s = check_ptrs({tmpl, grad_p0}))) return s;
     if (F > 0 && (s = check_ptrs({poses, cot}))) return s;
@@ -1141,7 +1167,7 @@ pa_status pa_adjoint_pose(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, c
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
+    pa_status s = plan_for(ctx, grid, acq, E, F, pl);
     if (s) return s;
     if ((s = check_ptrs({tmpl, p0, grad_p0}))) return s;
     if (F > 0 && (s = check_ptrs({poses, cot, grad_pose}))) return s;
@@ -1162,7 +1188,7 @@ pa_status pa_pose_grad(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, cons
 {
     if (!ctx) return fail(PA_EINVAL, "null ctx");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
+    pa_status s = plan_for(ctx, grid, acq, E, F, pl);
     if (s) return s;
     if (F == 0) return PA_OK;
     if ((s = check_ptrs({tmpl, poses, p0, cot, grad_pose}))) return s;
@@ -1254,7 +1280,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
 {
     if (!ctx || !cfg) return fail(PA_EINVAL, "null ctx/cfg");
     Plan pl;
-    pa_status s = make_plan(grid, acq, E, F, ctx->policy, pl);
+    pa_status s = plan_for(ctx, grid, acq, E, F, pl);
     if (s) return s;
     if (cfg->step < 1) return fail(PA_EINVAL, "cfg.step must be >= 1");
     if (cfg->loss_kind != 0 && cfg->loss_kind != 1) return fail(PA_EINVAL, "cfg.loss_kind must be 0 or 1");

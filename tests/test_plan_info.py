@@ -81,3 +81,34 @@ def test_other_families_use_direct_forward():
     grid = dict(nx=16, ny=16, nz=16, origin=(0.0, 0.0, 0.0), pitch=0.1)
     info = plan_info(grid, gen.family_acq(acq, "exp"), 4)
     assert info["fwd_deposit"] == 0 and info["adj_taylor"] == 0
+
+
+@pytest.mark.parametrize("kernel,s,kappa,pitch,want", [
+    ("gauss", 0.2, 5.0, 0.2, ("fast", 53)), ("gauss", 0.6, 5.0, 0.2, ("fast", 160)), ("gauss", 0.9, 5.0, 0.2, ("fast", 239)),
+    ("gauss", 0.05, 5.0, 0.2, ("direct_rt", 13)), ("exp", 0.075, 10.0, 0.2, ("direct_rt", 40)),
+    ("exp", 0.1, 10.0, 0.2, ("direct", 53)), ("pow", 0.15, 10.0, 0.2, ("direct_rt", 80)),
+    ("exp", 0.3, 30.0, 0.2, ("unsupported", 480)), ("pow", 0.5, 10.0, 0.2, ("unsupported", 266))])
+def test_kernel_selection_over_window_lengths(kernel, s, kappa, pitch, want):
+    """R26: which kernels a window length runs (host-only plan): the Gaussian fast path for 21 <= L_min <= 256, the
+    compiled direct classes for L_min in {26, 53, 106}, runtime direct classes when spread <= L_min and
+    L_min + spread <= 128, PA_EUNSUPPORTED beyond."""
+    from paper_2604_09643_b200._pa import PAError, PA_EUNSUPPORTED
+
+    grid = gen.make_grid((32, 32, 32), pitch)
+    acq = gen.make_acq(2048, s, t0=2.0, kappa=kappa, kernel=kernel, nu=1.5 if kernel == "pow" else 0.0)
+    kind, lmin = want
+    if kind == "unsupported":
+        with pytest.raises(PAError) as ei:
+            plan_info(grid, acq, 16)
+        assert ei.value.status == PA_EUNSUPPORTED and f"L_min={lmin}" in str(ei.value)
+        return
+    info = plan_info(grid, acq, 16)
+    assert info["lmin"] == lmin, info
+    if kind == "fast":
+        assert info["fwd_deposit"] == 1 and info["adj_kernel"] in (1, 2), info
+    elif kind == "direct":
+        assert info["fwd_deposit"] == 0 and info["adj_kernel"] == 0 and info["direct_class"] == lmin, info
+    else:
+        assert info["fwd_deposit"] == 0 and info["adj_kernel"] == 0 and info["direct_class"] < 0, info
+        spread = int(np.floor(np.sqrt(3.0) * pitch / (C_MM_US * DT))) + 2
+        assert -info["direct_class"] >= lmin + spread and spread <= lmin, (info, spread)

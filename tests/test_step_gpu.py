@@ -244,3 +244,34 @@ def test_tgv_lambda_applied_in_kernel(ctx):
     assert rel(m_w.cpu().numpy(), (0.1 * lam * gw.double().ravel()).cpu().numpy()) <= 1e-6
     vo, _, gwo = tgv_oracle(f64(p0), f64(w), float(np.float32(0.2)), 1.0, 2.0, 1e-3)
     assert rel(m_w.cpu().numpy(), 0.1 * lam * gwo.ravel()) <= 1e-5
+
+
+def test_pa_step_does_not_synchronise_the_host(ctx):
+    """pa_step enqueues its whole SfM iteration and returns (R25): on the C2 workload (~0.2 s of
+    device work per step) the host call returns in a small fraction of the device time, and a second step can be
+    enqueued behind the first without waiting."""
+    import time
+
+    w = gen.workload("c2", frames=60)
+    grid, acq = grid32(w.grid), acq32(w.acq)
+    tm = T(w.tmpl)
+    meas = ctx.forward(grid, acq, tm, T(w.poses_true()), T(gen.phantom(w)))
+    nv = w.grid["nx"] * w.grid["ny"] * w.grid["nz"]
+    p = torch.full((nv,), 0.05, device="cuda")
+    eu = T(w.euler_true)
+    am, aq = torch.zeros(2 * nv, device="cuda"), torch.zeros(12 * w.F, device="cuda")
+    g, L = torch.empty(nv, device="cuda"), torch.empty(2, device="cuda")
+    cfg = dict(lr_p0=1e-3, lr_rot=1e-3, lr_trans=1e-2, step=1)
+    ctx.step(grid, acq, tm, meas, p, eu, am, aq, g, L, cfg)  # warm-up (workspace allocation)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    t0 = time.perf_counter()
+    ctx.step(grid, acq, tm, meas, p, eu, am, aq, g, L, dict(cfg, step=2))
+    ctx.step(grid, acq, tm, meas, p, eu, am, aq, g, L, dict(cfg, step=3))
+    host_s = time.perf_counter() - t0
+    b.record()
+    torch.cuda.synchronize()
+    dev_s = a.elapsed_time(b) / 1e3
+    assert dev_s > 0.05 and host_s < 0.25 * dev_s, (host_s, dev_s)
+    ctx.step_status()
