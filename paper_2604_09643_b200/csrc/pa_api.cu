@@ -576,7 +576,7 @@ __global__ void k_count(Geo g, double c, double t0, double dt, double kappa, dou
         s = __dadd_rn(s, __dmul_rn((double)P[3 * a + 2], (double)xh[2]));
         x[a] = __dadd_rn(s, (double)P[9 + a]);
     }
-    const double w = __dmul_rn(kappa, sigma), cdt = __dmul_rn(c, dt);
+    const double w = __dmul_rn(kappa, sigma), cdt = __dmul_rn(c, dt), inv_cdt = 1.0 / cdt;
     const long long nvox = (long long)g.nx * g.ny * g.nz;
     long long n = 0;
     for (long long k = threadIdx.x; k < nvox; k += blockDim.x) {
@@ -586,8 +586,9 @@ __global__ void k_count(Geo g, double c, double t0, double dt, double kappa, dou
         const double y2 = __dadd_rn(g.oz, __dmul_rn(g.h, (double)l));
         const double dx = __dsub_rn(x[0], y0), dy = __dsub_rn(x[1], y1), dz = __dsub_rn(x[2], y2);
         const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-        const double lo = ceil(__ddiv_rn(__dsub_rn(__dsub_rn(r, w), __dmul_rn(c, t0)), cdt));
-        const double hi = floor(__ddiv_rn(__dsub_rn(__dadd_rn(r, w), __dmul_rn(c, t0)), cdt));
+        // first guess by a multiplication (the literal-predicate corrections below make the result exact)
+        const double lo = ceil(__dmul_rn(__dsub_rn(__dsub_rn(r, w), __dmul_rn(c, t0)), inv_cdt));
+        const double hi = floor(__dmul_rn(__dsub_rn(__dadd_rn(r, w), __dmul_rn(c, t0)), inv_cdt));
         if (hi < 0.0 || lo > (double)(g.nt - 1)) continue;
         int jlo = lo < 0.0 ? 0 : (int)lo;
         int jhi = hi > (double)(g.nt - 1) ? g.nt - 1 : (int)hi;

@@ -15,6 +15,8 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 cfgname = sys.argv[3] if len(sys.argv) > 3 else "c4"
 w = gen.workload(cfgname, frames=frames)
 ctx = Context(0)
+if os.environ.get("AB_POLICY"):  # e.g. adj_taylor: the kernel-selection policy of the timed context
+    ctx.set_policy(os.environ["AB_POLICY"].split(","))
 T = lambda a: torch.tensor(np.asarray(a, dtype=np.float32), device="cuda")  # noqa: E731
 tmpl = T(w.tmpl)
 meas = ctx.forward(w.grid, w.acq, tmpl, T(w.poses_true()), T(gen.phantom(w)))
@@ -31,5 +33,6 @@ for s in range(1, steps + 2):
         a, b = ctx.last_kernel_ms()
         fw.append(a)
         ad.append(b)
-print(json.dumps({"lib": os.environ.get("PA_LIB_PATH", "default"), "config": cfgname, "frames": frames,
+print(json.dumps({"lib": os.environ.get("PA_LIB_PATH", "default"), "policy": os.environ.get("AB_POLICY", "default"),
+                  "config": cfgname, "frames": frames,
                   "fwd_ms": float(np.median(fw)), "adj_ms": float(np.median(ad)), "loss": float(L[0])}))
