@@ -248,7 +248,7 @@ typedef struct {
     int32_t adj_taylor;  /* 1: the moment-filter adjoint K2a + K2c is available; 0: direct K2     */
     int32_t tay_order;   /* K2a/K2c: Taylor order M of the moment filters                       */
     double tay_err;      /* K2a/K2c: host bound on the Taylor remainder, relative to sum |terms| */
-    int32_t adj_svd;     /* 1: the adjoint runs in the forward's basis (K2s; default for L_min <= 32) */
+    int32_t adj_svd;     /* 1: the adjoint runs in the forward's basis (K2s: when K2c's bounds fail)  */
     double svd_derr;     /* K2s: max error of d/dt of the factorisation (pose moment), relative  */
     int32_t dep_groups;  /* K1d: round-accumulator copies (2 when pitch < 4 c dt, else 1)         */
     int32_t dep_ring;    /* K1d: positions of the round-accumulator ring (= nt + L_min: no ring)  */

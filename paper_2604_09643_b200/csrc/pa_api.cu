@@ -500,10 +500,10 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     if (policy & PA_POLICY_ADJ_DIRECT) pl.adj = ADJ_DIRECT;
     else if ((policy & PA_POLICY_ADJ_SVD) && svd_avail) pl.adj = ADJ_SVD;
     else if ((policy & PA_POLICY_ADJ_TAYLOR) && tay_avail) pl.adj = ADJ_TAY;
-    // default: the Taylor form, except where it needs 48-B filter records (short windows) and the
-    // rank-R basis is accurate enough (K2s measured 5% faster for the C5 class)
-    else if (svd_avail && (!tay_avail || pl.tay_NF > 8)) pl.adj = ADJ_SVD;
+    // default: the moment-filter adjoint K2c wherever its bounds hold (r2: also for short windows, where its
+    // 48-B records now beat K2s: C5, 8 frames, 461 vs 624 ms), else the rank-R-basis adjoint K2s
     else if (tay_avail) pl.adj = ADJ_TAY;
+    else if (svd_avail) pl.adj = ADJ_SVD;
     else pl.adj = ADJ_DIRECT;
     if ((!pl.fwd_dep || pl.adj == ADJ_DIRECT) && pl.klass < 0)
         return fail(PA_EUNSUPPORTED,
