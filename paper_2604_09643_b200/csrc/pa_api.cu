@@ -319,7 +319,7 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     // tile spans few window positions (h / a < 4: many lanes of a deposit instruction share a position, and
     // same-address atomics serialise), else 1.
     pl.dep_g = pl.g.h / a < 4.0 ? 2 : 1;
-    const int CS = (pl.dep_g * (R + 2)) | 1, CF = R + 1, NJ = pl.g.nt + lmin;
+    const int CS = (pl.dep_g * (R + 2 + PA_DEP_CNT)) | 1, CF = R + 1, NJ = pl.g.nt + lmin;
     auto ring = [&](int nw, int &nr, unsigned &nrm) {
         const int bzt = nw / 4 * PA_DEP_TPR;  // tiles along z in a round's block
         const double dist = pl.g.h * std::sqrt((double)(TX * TX + TY * TY) + (double)(TZ * (bzt - 1)) * (TZ * (bzt - 1)));

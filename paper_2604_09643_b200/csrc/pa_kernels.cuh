@@ -1120,6 +1120,11 @@ struct DepConst {
 #ifndef PA_DEP_TPR
 #define PA_DEP_TPR 4
 #endif
+#ifndef PA_DEP_CNT
+// 1: deposits carry the raw shifter bits (0x4B400000 + n: no subtraction per deposit) and a count word per
+// position (one more atomic of the constant 1); the flush removes count x 0x4B400000 (mod 2^32)
+#define PA_DEP_CNT 0
+#endif
 #ifndef PA_DEP_MAP
 #define PA_DEP_MAP 2  // lane -> voxel map: 2 = two z-adjacent tiles per warp slot (default); 1 = one tile, 2x4x1 per lane; 0 = 2x2x2 cluster
 #endif
@@ -1132,7 +1137,8 @@ constexpr int dep_nb(int nw) { return 22 - dep_ilog2(nw * PA_DEP_TPR); }
 template <int R_, int NW, int G_ = 1>
 struct DepCfg {
     static constexpr int R = R_;                  // separable rank (5 or 6; chosen per geometry on the host)
-    static constexpr int NQ = R + 2;              // int words per position: R channels, X, low word of channel 0
+    static constexpr int NQ = R + 2 + PA_DEP_CNT; // int words per position: R channels, X, low word of channel 0
+                                                  // (+ the deposit count, PA_DEP_CNT)
     static constexpr int G = G_;                  // lanes of one deposit instruction at the same position hit
                                                   // G different words (same-address atomics serialise)
     static constexpr int CS = (G * NQ) | 1;       // odd stride
@@ -1217,6 +1223,16 @@ __device__ __forceinline__ void red_s32(unsigned addr, int v)
 {
     asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
 }
+template <int OFF>
+__device__ __forceinline__ void red_one(unsigned addr)  // the deposit count (PA_DEP_CNT)
+{
+    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(addr), "n"(OFF) : "memory");
+}
+#if PA_DEP_CNT
+#define DEPV(x) __float_as_int(x)  // raw shifter bits; the flush subtracts count x 0x4B400000
+#else
+#define DEPV(x) (__float_as_int(x) - 0x4B400000)
+#endif
 
 #ifndef PA_DEP_MINB
 #define PA_DEP_MINB 3  // resident CTAs per SM of the 8-warp K1d (<= 80 registers, no spills; 2: 128 registers, 4.5% slower at C4)
@@ -1423,16 +1439,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
                         const float2 xm = __fmul2_rn(poly(0), ct);
                         const float2 hs = __ffma2_rn(xm, f2(1.0f / 1024.0f), f2(12582912.0f));
                         const float2 ls = __fadd2_rn(__ffma2_rn(__fadd2_rn(hs, f2(-12582912.0f)), f2(-1024.0f), xm), f2(12582912.0f));
-                        red_s32<0>(sax, __float_as_int(hs.x) - 0x4B400000);
-                        red_s32<0>(say, __float_as_int(hs.y) - 0x4B400000);
-                        red_s32<4 * (R + 1)>(sax, __float_as_int(ls.x) - 0x4B400000);
-                        red_s32<4 * (R + 1)>(say, __float_as_int(ls.y) - 0x4B400000);
+                        red_s32<0>(sax, DEPV(hs.x));
+                        red_s32<0>(say, DEPV(hs.y));
+                        red_s32<4 * (R + 1)>(sax, DEPV(ls.x));
+                        red_s32<4 * (R + 1)>(say, DEPV(ls.y));
+#if PA_DEP_CNT
+                        red_one<4 * (R + 2)>(sax);
+                        red_one<4 * (R + 2)>(say);
+#endif
                     }
                     auto chan = [&](auto mc) {
                         constexpr int m = decltype(mc)::value;
                         const float2 xm = __ffma2_rn(poly(m), (m & 1) ? o0 : ct, f2(12582912.0f));
-                        red_s32<4 * m>(sax, __float_as_int(xm.x) - 0x4B400000);
-                        red_s32<4 * m>(say, __float_as_int(xm.y) - 0x4B400000);
+                        red_s32<4 * m>(sax, DEPV(xm.x));
+                        red_s32<4 * m>(say, DEPV(xm.y));
                     };
                     chan(std::integral_constant<int, 1>{});
                     chan(std::integral_constant<int, 2>{});
@@ -1445,8 +1465,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
                         const float2 cx = make_float2(Lxx ? ct.x : 0.0f, Lxy ? ct.y : 0.0f);
                         const float2 px = __ffma2_rn(__ffma2_rn(__ffma2_rn(dc.cf2[R][3], t, dc.cf2[R][2]), t, dc.cf2[R][1]), t, dc.cf2[R][0]);
                         const float2 xm = __ffma2_rn(px, cx, f2(12582912.0f));
-                        red_s32<4 * R>(sax, __float_as_int(xm.x) - 0x4B400000);
-                        red_s32<4 * R>(say, __float_as_int(xm.y) - 0x4B400000);
+                        red_s32<4 * R>(sax, DEPV(xm.x));
+                        red_s32<4 * R>(say, DEPV(xm.y));
                     }
                 }
             }
@@ -1465,6 +1485,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
                 for (int k = 1; k < G; ++k)
 #pragma unroll
                     for (int c = 0; c < NQ; ++c) n[c] += qi[k * NQ + c];  // all copies together < 2^30: no overflow
+#if PA_DEP_CNT
+#pragma unroll
+                for (int c = 0; c < R + 2; ++c) n[c] = (int)((unsigned)n[c] - (unsigned)n[R + 2] * 0x4B400000u);
+#endif
                 qf[0] += __fmaf_rn((float)n[0], 1024.0f, (float)n[R + 1]);
 #pragma unroll
                 for (int c = 1; c <= R; ++c) qf[c] += (float)n[c];
