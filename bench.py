@@ -35,7 +35,7 @@ LANES = 128
 # (c dt) (in-window samples per pair).  The direct kernels (exp / power-law families, Gaussian fallback) walk the
 # window: the survey's per-update basis x W.
 OPS_PAIR = {
-    "k_fwd_dep": 78.5,            # K1d: geometry + window 31.5, Horner channels 30, 7 ATOMS + 7 bias adds + 3 address
+    "k_fwd_dep": 72.5,            # K1d: geometry + window 31.5, Horner channels 30, 8 ATOMS (7 words + count) + 3 address
     "k_adjoint_tay2_8": 76.25,    # K2c, 32-B records: geometry 25 + series & moments 36 + gradient 8.5 + reduction 6.75
     "k_adjoint_tay2_12": 88.25,   # K2c, 48-B records (short windows): synthetic division 27 instead of 15
     "k_adjoint_svd": 84.0,        # K2s: geometry 25 + rank-R basis evaluation 44 + gradient 8.5 + reduction 6.75

@@ -1122,8 +1122,9 @@ struct DepConst {
 #endif
 #ifndef PA_DEP_CNT
 // 1: deposits carry the raw shifter bits (0x4B400000 + n: no subtraction per deposit) and a count word per
-// position (one more atomic of the constant 1); the flush removes count x 0x4B400000 (mod 2^32)
-#define PA_DEP_CNT 0
+// position (one more atomic of the constant 1); the flush removes count x 0x4B400000 (mod 2^32, exact since
+// |sum n| < 2^30).  Measured 1% faster at C4 than subtracting per deposit (124.6 vs 125.8 ms per 16 frames).
+#define PA_DEP_CNT 1
 #endif
 #ifndef PA_DEP_MAP
 #define PA_DEP_MAP 2  // lane -> voxel map: 2 = two z-adjacent tiles per warp slot (default); 1 = one tile, 2x4x1 per lane; 0 = 2x2x2 cluster

@@ -55,7 +55,7 @@ def test_round_accumulator_ring(name):
     rt = 0.5 * h * np.sqrt(7.0 ** 2 + 7.0 ** 2 + 3.0 ** 2)
     span = dist / a + 1 + 2 * rt / a + 7
     ring = info["dep_ring"]
-    cs = (info["dep_groups"] * (info["dep_rank"] + 2)) | 1
+    cs = (info["dep_groups"] * (info["dep_rank"] + 3)) | 1  # R channels, X, channel 0 low word, deposit count
     assert ring >= span and ring * cs >= nt, (ring, span)
     assert ring == nt + lmin or (ring & (ring - 1)) == 0, ring
 
