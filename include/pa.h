@@ -255,6 +255,7 @@ typedef struct {
     int32_t adj_kernel;  /* the adjoint that runs: 0 direct K2, 1 moment-filter K2a+K2c, 2 K2s     */
     int32_t direct_class;/* direct kernels (K1/K2): L_min of the compiled class, or -capacity of the
                             runtime class (L_min + cluster spread <= capacity), 0 if none fits     */
+    int32_t dep_round;   /* K1d: tiles per warp per round (8 when its ring keeps the CTAs per SM, else 4) */
 } pa_plan_info;
 pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out);
 /* The same for a context (its pa_set_policy applied). */

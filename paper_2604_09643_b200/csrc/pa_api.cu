@@ -136,6 +136,7 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     pl.svd_derr = 1.0;
     pl.dep_nw = 0;
     pl.dep_g = 1;
+    pl.dep_tpr = 4;
     pl.dep_R = lmin <= 32 ? 6 : 5;
     auto G = [&](double t, int q) {  // tap q in [0, K): k = q - MA
         const double D = Dc + Dw * t - (double)(q - MA) * a;
@@ -320,8 +321,8 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     // same-address atomics serialise), else 1.
     pl.dep_g = pl.g.h / a < 4.0 ? 2 : 1;
     const int CS = (pl.dep_g * (R + 2 + PA_DEP_CNT)) | 1, CF = R + 1, NJ = pl.g.nt + lmin;
-    auto ring = [&](int nw, int &nr, unsigned &nrm) {
-        const int bzt = nw / 4 * PA_DEP_TPR;  // tiles along z in a round's block
+    auto ring = [&](int nw, int tpr, int &nr, unsigned &nrm) {
+        const int bzt = nw / 4 * tpr;  // tiles along z in a round's block
         const double dist = pl.g.h * std::sqrt((double)(TX * TX + TY * TY) + (double)(TZ * (bzt - 1)) * (TZ * (bzt - 1)));
         const int need = std::max((int)std::ceil((dist + 2.0 * pl.g.rt_d + 2.0 * a) / a) + 16, (pl.g.nt + CS - 1) / CS);
         int p2 = 64;
@@ -336,23 +337,32 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     };
     auto smem = [&](int nr) { return ((size_t)CS * nr + (size_t)CF * NJ) * 4; };
     const size_t st8 = 8 * 32 * 8 + 4 * (32 + CS) + 64, st16 = 16 * 32 * 8 + 4 * (32 + CS) + 64;  // static smem
-    int nr8, nr16;
-    unsigned m8, m16;
-    ring(8, nr8, m8);
-    ring(16, nr16, m16);
-    if (2 * (smem(nr8) + st8 + 1024) <= 228 * 1024) {
+    // resident 8-warp CTAs per SM with a ring for rounds of tpr tiles per warp
+    auto ncta8 = [&](int tpr, int &nr, unsigned &nrm) {
+        ring(8, tpr, nr, nrm);
+        return std::min(PA_DEP_MINB, (int)((228 * 1024) / (smem(nr) + st8 + 1024)));
+    };
+    int nr4, nr8t, nr16;
+    unsigned m4, m8t, m16;
+    const int n4 = ncta8(4, nr4, m4), n8 = ncta8(8, nr8t, m8t);
+    ring(16, 4, nr16, m16);
+    if (n4 >= 2) {
+        // rounds of 8 tiles per warp (half the flushes and barriers; one bit less per deposit word, NB) when
+        // their larger ring keeps the resident CTAs of rounds of 4 (C4: 122.5 vs 124.6 ms per 16 frames)
         pl.dep_nw = 8;
-        dc.nr = nr8;
-        dc.nrm = m8;
+        pl.dep_tpr = n8 >= n4 ? 8 : 4;
+        dc.nr = pl.dep_tpr == 8 ? nr8t : nr4;
+        dc.nrm = pl.dep_tpr == 8 ? m8t : m4;
     } else if (smem(nr16) + st16 <= 227 * 1024) {
         pl.dep_nw = 16;
+        pl.dep_tpr = 4;
         dc.nr = nr16;
         dc.nrm = m16;
     } else {
         pl.dep_nw = 0;  // the row accumulators do not fit: the direct forward K1
         return;
     }
-    const int NB = dep_nb(pl.dep_nw), NB0 = NB + 10;  // == DepCfg<R, NW>::NB, NB0
+    const int NB = dep_nb(pl.dep_nw, pl.dep_tpr), NB0 = NB + 10;  // == DepCfg<R, NW, G, TPR>::NB, NB0
     // fixed-point scales: |c| <= 1 (P / Pmax, r_lo / r), |n| <= 2^NB (channel 0: 2^NB0)
     for (int m = 0; m <= R; ++m) {
         const double S = std::ldexp(1.0, m == 0 ? NB0 : NB) / (pmaxv[m] * (1.0 + 1e-3) + 1e-300);
@@ -486,6 +496,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     pl.dep_R = 0;
     pl.dep_nw = 0;
     pl.dep_g = 1;
+    pl.dep_tpr = 4;
     const bool fast = pl.fam == KF_GAUSS && wmin >= FAST_LMIN && wmin <= PA_LMAX;
     if (fast) {
         make_tay(pl, wmin, a, sig);
@@ -1423,6 +1434,7 @@ static void fill_info(const Plan &pl, pa_plan_info *out)
     out->svd_derr = pl.svd_derr;
     out->dep_groups = pl.dep_g;
     out->dep_ring = pl.dc.nr;
+    out->dep_round = pl.dep_tpr;
     out->adj_kernel = pl.adj;
     out->direct_class = pl.klass < 0 ? 0 : (pl.klass >= KLASS_RT ? -kRtClasses[pl.klass - KLASS_RT].rc : kClasses[pl.klass].lmin);
 }

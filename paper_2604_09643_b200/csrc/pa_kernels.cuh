@@ -1117,9 +1117,6 @@ struct DepConst {
     unsigned nrm;              // nr - 1 (nr a power of two), or ~0 when the ring covers the whole row (nr = NJ)
 };
 
-#ifndef PA_DEP_TPR
-#define PA_DEP_TPR 4
-#endif
 #ifndef PA_DEP_CNT
 // 1: deposits carry the raw shifter bits (0x4B400000 + n: no subtraction per deposit) and a count word per
 // position (one more atomic of the constant 1); the flush removes count x 0x4B400000 (mod 2^32, exact since
@@ -1129,13 +1126,13 @@ struct DepConst {
 #ifndef PA_DEP_MAP
 #define PA_DEP_MAP 2  // lane -> voxel map: 2 = two z-adjacent tiles per warp slot (default); 1 = one tile, 2x4x1 per lane; 0 = 2x2x2 cluster
 #endif
-// |deposit| <= 2^NB with NW warps x PA_DEP_TPR tiles x 256 voxels adding to a word per round: sums < 2^30
+// |deposit| <= 2^NB with NW warps x TPR tiles x 256 voxels adding to a word per round: sums < 2^30
 constexpr int dep_ilog2(int x) { return x <= 1 ? 0 : 1 + dep_ilog2(x / 2); }
-constexpr int dep_nb(int nw) { return 22 - dep_ilog2(nw * PA_DEP_TPR); }
+constexpr int dep_nb(int nw, int tpr) { return 22 - dep_ilog2(nw * tpr); }
 
 // G = copies of the round accumulator, interleaved per position; lane l deposits into copy l % G
 // (chosen per geometry on the host: Plan::dep_g)
-template <int R_, int NW, int G_ = 1>
+template <int R_, int NW, int G_ = 1, int TPR_ = 4>
 struct DepCfg {
     static constexpr int R = R_;                  // separable rank (5 or 6; chosen per geometry on the host)
     static constexpr int NQ = R + 2 + PA_DEP_CNT; // int words per position: R channels, X, low word of channel 0
@@ -1144,8 +1141,8 @@ struct DepCfg {
                                                   // G different words (same-address atomics serialise)
     static constexpr int CS = (G * NQ) | 1;       // odd stride
     static constexpr int CF = R + 1;              // fp32 words per position
-    static constexpr int TPR = PA_DEP_TPR;        // tiles per warp per round
-    static constexpr int NB = dep_nb(NW);         // a round adds <= 256 NW TPR deposits per word
+    static constexpr int TPR = TPR_;              // tiles per warp per round (4 or 8, chosen per geometry on the host)
+    static constexpr int NB = dep_nb(NW, TPR);    // a round adds <= 256 NW TPR deposits per word
     static constexpr int NB0 = NB + 10;           // channel 0: hi (<= 2^NB) * 2^10 + lo
     static __host__ __device__ int njp(int nt, int lmin) { return nt + lmin; }
     // ring of nr positions x CS round words + NJ x CF fp32 row accumulators
@@ -1238,7 +1235,7 @@ __device__ __forceinline__ void red_one(unsigned addr)  // the deposit count (PA
 #ifndef PA_DEP_MINB
 #define PA_DEP_MINB 3  // resident CTAs per SM of the 8-warp K1d (<= 80 registers, no spills; 2: 128 registers, 4.5% slower at C4)
 #endif
-template <int RK, int NW, int NG>
+template <int RK, int NW, int NG, int TPR_>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(Geo g, DepConst dc, const float *__restrict__ poses,
                                                                        const float *__restrict__ tmpl,
                                                                        const float *__restrict__ p0,
@@ -1248,7 +1245,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
                                                                        const uint8_t *__restrict__ row_mask,
                                                                        double *__restrict__ rowloss)
 {
-    using C = DepCfg<RK, NW, NG>;
+    using C = DepCfg<RK, NW, NG, TPR_>;
     constexpr int R = C::R, CS = C::CS, CF = C::CF, NQ = C::NQ, G = C::G;
     extern __shared__ int smi[];
     const int LMIN = g.lmin;  // runtime window length L_min

@@ -58,6 +58,7 @@ struct Plan {
     int dep_R;        // separable rank (5 or 6)
     int dep_nw;       // K1d warps per CTA (8: two CTAs per SM; 16: one)
     int dep_g;        // K1d round-accumulator copies (lane l deposits into copy l % dep_g)
+    int dep_tpr;      // K1d tiles per warp per round (8 when it keeps the resident CTAs per SM of 4, else 4)
     double dep_err;   // measured error of the factorisation (relative to max |G|)
     int klass;        // direct-kernel class (index into kClasses) or -1
     int fam;          // pa_kernel (KF_*)

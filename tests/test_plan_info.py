@@ -43,14 +43,15 @@ def test_plan_of_baseline_configs(name):
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_round_accumulator_ring(name):
     """K1d's fixed-point round accumulator is a ring of positions (pos mod ring): it must hold every
-    position one round can touch — the window-base spread of the round's 2 x 2 x (NW/4 x 4) block of
-    8x8x4 tiles (centre distance / a, +1) plus one tile's window span (spanhi - spanlo <= 2 rt / a + 7,
+    position one round can touch — the window-base spread of the round's 2 x 2 x (NW/4 x TPR) block of
+    8x8x4 tiles (TPR = tiles per warp per round, 4 or 8) (centre distance / a, +1) plus one tile's window span (spanhi - spanlo <= 2 rt / a + 7,
     rt = tile half-diagonal) — and the final nt-sample trace, which reuses it."""
     w = gen.workload(name, frames=2)
     info = plan_info(w.grid, w.acq, w.E)
     h, a, nt, lmin = w.grid["pitch"], C_MM_US * DT, w.acq["nt"], info["lmin"]
     assert info["dep_groups"] == (2 if h / a < 4.0 else 1)
-    bzt = info["dep_warps"] // 4 * 4                       # tiles along z per round (4 tiles per warp)
+    assert info["dep_round"] in (4, 8)
+    bzt = info["dep_warps"] // 4 * info["dep_round"]       # tiles along z per round
     dist = h * np.sqrt(8.0 ** 2 + 8.0 ** 2 + (4.0 * (bzt - 1)) ** 2)
     rt = 0.5 * h * np.sqrt(7.0 ** 2 + 7.0 ** 2 + 3.0 ** 2)
     span = dist / a + 1 + 2 * rt / a + 7
