@@ -17,10 +17,10 @@ pa_status launch_tay_t(pa_ctx *ctx, const Plan &pl, const float *poses, const fl
     const size_t per_frame = (size_t)E * njp * T::NF * sizeof(float);
     int Fc = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t(48) << 20) / per_frame));
     auto smem_of = [&](int fc) {
-        return (size_t)2 * E4 * sizeof(AncT) +
-               ((size_t)(ADJ_THREADS / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
+        return (size_t)PA_ADJ_TPC * E4 * sizeof(AncT) +
+               ((size_t)(TAY_NT / 32) * E * 3 + (POSE ? (size_t)fc * E * 3 : 0)) * sizeof(float);
     };
-    while (Fc > 1 && smem_of(Fc) > 113 * 1024) --Fc;
+    while (Fc > 1 && smem_of(Fc) > (size_t)(228 / PA_ADJ_MINB - 1) * 1024) --Fc;  // keep PA_ADJ_MINB CTAs per SM
     Fc = std::min(Fc, std::max(1, 65535 / E));  // K2a grid.y = Fc E
     Fc = std::min(Fc, F > 0 ? F : 1);
     const size_t smem = smem_of(Fc);
@@ -28,10 +28,10 @@ pa_status launch_tay_t(pa_ctx *ctx, const Plan &pl, const float *poses, const fl
     auto kern = k_adjoint_tay2<NF, POSE, ADJ>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ADJ_THREADS, smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TAY_NT, smem));
     if (occ < 1) occ = 1;
     int P = occ * ctx_nsm(ctx);
-    const int nwork = pl.g.ntx * pl.g.nty * ((pl.g.ntz + 1) / 2);  // tile pairs
+    const int nwork = pl.g.ntx * pl.g.nty * (PA_ADJ_TPC == 2 ? (pl.g.ntz + 1) / 2 : pl.g.ntz);  // tile pairs / tiles
     if (P > nwork) P = nwork;
     L.P = P;
     L.Fc = Fc;
@@ -46,7 +46,7 @@ pa_status launch_tay_t(pa_ctx *ctx, const Plan &pl, const float *poses, const fl
         k_adj_filter<NF><<<dim3((njp + 255) / 256, fn * E), 256, 0, st>>>(pl.g, pl.tf, cot, f0, fn, njp, Fg);
         CUDA_TRY(cudaGetLastError());
         ++g_nlaunch;
-        kern<<<P, ADJ_THREADS, smem, st>>>(pl.g, pl.tc, poses, tmpl, p0, Fg, grad_p0, partial, f0, fn, njp,
+        kern<<<P, TAY_NT, smem, st>>>(pl.g, pl.tc, poses, tmpl, p0, Fg, grad_p0, partial, f0, fn, njp,
                                            pl.tay_pad, pl.tay_sentinel);
         CUDA_TRY(cudaGetLastError());
     }

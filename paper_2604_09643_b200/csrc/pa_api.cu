@@ -6,6 +6,8 @@
 #define PA_API_TU
 #include "pa_plan.h"
 
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1048,13 +1050,59 @@ pa_status tgv_args(const pa_grid *grid, float a1, float a0, float eps, float gs,
     return PA_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// TMA tensor maps of P {nx, ny, nz} and w {nx, ny, nz, 3} (fp32, boxes {40, 10, 1(, 3)}, zero fill outside);
+// false when the shape / alignment does not allow them (row pitch a multiple of 16 B, 16-B aligned bases)
+bool tgv_tensor_maps(const TgvArgs &t, const float *P, const float *w, CUtensorMap &mP, CUtensorMap &mW)
+{
+    auto enc = tensor_map_encoder();
+    if (!enc || t.nx % 4 != 0 || (reinterpret_cast<uintptr_t>(P) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
+    const cuuint64_t nx = t.nx, ny = t.ny, nz = t.nz;
+    const cuuint64_t dims[4] = {nx, ny, nz, 3};
+    const cuuint64_t strides[3] = {nx * 4, nx * ny * 4, nx * ny * nz * 4};
+    const cuuint32_t box[4] = {(cuuint32_t)TGV_BOXX, (cuuint32_t)TGV_RY, 1, 3};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&mP, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(P), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(&mW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(w), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    return true;
+}
+
+#ifndef PA_TGV_TMA
+#define PA_TGV_TMA 1  // 0: always the register-streamed k_tgv
+#endif
 // value: out[0] = vscale * TGV (+ out[0] if accumulate); gradients scaled by gscale (TgvArgs::gs)
 pa_status launch_tgv(const TgvArgs &t, const float *P, const float *w, float *gP, float *gw, double *part, float *value,
                      float vscale, int accumulate, cudaStream_t st)
 {
     dim3 gd((t.nx + TGV_BX - 1) / TGV_BX, (t.ny + TGV_BY - 1) / TGV_BY, (t.nz + TGV_ZS - 1) / TGV_ZS);
+    CUtensorMap mP, mW;
     ++g_nlaunch;
-    k_tgv<<<gd, TGV_NT, 0, st>>>(t, P, w, gP, gw, part);
+    if (PA_TGV_TMA && tgv_tensor_maps(t, P, w, mP, mW)) {
+        const size_t smem = tgv_tma_smem();
+        CUDA_TRY(cudaFuncSetAttribute(k_tgv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_tgv_tma<<<gd, TGV_NT, smem, st>>>(t, mP, mW, gP, gw, part);
+    } else {
+        k_tgv<<<gd, TGV_NT, 0, st>>>(t, P, w, gP, gw, part);
+    }
     CUDA_TRY(cudaGetLastError());
     ++g_nlaunch;
     k_sum_parts<<<1, 256, 0, st>>>(part, (long long)gd.x * gd.y * gd.z, vscale, accumulate, value);

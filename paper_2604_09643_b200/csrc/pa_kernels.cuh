@@ -1532,7 +1532,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
 // from the L2-resident per-row filter records (one 256-bit load per voxel, the last tap included),
 // A1 = u_m (D_m S0 - a S1) and Bq / s^2 = u_m ((D_m^2/s^2 - 1) S0 - (2a/s^2) D_m S1 + (a^2/s^2) S2) (the
 // filters carry the 1/2 of D/(2r)).  A thread owns voxels z and z + 2 of an 8x8x4 anchor tile (a CTA =
-// two tiles stacked in z, 128 threads each), so the geometry, the series and the gradient terms of the
+// one tile of 128 threads, or two stacked in z: PA_ADJ_TPC), so the geometry, the series and the gradient terms of the
 // two voxels run as FFMA2/FMUL2/FADD2, the anchor is read once for both, and their element-gradient
 // terms are summed before the warp reduction.  No per-pair validity logic: zero-padded filter rows, a
 // sentinel anchor for culled / padding elements, amplitude 0 for voxels outside the grid.
@@ -1665,11 +1665,18 @@ __device__ __forceinline__ void tay2_stage_b(const Geo &g, const TayConst &tc, c
     }
 }
 
-#ifndef PA_ADJ_MINB
-#define PA_ADJ_MINB 2  // resident CTAs per SM of K2c
+#ifndef PA_ADJ_TPC
+// K2c tiles per CTA: 1 (128 threads, 4 CTAs/SM at 128 registers: C4 105.8 ms per 16 frames) or 2 (256
+// threads, 2 CTAs/SM: 107.2 ms).  Measured with 1 tile per CTA: 5 CTAs/SM (96 registers, 16 B spills)
+// 106.3 ms, 6 CTAs/SM (80 registers) 106.4 ms — more resident warps do not pay.
+#define PA_ADJ_TPC 1
 #endif
+#ifndef PA_ADJ_MINB
+#define PA_ADJ_MINB (PA_ADJ_TPC == 2 ? 2 : 4)  // resident CTAs per SM of K2c
+#endif
+constexpr int TAY_NT = 128 * PA_ADJ_TPC;  // K2c threads per CTA
 template <int NF, bool POSE, bool ADJ>
-__global__ void __launch_bounds__(ADJ_THREADS, PA_ADJ_MINB) k_adjoint_tay2(Geo g, TayConst tc, const float *__restrict__ poses,
+__global__ void __launch_bounds__(TAY_NT, PA_ADJ_MINB) k_adjoint_tay2(Geo g, TayConst tc, const float *__restrict__ poses,
                                                                 const float *__restrict__ tmpl,
                                                                 const float *__restrict__ p0,
                                                                 const float *__restrict__ Fg,
@@ -1680,11 +1687,12 @@ __global__ void __launch_bounds__(ADJ_THREADS, PA_ADJ_MINB) k_adjoint_tay2(Geo g
     extern __shared__ float sm[];
     const int E = g.E, F = g.F;
     const int E4 = (E + 3) & ~3;                           // elements padded to the unroll of 4 (sentinels)
-    AncT *anc = reinterpret_cast<AncT *>(sm);             // [2][E4]: the two tiles of the CTA
-    float *wred = reinterpret_cast<float *>(anc + 2 * E4); // [8][E][3]
-    float *gacc = wred + (ADJ_THREADS / 32) * E * 3;       // [fn][E][3]
+    constexpr int TPC = PA_ADJ_TPC, NT = TAY_NT;
+    AncT *anc = reinterpret_cast<AncT *>(sm);               // [TPC][E4]: the tiles of the CTA
+    float *wred = reinterpret_cast<float *>(anc + TPC * E4); // [NT/32][E][3]
+    float *gacc = wred + (NT / 32) * E * 3;                  // [fn][E][3]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int half = tid >> 7, u = tid & 127;
+    const int half = TPC == 2 ? tid >> 7 : 0, u = tid & 127;
     const int lx = u & 7, ly = (u >> 3) & 7, lzp = u >> 6;  // voxels (lx, ly, lzp) and (lx, ly, lzp + 2)
     const float ex = ((float)lx - 0.5f * (TX - 1)) * g.hf;
     const float ey = ((float)ly - 0.5f * (TY - 1)) * g.hf;
@@ -1694,14 +1702,14 @@ __global__ void __launch_bounds__(ADJ_THREADS, PA_ADJ_MINB) k_adjoint_tay2(Geo g
     const float ex2x = 2.0f * ex, ey2x = 2.0f * ey;
     const float2 ez2x = __fmul2_rn(f2(2.0f), ez);
     const AncT *anch = anc + half * E4;
-    const int ntzp = (g.ntz + 1) >> 1, ntp = g.ntx * g.nty * ntzp;
+    const int ntzp = TPC == 2 ? (g.ntz + 1) >> 1 : g.ntz, ntp = g.ntx * g.nty * ntzp;
 
     if (POSE) {
-        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS) gacc[q] = 0.0f;
+        for (int q = tid; q < fn * E * 3; q += NT) gacc[q] = 0.0f;
     }
     for (int tp = blockIdx.x; tp < ntp; tp += gridDim.x) {
         const int tx = tp % g.ntx, ty = (tp / g.ntx) % g.nty, tzp = tp / (g.ntx * g.nty);
-        const int tz = 2 * tzp + half;
+        const int tz = TPC * tzp + half;
         const int ix = TX * tx + lx, iy = TY * ty + ly, iza = TZ * tz + lzp, izb = iza + 2;
         const bool ina = ix < g.nx && iy < g.ny && iza < g.nz, inb = ix < g.nx && iy < g.ny && izb < g.nz;
         const size_t ka = ((size_t)iza * g.ny + iy) * g.nx + ix, kb = ka + 2 * (size_t)g.nx * g.ny;
@@ -1711,9 +1719,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, PA_ADJ_MINB) k_adjoint_tay2(Geo g
         for (int fl = 0; fl < fn; ++fl) {
             const int f = f0 + fl;
             __syncthreads();  // previous frame's anchors / wred consumed
-            for (int q = tid; q < 2 * E4; q += ADJ_THREADS) {
+            for (int q = tid; q < TPC * E4; q += NT) {
                 const int hh = q / E4, e = q - hh * E4;
-                const int tzh = 2 * tzp + hh;
+                const int tzh = TPC * tzp + hh;
                 Anc A;
                 bool culled = true;
                 if (e < E) {
@@ -1791,10 +1799,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, PA_ADJ_MINB) k_adjoint_tay2(Geo g
             }
             if (POSE) {
                 __syncthreads();
-                for (int q = tid; q < E * 3; q += ADJ_THREADS) {
+                for (int q = tid; q < E * 3; q += NT) {
                     float s = 0.0f;
 #pragma unroll
-                    for (int w = 0; w < ADJ_THREADS / 32; ++w) s += wred[w * E * 3 + q];
+                    for (int w = 0; w < NT / 32; ++w) s += wred[w * E * 3 + q];
                     gacc[fl * E * 3 + q] += s;
                 }
             }
@@ -1806,7 +1814,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, PA_ADJ_MINB) k_adjoint_tay2(Geo g
     }
     if (POSE) {
         __syncthreads();
-        for (int q = tid; q < fn * E * 3; q += ADJ_THREADS)
+        for (int q = tid; q < fn * E * 3; q += NT)
             partial[((size_t)blockIdx.x * F + f0) * E * 3 + q] = gacc[q];
     }
 }
@@ -2097,17 +2105,31 @@ static __global__ void k_absmax(const float *__restrict__ p, long long n, unsign
 
 }  // namespace pa
 
-#ifdef PA_API_TU  // the TGV kernel is launched from pa_api.cu only
+#ifdef PA_API_TU  // the TGV kernels are launched from pa_api.cu only
+#include <cuda.h>  // CUtensorMap
 namespace pa {
 
 // ============================================================================================
 // K7 — TGV^2 regulariser of Eq. 2 (reading R20): value and gradients
 //   L = a1 sum_O phi(grad P - w) + a0 sum_O phi(E w),  phi(v) = sqrt(|v|^2 + eps^2) - eps,
-//   forward differences, O = {x : x_d <= n_d - 2}.
-// One thread per voxel x; the gradient is a gather: the dphi fields n(y) = g/|g|_eps and
-// m(y) = Ew/|Ew|_eps are recomputed at y in {x, x - e_x, x - e_y, x - e_z} from cached P, w
-// (no workspace, one pass, HBM traffic ~ 32 B per voxel).  The value is reduced per block in
-// fp64 (fixed order) into `part`, summed by k_sum_parts.
+//   forward differences, O = {x : x_d <= n_d - 2}, and
+//   dL/dP(k)   = a1/h sum_d [n_d(k - e_d) - n_d(k)]
+//   dL/dw_b(k) = -a1 n_b(k) + a0/h sum_a [m_ab(k - e_a) - m_ab(k)]      (m symmetric)
+// with the dphi fields n = g/|g|_eps (g = grad P - w) and m = E/|E|_eps (E = sym grad w).
+// 2.5-D streaming: a CTA owns a 32 x 8 column of (x, y) outputs and walks z through a slab; thread q owns the
+// raw point (x0 - 1 + q % 34, y0 - 1 + q / 34) of a 34 x 10 region.  Per plane z, the 33 x 9 halo points form
+// n and m from raw plane z (own value, x + 1 and y + 1 neighbours) and their own plane-(z + 1) value, keep
+// n and m in registers and publish only what a neighbour's gradient reads: the x-row (n_x, m_xx, m_xy, m_xz)
+// and the y-row (n_y, m_xy, m_yy, m_yz); the gradient of plane z at the owned points takes the -e_x / -e_y
+// rows from shared memory and the -e_z row (n_z, m_xz, m_yz, m_zz of plane z - 1) from the registers of the
+// previous plane.  The value is reduced per block in fp64 (fixed order) into `part`, summed by k_sum_parts.
+// Two variants move the raw planes:
+//   k_tgv_tma (nx % 4 == 0, 16-B aligned): TMA (cp.async.bulk.tensor) copies each raw plane (40 x 10 box of
+//     P and 40 x 10 x 3 of w, x from x0 - 4: TMA needs a 16-B aligned innermost start; zero-filled outside the volume) into a ring of TGV_STAGES shared-memory stages
+//     on an mbarrier, issued TGV_STAGES - 1 planes ahead — the kernel is HBM-latency-bound, and the ring keeps
+//     ~4x more bytes in flight per SM than registers can; double-buffered field rows, one barrier per plane;
+//   k_tgv (any shape): each thread streams its column through four register buffers (rotated by name) and
+//     publishes raw plane z in shared memory; two barriers per plane.
 // ============================================================================================
 struct TgvArgs {
     int nx, ny, nz;
@@ -2115,203 +2137,282 @@ struct TgvArgs {
     float gs;  // scale of both gradients (lambda of Eq. 2 inside pa_step, 1 for pa_tgv)
 };
 
-__device__ __forceinline__ bool tgv_in(const TgvArgs &t, int x, int y, int z)
-{
-    return x >= 0 && y >= 0 && z >= 0 && x <= t.nx - 2 && y <= t.ny - 2 && z <= t.nz - 2;
-}
-
-// n(y) and m(y) (6 unique: xx, yy, zz, xy, xz, yz) at an interior point y; also |g|_eps, |Ew|_eps
-__device__ __forceinline__ void tgv_fields(const TgvArgs &t, const float *__restrict__ P, const float *__restrict__ w,
-                                           int x, int y, int z, float n[3], float m[6], float &ng, float &ne)
-{
-    // 32-bit offsets: 3 nv < 2^31 (checked by launch_tgv)
-    const int sy = t.nx, sz = t.nx * t.ny, nv = sz * t.nz;
-    const int k = z * sz + y * sy + x;
-    const int off[3] = {1, sy, sz};
-    const float p = __ldg(P + k);
-    float wv[3], D[3][3];  // D[a][b] = d_a w_b
-#pragma unroll
-    for (int b = 0; b < 3; ++b) wv[b] = __ldg(w + b * nv + k);
-    float g[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        g[a] = (__ldg(P + k + off[a]) - p) * t.inv_h - wv[a];
-#pragma unroll
-        for (int b = 0; b < 3; ++b) D[a][b] = (__ldg(w + b * nv + k + off[a]) - wv[b]) * t.inv_h;
-    }
-    // |v|_eps and 1/|v|_eps from one MUFU.RSQ (no IEEE sqrt / division sequences)
-    const float sg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + t.eps * t.eps;
-    const float ig = rsqrtf(sg);
-    ng = sg * ig;
-    n[0] = g[0] * ig;
-    n[1] = g[1] * ig;
-    n[2] = g[2] * ig;
-    const float exx = D[0][0], eyy = D[1][1], ezz = D[2][2];
-    const float exy = 0.5f * (D[0][1] + D[1][0]), exz = 0.5f * (D[0][2] + D[2][0]), eyz = 0.5f * (D[1][2] + D[2][1]);
-    const float se = exx * exx + eyy * eyy + ezz * ezz + 2.0f * (exy * exy + exz * exz + eyz * eyz) + t.eps * t.eps;
-    const float ie = rsqrtf(se);
-    ne = se * ie;
-    m[0] = exx * ie;
-    m[1] = eyy * ie;
-    m[2] = ezz * ie;
-    m[3] = exy * ie;
-    m[4] = exz * ie;
-    m[5] = eyz * ie;
-}
-
-__device__ __forceinline__ float msym(const float m[6], int a, int b)
-{
-    if (a == b) return m[a];
-    const int s = a + b;  // (0,1)->1 xy, (0,2)->2 xz, (1,2)->3 yz
-    return s == 1 ? m[3] : (s == 2 ? m[4] : m[5]);
-}
-
-// 2.5-D streaming version: a CTA owns a 32 x 8 column of (x, y) and walks z through a slab.  Thread q
-// owns the raw point (x0 - 1 + q % 34, y0 - 1 + q / 34) of a 34 x 10 region and streams its z column in
-// registers: the values (P, w_x, w_y, w_z) of plane z + 1 are loaded one iteration ahead and those of
-// plane z + 2 issued before the current plane's work, so every value is read from global memory once per
-// CTA and its latency hides behind a plane of compute.  Per plane: the raw values of plane z go to a
-// shared plane (for the x + 1 / y + 1 neighbours of the fields), the 33 x 9 halo points compute the dphi
-// fields (n: 3, m: 6) from that plane and their own plane-(z + 1) registers, and the gradient of plane z is
-// a gather from field planes z and z - 1 (previous plane kept).
 constexpr int TGV_BX = 32, TGV_BY = 8, TGV_ZS = 32;
-constexpr int TGV_MINB = 4;  // 4 CTAs/SM (<= 46 registers): 0.22 vs 0.24 ms at 256^3 with 3 (52 registers)
 constexpr int TGV_RX = TGV_BX + 2, TGV_RY = TGV_BY + 2;               // raw region 34 x 10
 constexpr int TGV_NT = (TGV_RX * TGV_RY + 31) / 32 * 32;              // 352 threads
+constexpr int TGV_PX = TGV_BX + 1, TGV_PY = TGV_BY + 1;               // halo (field) points 33 x 9
+#ifndef TGV_MINB
+#define TGV_MINB 3
+#endif
 
-__global__ void __launch_bounds__(TGV_NT, TGV_MINB) k_tgv(TgvArgs t, const float *__restrict__ P,
-                                                const float *__restrict__ w, float *__restrict__ gP,
-                                                float *__restrict__ gw, double *__restrict__ part)
+// The dphi fields at a halo point of plane z (zero outside O): c = (P, w) at the point, rx / ry at its
+// x + 1 / y + 1 neighbours, c1 at z + 1.  Publishes the x- and y-rows; returns n, m and this point's value
+// terms a1 phi(g) + a0 phi(E) (0 outside O).
+struct TgvF {
+    float n0, n1, n2, mxx, myy, mzz, mxy, mxz, myz;
+};
+__device__ __forceinline__ TgvF tgv_fields(const TgvArgs &t, bool in, const float c[4], const float rx[4],
+                                           const float ry[4], const float c1[4], float &v)
 {
-    constexpr int PX = TGV_BX + 1, PY = TGV_BY + 1, NF = 9, NWT = TGV_NT / 32;
-    __shared__ float fld[2][NF][PY][PX];     // field planes: n0..2, m0..5 at (x - 1 .. x + 31, y - 1 .. y + 7)
-    __shared__ float raw[4][TGV_RY][TGV_RX];  // raw plane z: P, w_x, w_y, w_z at (x - 1 .. x + 32, y - 1 .. y + 8)
-    const int i = threadIdx.x % TGV_RX, j = threadIdx.x / TGV_RX;  // this thread's raw point
-    const int x0 = blockIdx.x * TGV_BX, y0 = blockIdx.y * TGV_BY, z0 = blockIdx.z * TGV_ZS;
-    const int x = x0 - 1 + i, y = y0 - 1 + j;
-    const bool rp = threadIdx.x < TGV_RX * TGV_RY;           // a raw point
-    const bool pt = rp && i < PX && j < PY;                  // a halo point (computes fields)
-    const bool own = pt && i >= 1 && j >= 1;                 // owns output voxel (x, y) and its value term
-    const int sz = t.nx * t.ny, nv = sz * t.nz;              // 3 nv < 2^31 (launch_tgv)
-    const bool inxy = rp && x >= 0 && y >= 0 && x < t.nx && y < t.ny;
-    const int kxy = inxy ? y * t.nx + x : 0;
-    double val = 0.0;
-    auto ld = [&](int z, float v[4]) {  // this column's raw values at plane z (0 outside the volume)
-        const bool ok = inxy && z >= 0 && z < t.nz;
-        const int k = z * sz + kxy;
-        v[0] = ok ? __ldg(P + k) : 0.0f;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) v[1 + c] = ok ? __ldg(w + c * nv + k) : 0.0f;
-    };
-    float cz[4] = {}, c1[4] = {}, c2[4] = {};  // the column at planes z, z + 1, z + 2
-    // fields at this halo point of plane z from raw plane z (shared) and the column's plane z + 1
-    auto fill = [&](int buf, int z, bool count) {
-        if (!pt) return;
-        float n[3] = {0.f, 0.f, 0.f}, m[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (tgv_in(t, x, y, z)) {
-            const float p = cz[0];
-            const float pn[3] = {raw[0][j][i + 1], raw[0][j + 1][i], c1[0]};
-            float D[3][3], g[3];
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-                D[0][b] = (raw[1 + b][j][i + 1] - cz[1 + b]) * t.inv_h;
-                D[1][b] = (raw[1 + b][j + 1][i] - cz[1 + b]) * t.inv_h;
-                D[2][b] = (c1[1 + b] - cz[1 + b]) * t.inv_h;
-            }
-#pragma unroll
-            for (int a = 0; a < 3; ++a) g[a] = (pn[a] - p) * t.inv_h - cz[1 + a];
-            // |v|_eps and 1/|v|_eps from one MUFU.RSQ
-            const float sg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + t.eps * t.eps;
-            const float ig = rsqrtf(sg), ng = sg * ig;
-            n[0] = g[0] * ig;
-            n[1] = g[1] * ig;
-            n[2] = g[2] * ig;
-            const float exx = D[0][0], eyy = D[1][1], ezz = D[2][2];
-            const float exy = 0.5f * (D[0][1] + D[1][0]), exz = 0.5f * (D[0][2] + D[2][0]), eyz = 0.5f * (D[1][2] + D[2][1]);
-            const float se = exx * exx + eyy * eyy + ezz * ezz + 2.0f * (exy * exy + exz * exz + eyz * eyz) + t.eps * t.eps;
-            const float ie = rsqrtf(se), ne = se * ie;
-            m[0] = exx * ie;
-            m[1] = eyy * ie;
-            m[2] = ezz * ie;
-            m[3] = exy * ie;
-            m[4] = exz * ie;
-            m[5] = eyz * ie;
-            // the value is counted once, by the owner of the interior point (i, j >= 1) in its own slab
-            if (own && count) val += (double)t.a1 * (ng - t.eps) + (double)t.a0 * (ne - t.eps);
-        }
-#pragma unroll
-        for (int f = 0; f < 3; ++f) fld[buf][f][j][i] = n[f];
-#pragma unroll
-        for (int f = 0; f < 6; ++f) fld[buf][3 + f][j][i] = m[f];
-    };
-    auto stage = [&]() {  // this column's plane-z values into the shared raw plane
-        if (rp) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) raw[c][j][i] = cz[c];
-        }
-    };
-    const int zend = min(z0 + TGV_ZS, t.nz);
-    // prologue: the plane below the slab (fields only: its value belongs to the slab below)
-    ld(z0 - 1, cz);
-    ld(z0, c1);
-    ld(z0 + 1, c2);
-    stage();
-    __syncthreads();
-    fill(0, z0 - 1, false);
-    int cur = 1;
-    for (int z = z0; z < zend; ++z) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            cz[c] = c1[c];
-            c1[c] = c2[c];
-        }
-        ld(z + 2, c2);   // two planes ahead: in flight during this plane
-        __syncthreads();  // raw plane z - 1 consumed (fill of z - 1 done by every thread)
-        stage();
-        __syncthreads();
-        fill(cur, z, true);
-        __syncthreads();
-        if (own && x < t.nx && y < t.ny) {
-            const int prv = cur ^ 1;
-            float gpv = 0.0f, gwv[3];
-            float m0[6], mx[6], my[6], mz[6];
-#pragma unroll
-            for (int f = 0; f < 6; ++f) {
-                m0[f] = fld[cur][3 + f][j][i];
-                mx[f] = fld[cur][3 + f][j][i - 1];
-                my[f] = fld[cur][3 + f][j - 1][i];
-                mz[f] = fld[prv][3 + f][j][i];
-            }
-            const float nxm = fld[cur][0][j][i - 1], nym = fld[cur][1][j - 1][i], nzm = fld[prv][2][j][i];
-            const float n00 = fld[cur][0][j][i], n01 = fld[cur][1][j][i], n02 = fld[cur][2][j][i];
-            gpv = t.a1 * t.inv_h * ((nxm - n00) + (nym - n01) + (nzm - n02));
-            const float nn[3] = {n00, n01, n02};
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                float s = 0.0f;
-                s += msym(mx, 0, d) - msym(m0, 0, d);
-                s += msym(my, 1, d) - msym(m0, 1, d);
-                s += msym(mz, 2, d) - msym(m0, 2, d);
-                gwv[d] = -t.a1 * nn[d] + t.a0 * t.inv_h * s;
-            }
-            const int k = z * sz + y * t.nx + x;
-            gP[k] = t.gs * gpv;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) gw[d * nv + k] = t.gs * gwv[d];
-        }
-        cur ^= 1;
-    }
-    // fixed-order block sum: shuffle tree per warp, then the warp partials in order
-    __shared__ double red[NWT];
+    TgvF F = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    v = 0.0f;
+    if (!in) return F;
+    const float h1 = t.inv_h, ee = t.eps * t.eps;
+    const float g0 = __fmaf_rn(rx[0] - c[0], h1, -c[1]);
+    const float g1 = __fmaf_rn(ry[0] - c[0], h1, -c[2]);
+    const float g2 = __fmaf_rn(c1[0] - c[0], h1, -c[3]);
+    // D[a][b] = d_a w_b
+    const float dxx = (rx[1] - c[1]) * h1, dxy = (rx[2] - c[2]) * h1, dxz = (rx[3] - c[3]) * h1;
+    const float dyx = (ry[1] - c[1]) * h1, dyy = (ry[2] - c[2]) * h1, dyz = (ry[3] - c[3]) * h1;
+    const float dzx = (c1[1] - c[1]) * h1, dzy = (c1[2] - c[2]) * h1, dzz = (c1[3] - c[3]) * h1;
+    const float sg = __fmaf_rn(g0, g0, __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, ee)));
+    const float ig = rsqrtf(sg);  // |v|_eps and 1/|v|_eps from one MUFU.RSQ
+    F.n0 = g0 * ig;
+    F.n1 = g1 * ig;
+    F.n2 = g2 * ig;
+    const float exy = 0.5f * (dxy + dyx), exz = 0.5f * (dxz + dzx), eyz = 0.5f * (dyz + dzy);
+    const float se = __fmaf_rn(dxx, dxx, __fmaf_rn(dyy, dyy, __fmaf_rn(dzz, dzz,
+                     __fmaf_rn(2.0f * exy, exy, __fmaf_rn(2.0f * exz, exz, __fmaf_rn(2.0f * eyz, eyz, ee))))));
+    const float ie = rsqrtf(se);
+    F.mxx = dxx * ie;
+    F.myy = dyy * ie;
+    F.mzz = dzz * ie;
+    F.mxy = exy * ie;
+    F.mxz = exz * ie;
+    F.myz = eyz * ie;
+    v = t.a1 * (sg * ig - t.eps) + t.a0 * (se * ie - t.eps);
+    return F;
+}
+
+// the gradient at an owned point k from its fields F, the -e_x / -e_y rows and the -e_z row pz
+__device__ __forceinline__ void tgv_grad(const TgvArgs &t, const TgvF &F, float4 fx, float4 fy, const float pz[4],
+                                         int k, int nv, float *__restrict__ gP, float *__restrict__ gw)
+{
+    const float ga = t.gs * t.a1 * t.inv_h, gb = t.gs * t.a0 * t.inv_h, gc = t.gs * t.a1;
+    gP[k] = ga * ((fx.x - F.n0) + (fy.x - F.n1) + (pz[0] - F.n2));
+    gw[k] = __fmaf_rn(-gc, F.n0, gb * ((fx.y - F.mxx) + (fy.y - F.mxy) + (pz[1] - F.mxz)));
+    gw[nv + k] = __fmaf_rn(-gc, F.n1, gb * ((fx.z - F.mxy) + (fy.z - F.myy) + (pz[2] - F.myz)));
+    gw[2 * nv + k] = __fmaf_rn(-gc, F.n2, gb * ((fx.w - F.mxz) + (fy.w - F.myz) + (pz[3] - F.mzz)));
+}
+
+// fixed-order block sum of the value: shuffle tree per warp, then the warp partials in order
+__device__ __forceinline__ void tgv_block_value(double val, double *red, double *__restrict__ part)
+{
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) val += __shfl_down_sync(0xffffffffu, val, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = val;
     __syncthreads();
     if (threadIdx.x == 0) {
         double s2 = 0.0;
-        for (int q = 0; q < NWT; ++q) s2 += red[q];
+        for (int q = 0; q < TGV_NT / 32; ++q) s2 += red[q];
         part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s2;
     }
+}
+
+__global__ void __launch_bounds__(TGV_NT, 2) k_tgv(TgvArgs t, const float *__restrict__ P,
+                                                const float *__restrict__ w, float *__restrict__ gP,
+                                                float *__restrict__ gw, double *__restrict__ part)
+{
+    __shared__ float raw[4][TGV_RY][TGV_RX];  // raw plane z: P, w_x, w_y, w_z at (x - 1 .. x + 32, y - 1 .. y + 8)
+    __shared__ float4 fxr[TGV_PY][TGV_PX];    // x-row of the fields: (n_x, m_xx, m_xy, m_xz)
+    __shared__ float4 fyr[TGV_PY][TGV_PX];    // y-row of the fields: (n_y, m_xy, m_yy, m_yz)
+    __shared__ double red[TGV_NT / 32];
+    const int i = threadIdx.x % TGV_RX, j = threadIdx.x / TGV_RX;  // this thread's raw point
+    const int x0 = blockIdx.x * TGV_BX, y0 = blockIdx.y * TGV_BY, z0 = blockIdx.z * TGV_ZS;
+    const int x = x0 - 1 + i, y = y0 - 1 + j;
+    const bool rp = threadIdx.x < TGV_RX * TGV_RY;           // a raw point
+    const bool pt = rp && i < TGV_PX && j < TGV_PY;          // a halo point (computes fields)
+    const int sz = t.nx * t.ny, nv = sz * t.nz;              // 3 nv < 2^31 (tgv_args)
+    const bool own = pt && i >= 1 && j >= 1 && x < t.nx && y < t.ny;  // owns output voxel (x, y)
+    const bool inxy = rp && x >= 0 && y >= 0 && x < t.nx && y < t.ny;
+    const bool fxy = x >= 0 && y >= 0 && x <= t.nx - 2 && y <= t.ny - 2;  // interior in x, y
+    const int kxy = inxy ? y * t.nx + x : 0;
+    const int zbeg = z0 - 1, zend = min(z0 + TGV_ZS, t.nz);
+    double val = 0.0;
+    auto ld = [&](int z, float v[4]) {  // this column's raw values at plane z (0 outside the volume / past the slab)
+        const bool ok = inxy && z >= 0 && z < t.nz && z <= zend;
+        const int k = z * sz + kxy;
+        v[0] = ok ? __ldg(P + k) : 0.0f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[1 + c] = ok ? __ldg(w + c * nv + k) : 0.0f;
+    };
+    float pz[4] = {0.f, 0.f, 0.f, 0.f};  // n_z, m_xz, m_yz, m_zz of the previous plane at this point
+    auto plane = [&](int z, const float cz[4], const float c1[4]) {
+        if (rp) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) raw[c][j][i] = cz[c];
+        }
+        __syncthreads();  // raw plane z published (and the previous plane's field rows consumed)
+        TgvF F = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (pt) {
+            const bool in = fxy && z >= 0 && z <= t.nz - 2;
+            float rx[4], ry[4], v;
+            if (in) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    rx[c] = raw[c][j][i + 1];
+                    ry[c] = raw[c][j + 1][i];
+                }
+            }
+            F = tgv_fields(t, in, cz, rx, ry, c1, v);
+            if (own && z >= z0) val += (double)v;  // counted once, by the owner, in its own slab
+            fxr[j][i] = make_float4(F.n0, F.mxx, F.mxy, F.mxz);
+            fyr[j][i] = make_float4(F.n1, F.mxy, F.myy, F.myz);
+        }
+        __syncthreads();  // field rows of plane z published (and raw plane z consumed)
+        if (own && z >= z0) tgv_grad(t, F, fxr[j][i - 1], fyr[j - 1][i], pz, z * sz + kxy, nv, gP, gw);
+        pz[0] = F.n2;
+        pz[1] = F.mxz;
+        pz[2] = F.myz;
+        pz[3] = F.mzz;
+    };
+    // four column buffers rotated by name (unrolled by 4: no register move waits on a load in flight), each
+    // refilled right after its plane is done — planes z + 1 .. z + 3 are in flight during plane z
+    float b0[4], b1[4], b2[4], b3[4];
+    ld(zbeg, b0);
+    ld(zbeg + 1, b1);
+    ld(zbeg + 2, b2);
+    ld(zbeg + 3, b3);
+    for (int z = zbeg; z < zend; z += 4) {
+        plane(z, b0, b1);
+        ld(z + 4, b0);
+        if (z + 1 >= zend) break;
+        plane(z + 1, b1, b2);
+        ld(z + 5, b1);
+        if (z + 2 >= zend) break;
+        plane(z + 2, b2, b3);
+        ld(z + 6, b2);
+        if (z + 3 >= zend) break;
+        plane(z + 3, b3, b0);
+        ld(z + 7, b3);
+    }
+    tgv_block_value(val, red, part);
+}
+
+// ---- TMA-staged variant ------------------------------------------------------------------------------
+#ifndef TGV_STAGES
+#define TGV_STAGES 6
+#endif
+// TMA box: x0 - 4 .. x0 + 35 (the innermost start coordinate must be a multiple of 16 B, so not x0 - 1;
+// raw column i of the thread grid is box column i + 3), y0 - 1 .. y0 + 8
+constexpr int TGV_BOXX = 40, TGV_BOX0 = 3;
+constexpr int TGV_PLN = TGV_BOXX * TGV_RY;                      // floats of one channel plane (400)
+constexpr int TGV_WOFF = 416;                                   // w boxes after the P box (1600 B padded to 1664)
+constexpr int TGV_STAGE_F = TGV_WOFF + 1216;                    // w boxes (4800 B) padded to 4864: 6528 B per stage
+constexpr unsigned TGV_TX_BYTES = 4u * 4u * TGV_PLN;            // bytes a stage receives (6400)
+constexpr size_t tgv_tma_smem() { return (size_t)TGV_STAGES * TGV_STAGE_F * 4 + 2 * 2 * TGV_PY * TGV_PX * 16 + 128; }
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned n)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TGV_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TGV_WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_3d(float *dst, const void *tm, int x, int y, int z, uint64_t *b)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)), "l"(tm), "r"(x), "r"(y), "r"(z), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ void tma_4d(float *dst, const void *tm, int x, int y, int z, int c, uint64_t *b)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+            "r"(smem_u32(dst)), "l"(tm), "r"(x), "r"(y), "r"(z), "r"(c), "r"(smem_u32(b))
+        : "memory");
+}
+
+// tmP: P as {nx, ny, nz} fp32, box {40, 10, 1};  tmW: w as {nx, ny, nz, 3}, box {40, 10, 1, 3}.
+// (Measured alternative: two raw rows per thread — the y + 1 neighbour of the first point is the second —
+// 192 threads per CTA: 0.19 vs 0.178 ms at 256^3.)
+__global__ void __launch_bounds__(TGV_NT, TGV_MINB) k_tgv_tma(TgvArgs t, const __grid_constant__ CUtensorMap tmP,
+                                                    const __grid_constant__ CUtensorMap tmW,
+                                                    float *__restrict__ gP, float *__restrict__ gw,
+                                                    double *__restrict__ part)
+{
+    extern __shared__ __align__(128) float tsm_[];
+    // TMA destinations 128-B aligned whatever the dynamic base (tgv_tma_smem() has 128 B of slack)
+    float *tsm = tsm_ + ((128u - (smem_u32(tsm_) & 127u)) & 127u) / 4;
+    float *stg = tsm;                                                          // [S][TGV_STAGE_F]
+    float4 *frows = reinterpret_cast<float4 *>(tsm + TGV_STAGES * TGV_STAGE_F); // [2 planes][X, Y][PY][PX]
+    __shared__ __align__(8) uint64_t full[TGV_STAGES];
+    __shared__ double red[TGV_NT / 32];
+    const int i = threadIdx.x % TGV_RX, j = threadIdx.x / TGV_RX;
+    const int x0 = blockIdx.x * TGV_BX, y0 = blockIdx.y * TGV_BY, z0 = blockIdx.z * TGV_ZS;
+    const int x = x0 - 1 + i, y = y0 - 1 + j;
+    const bool rp = threadIdx.x < TGV_RX * TGV_RY;
+    const bool pt = rp && i < TGV_PX && j < TGV_PY;
+    const int sz = t.nx * t.ny, nv = sz * t.nz;
+    const bool own = pt && i >= 1 && j >= 1 && x < t.nx && y < t.ny;
+    const bool fxy = x >= 0 && y >= 0 && x <= t.nx - 2 && y <= t.ny - 2;
+    const int kxy = (x >= 0 && y >= 0) ? y * t.nx + x : 0;
+    const int zbeg = z0 - 1, zend = min(z0 + TGV_ZS, t.nz), nq = zend - zbeg;  // planes zbeg .. zend (nq + 1)
+    const int o = j * TGV_BOXX + i + TGV_BOX0;                                   // this point in a box plane
+    auto issue = [&](int q) {  // plane zbeg + q into stage q % S (one thread)
+        float *d = stg + (q % TGV_STAGES) * TGV_STAGE_F;
+        uint64_t *b = &full[q % TGV_STAGES];
+        mbar_expect_tx(b, TGV_TX_BYTES);
+        tma_3d(d, &tmP, x0 - 4, y0 - 1, zbeg + q, b);
+        tma_4d(d + TGV_WOFF, &tmW, x0 - 4, y0 - 1, zbeg + q, 0, b);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TGV_STAGES; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int q = 0; q < TGV_STAGES && q <= nq; ++q) issue(q);
+    double val = 0.0;
+    float pz[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int q = 0; q < nq; ++q) {
+        const int z = zbeg + q;
+        const float *s0 = stg + (q % TGV_STAGES) * TGV_STAGE_F, *s1 = stg + ((q + 1) % TGV_STAGES) * TGV_STAGE_F;
+        float4 *fx = frows + (q & 1) * 2 * TGV_PY * TGV_PX, *fy = fx + TGV_PY * TGV_PX;
+        mbar_wait(&full[q % TGV_STAGES], (unsigned)(q / TGV_STAGES) & 1u);
+        mbar_wait(&full[(q + 1) % TGV_STAGES], (unsigned)((q + 1) / TGV_STAGES) & 1u);
+        TgvF F = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (pt) {
+            const bool in = fxy && z >= 0 && z <= t.nz - 2;
+            float c[4], c1[4], rx[4], ry[4], v;
+            if (in) {
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int co = cc == 0 ? 0 : TGV_WOFF + (cc - 1) * TGV_PLN;
+                    const float *a = s0 + co, *a1 = s1 + co;
+                    c[cc] = a[o];
+                    rx[cc] = a[o + 1];
+                    ry[cc] = a[o + TGV_BOXX];
+                    c1[cc] = a1[o];
+                }
+            }
+            F = tgv_fields(t, in, c, rx, ry, c1, v);
+            if (own && z >= z0) val += (double)v;  // counted once, by the owner, in its own slab
+            fx[j * TGV_PX + i] = make_float4(F.n0, F.mxx, F.mxy, F.mxz);
+            fy[j * TGV_PX + i] = make_float4(F.n1, F.mxy, F.myy, F.myz);
+        }
+        __syncthreads();  // field rows of plane z published; stage q consumed by every thread
+        if (threadIdx.x == 0 && q + TGV_STAGES <= nq) issue(q + TGV_STAGES);
+        if (own && z >= z0) tgv_grad(t, F, fx[j * TGV_PX + i - 1], fy[(j - 1) * TGV_PX + i], pz, z * sz + kxy, nv, gP, gw);
+        pz[0] = F.n2;
+        pz[1] = F.mxz;
+        pz[2] = F.myz;
+        pz[3] = F.mzz;
+    }
+    tgv_block_value(val, red, part);
 }
 
 }  // namespace pa

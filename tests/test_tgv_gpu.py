@@ -34,7 +34,10 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("shape", [(13, 19, 21), (2, 2, 2), (32, 32, 32), (1, 5, 7), (70, 9, 11), (33, 12, 40)])  # nz > 32: several z slabs
+# nz > 32: several z slabs; nx % 4 == 0 runs the TMA-staged kernel (k_tgv_tma), other widths the
+# register-streamed k_tgv
+@pytest.mark.parametrize("shape", [(13, 19, 21), (2, 2, 2), (32, 32, 32), (1, 5, 7), (70, 9, 11), (33, 12, 40),
+                                   (70, 9, 12), (5, 3, 4), (40, 17, 68)])
 def test_tgv_parity(ctx, shape, record_parity):
     rng = np.random.default_rng(sum(shape))
     grid = gen.make_grid(shape[::-1], 0.2)
