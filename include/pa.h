@@ -59,7 +59,7 @@ typedef enum {
     PA_ECUDA = 4,         /* a CUDA call or launch failed                                     */
     PA_ENOMEM = 5,        /* workspace allocation failed                                      */
     PA_EUNSUPPORTED = 6   /* geometry outside every kernel (see pa_get_plan_info): the Gaussian
-                             fast path runs any L_min = floor(2 kappa sigma/(c dt)) in [21, 256]
+                             fast path runs any L_min = floor(2 kappa sigma/(c dt)) in [21, 512]
                              (nt + L_min row accumulators permitting); the direct kernels (the
                              exponential and power-law families; shorter Gaussian windows) run
                              spread <= L_min < 160 with L_min + spread <= 128, spread =

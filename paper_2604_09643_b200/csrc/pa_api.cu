@@ -524,7 +524,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
                     "kernels need spread <= L_min, L_min + cluster spread <= 128, L_min < 160 and a tile span <= 128 (cluster spread %d, "
                     "tile span %d, segment %d)",
                     wmin, K2, pl.fam,
-                    !fast ? "outside the Gaussian fast path (Gaussian kernel, 21 <= L_min <= 256)"
+                    !fast ? "outside the Gaussian fast path (Gaussian kernel, 21 <= L_min <= 512)"
                           : (!pl.fwd_dep ? "the deposit forward is unavailable or not selected"
                                          : "the moment-filter adjoints are unavailable or not selected"),
                     o_need, span_need, seg_need);

@@ -1022,7 +1022,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 2) k_adjoint(Geo g, AdjConst ac, 
 // sides, so every pair of a non-culled (tile, element) — and every pair of a culled one, through a
 // sentinel anchor — addresses a valid position: no per-pair bounds checks (windows outside [0, nt)
 // read zeros).
-constexpr int PA_LMAX = 256;  // longest window (L_min) of the Gaussian fast path (K1d, K2a/K2c, K2s)
+constexpr int PA_LMAX = 512;  // longest window (L_min) of the Gaussian fast path (K1d, K2a/K2c, K2s)
 template <int NF_>
 struct TayCfg {
     static constexpr int NF = NF_;       // floats per record (32 / 48 B)
@@ -2137,7 +2137,13 @@ struct TgvArgs {
     float gs;  // scale of both gradients (lambda of Eq. 2 inside pa_step, 1 for pa_tgv)
 };
 
-constexpr int TGV_BX = 32, TGV_BY = 8, TGV_ZS = 32;
+#ifndef TGV_BYM
+#define TGV_BYM 8
+#endif
+#ifndef TGV_ZSM
+#define TGV_ZSM 32
+#endif
+constexpr int TGV_BX = 32, TGV_BY = TGV_BYM, TGV_ZS = TGV_ZSM;
 constexpr int TGV_RX = TGV_BX + 2, TGV_RY = TGV_BY + 2;               // raw region 34 x 10
 constexpr int TGV_NT = (TGV_RX * TGV_RY + 31) / 32 * 32;              // 352 threads
 constexpr int TGV_PX = TGV_BX + 1, TGV_PY = TGV_BY + 1;               // halo (field) points 33 x 9
@@ -2297,8 +2303,8 @@ __global__ void __launch_bounds__(TGV_NT, 2) k_tgv(TgvArgs t, const float *__res
 // raw column i of the thread grid is box column i + 3), y0 - 1 .. y0 + 8
 constexpr int TGV_BOXX = 40, TGV_BOX0 = 3;
 constexpr int TGV_PLN = TGV_BOXX * TGV_RY;                      // floats of one channel plane (400)
-constexpr int TGV_WOFF = 416;                                   // w boxes after the P box (1600 B padded to 1664)
-constexpr int TGV_STAGE_F = TGV_WOFF + 1216;                    // w boxes (4800 B) padded to 4864: 6528 B per stage
+constexpr int TGV_WOFF = (TGV_PLN + 31) / 32 * 32;              // w boxes after the P box (padded to 128 B)
+constexpr int TGV_STAGE_F = TGV_WOFF + (3 * TGV_PLN + 31) / 32 * 32;  // + the w boxes (padded): 6528 B per stage at BY = 8
 constexpr unsigned TGV_TX_BYTES = 4u * 4u * TGV_PLN;            // bytes a stage receives (6400)
 constexpr size_t tgv_tma_smem() { return (size_t)TGV_STAGES * TGV_STAGE_F * 4 + 2 * 2 * TGV_PY * TGV_PX * 16 + 128; }
 

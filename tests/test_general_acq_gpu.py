@@ -2,7 +2,7 @@
 Gaussian width sigma and the cut-off kappa are free parameters of Eq. gpu_forward_model; the
 paper's dynamic smoothing decays sigma continuously (Alg. 1).  The Gaussian fast path (K1d,
 K2a/K2c, K2s) takes the window length L_min = floor(2 kappa sigma / (c dt)) at run time, so any such
-acquisition with 21 <= L_min <= 256 runs.  Each case: forward, adjoint and pose gradient vs
+acquisition with 21 <= L_min <= 512 runs.  Each case: forward, adjoint and pose gradient vs
 the fp64 oracle on a ragged multi-tile grid, several frames, windows clipped at both ends."""
 import numpy as np
 import pytest
@@ -25,6 +25,9 @@ CASES = {
     "sigma0.5": (0.2, dict(sigma=0.5), 133),
     "sigma0.6": (0.2, dict(sigma=0.6), 160),
     "sigma0.9": (0.2, dict(sigma=0.9), 239),
+    "sigma1.0": (0.2, dict(sigma=1.0), 266),
+    "sigma1.6_h0.8": (0.8, dict(sigma=1.6), 426),
+    "sigma1.9": (0.2, dict(sigma=1.9), 506),
     "sigma0.08_h0.1": (0.1, dict(sigma=0.08), 21),
     "c1.54_fs50_kappa6_s0.22": (0.2, dict(c=1.54, dt=0.02, kappa=6.0, sigma=0.22), 85),
 }
