@@ -63,7 +63,8 @@ typedef enum {
                              (nt + L_min row accumulators permitting); the direct kernels (the
                              exponential and power-law families; shorter Gaussian windows) run
                              spread <= L_min < 160 with L_min + spread <= 128, spread =
-                             floor(sqrt(3) pitch/(c dt)) + 2                                  */
+                             floor(sqrt(3) pitch/(c dt)) + 2; every other window runs the generic
+                             kernels (any L_min and family, nt <= 51200); TGV 3 nx ny nz < 2^31 */
 } pa_status;
 
 /* Voxel grid.  Voxel (i,j,l) centre = origin + pitch*(i,j,l); p0[l][j][i]. */
@@ -103,7 +104,8 @@ void pa_destroy(pa_ctx *ctx);
 /* Kernel-selection policy of a context (default 0: the fastest kernels the geometry supports,
  * DESIGN.md §6).  Bits force the alternatives, for tests and diagnostics: the direct forward K1,
  * the direct adjoint K2, or prefer the rank-R-basis adjoint K2s / the moment-filter adjoint K2c.
- * A forced kernel that the geometry does not support makes the calls return PA_EUNSUPPORTED.
+ * A forced direct kernel whose window class does not hold the geometry runs as the generic kernels
+ * (K1g / K2g + K3g); a preferred adjoint that is unavailable falls back to the default choice.
  * Unknown bits -> PA_EINVAL.  The policy is per context (no global state). */
 enum {
     PA_POLICY_DEFAULT = 0,
@@ -256,6 +258,7 @@ typedef struct {
     int32_t direct_class;/* direct kernels (K1/K2): L_min of the compiled class, or -capacity of the
                             runtime class (L_min + cluster spread <= capacity), 0 if none fits     */
     int32_t dep_round;   /* K1d: tiles per warp per round (8 when its ring keeps the CTAs per SM, else 4) */
+    int32_t generic;     /* 1: a pass runs the generic kernels K1g / K2g+K3g (no direct class holds L_min) */
 } pa_plan_info;
 pa_status pa_get_plan_info(const pa_grid *grid, const pa_acq *acq, int32_t E, pa_plan_info *out);
 /* The same for a context (its pa_set_policy applied). */

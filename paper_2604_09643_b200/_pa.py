@@ -32,7 +32,7 @@ class PlanInfo(ctypes.Structure):
                 ("tay_order", ctypes.c_int32), ("tay_err", ctypes.c_double), ("adj_svd", ctypes.c_int32),
                 ("svd_derr", ctypes.c_double), ("dep_groups", ctypes.c_int32), ("dep_ring", ctypes.c_int32),
                 ("adj_kernel", ctypes.c_int32), ("direct_class", ctypes.c_int32),
-                ("dep_round", ctypes.c_int32)]
+                ("dep_round", ctypes.c_int32), ("generic", ctypes.c_int32)]
 
 
 def plan_info(grid, acq, E: int) -> dict:

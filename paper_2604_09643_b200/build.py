@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SRC = [os.path.join(CSRC, f) for f in ("pa_api.cu", "k_dep.cu", "k_tay.cu", "k_svd.cu", "k_direct_gauss.cu",
-                                       "k_direct_exp.cu", "k_direct_pow.cu")]
+                                       "k_direct_exp.cu", "k_direct_pow.cu", "k_generic.cu")]
 HDRS = [os.path.join(CSRC, f) for f in ("pa_kernels.cuh", "pa_plan.h", "k_direct_impl.cuh")] + \
     [os.path.join(ROOT, "include", "pa.h")]
 DEPS = SRC + HDRS

@@ -518,16 +518,15 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     else if (tay_avail) pl.adj = ADJ_TAY;
     else if (svd_avail) pl.adj = ADJ_SVD;
     else pl.adj = ADJ_DIRECT;
-    if ((!pl.fwd_dep || pl.adj == ADJ_DIRECT) && pl.klass < 0)
-        return fail(PA_EUNSUPPORTED,
-                    "no kernel for this geometry: L_min=%d (2 kappa sigma/(c dt)=%.4f), kernel family %d, %s; the direct "
-                    "kernels need spread <= L_min, L_min + cluster spread <= 128, L_min < 160 and a tile span <= 128 (cluster spread %d, "
-                    "tile span %d, segment %d)",
-                    wmin, K2, pl.fam,
-                    !fast ? "outside the Gaussian fast path (Gaussian kernel, 21 <= L_min <= 512)"
-                          : (!pl.fwd_dep ? "the deposit forward is unavailable or not selected"
-                                         : "the moment-filter adjoints are unavailable or not selected"),
-                    o_need, span_need, seg_need);
+    // no direct-kernel class holds the geometry: the direct passes run the generic kernels K1g/K2g/K3g (any
+    // window length and family; K1g keeps nw warp traces of nt floats in shared memory)
+    pl.gen = pl.klass < 0;
+    pl.gen_dt = (double)acq->dt;
+    pl.gen_sig = sig;
+    pl.gen_nw = std::max(1, std::min(8, (int)((200 * 1024) / ((size_t)g.nt * sizeof(float)))));
+    if (pl.gen && (!pl.fwd_dep || pl.adj == ADJ_DIRECT) && (size_t)g.nt * sizeof(float) > 200 * 1024)
+        return fail(PA_EUNSUPPORTED, "no kernel for this geometry: L_min=%d, nt=%d samples exceed the generic forward's "
+                                     "shared-memory trace (nt <= 51200)", wmin, g.nt);
     return PA_OK;
 }
 
@@ -989,6 +988,7 @@ pa_status launch_forward(pa_ctx *ctx, const Plan &pl, const float *poses, const 
                          int mode, const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st)
 {
     if (pl.fwd_dep) return launch_forward_dep(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    if (pl.gen) return launch_forward_generic(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
     return launch_forward_direct(pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
 }
 
@@ -999,7 +999,9 @@ pa_status launch_adjoint(pa_ctx *ctx, const Plan &pl, bool pose, bool adj, const
     switch (pl.adj) {
     case ADJ_TAY: return launch_adjoint_tay(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
     case ADJ_SVD: return launch_adjoint_svd(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
-    default: return launch_adjoint_direct(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+    default:
+        if (pl.gen) return launch_adjoint_generic(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
+        return launch_adjoint_direct(ctx, pl, pose, adj, poses, tmpl, p0, cot, grad_p0, partial, L, dry, st);
     }
 }
 
@@ -1483,6 +1485,7 @@ static void fill_info(const Plan &pl, pa_plan_info *out)
     out->dep_groups = pl.dep_g;
     out->dep_ring = pl.dc.nr;
     out->dep_round = pl.dep_tpr;
+    out->generic = (pl.gen && (!pl.fwd_dep || pl.adj == ADJ_DIRECT)) ? 1 : 0;
     out->adj_kernel = pl.adj;
     out->direct_class = pl.klass < 0 ? 0 : (pl.klass >= KLASS_RT ? -kRtClasses[pl.klass - KLASS_RT].rc : kClasses[pl.klass].lmin);
 }

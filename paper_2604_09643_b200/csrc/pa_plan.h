@@ -63,8 +63,11 @@ struct Plan {
     int klass;        // direct-kernel class (index into kClasses) or -1
     int fam;          // pa_kernel (KF_*)
     int policy;       // PA_POLICY_* bits
-    bool fwd_dep;     // the forward runs K1d (else the direct K1)
-    int adj;          // the adjoint: ADJ_TAY (K2a/K2c), ADJ_SVD (K2s) or ADJ_DIRECT (K2)
+    bool fwd_dep;     // the forward runs K1d (else the direct K1, or K1g when no direct class holds it)
+    int adj;          // the adjoint: ADJ_TAY (K2a/K2c), ADJ_SVD (K2s) or ADJ_DIRECT (K2, or K2g/K3g)
+    bool gen;         // no direct-kernel class holds the geometry: the direct passes run the generic K1g/K2g/K3g
+    int gen_nw;       // K1g warps per CTA (warp-private traces of nt floats in shared memory)
+    double gen_dt, gen_sig;  // fp64 copies of dt and sigma for the generic kernels' literal window predicate
 };
 enum { ADJ_DIRECT = 0, ADJ_TAY = 1, ADJ_SVD = 2 };
 
@@ -97,6 +100,12 @@ pa_status launch_adjoint_svd(pa_ctx *ctx, const Plan &pl, bool pose, bool adj, c
 pa_status launch_adjoint_direct(pa_ctx *ctx, const Plan &pl, bool pose, bool adj, const float *poses,
                                 const float *tmpl, const float *p0, const float *cot, float *grad_p0, float *partial,
                                 AdjLaunch &L, bool dry, cudaStream_t st);
+// generic kernels (k_generic.cu): any window length and family, literal window predicate, fp64 geometry
+pa_status launch_forward_generic(const Plan &pl, const float *poses, const float *tmpl, const float *p0, float *out,
+                                 int mode, const float *meas, const uint8_t *mask, double *rowloss, cudaStream_t st);
+pa_status launch_adjoint_generic(pa_ctx *ctx, const Plan &pl, bool pose, bool adj, const float *poses,
+                                 const float *tmpl, const float *p0, const float *cot, float *grad_p0, float *partial,
+                                 AdjLaunch &L, bool dry, cudaStream_t st);
 // family-specific direct launchers (k_direct_<family>.cu)
 pa_status launch_forward_direct_gauss(const Plan &, const float *, const float *, const float *, float *, int,
                                       const float *, const uint8_t *, double *, cudaStream_t);

@@ -88,11 +88,12 @@ def test_other_families_use_direct_forward():
     ("gauss", 0.2, 5.0, 0.2, ("fast", 53)), ("gauss", 0.6, 5.0, 0.2, ("fast", 160)), ("gauss", 0.9, 5.0, 0.2, ("fast", 239)),
     ("gauss", 0.05, 5.0, 0.2, ("direct_rt", 13)), ("exp", 0.075, 10.0, 0.2, ("direct_rt", 40)),
     ("exp", 0.1, 10.0, 0.2, ("direct", 53)), ("pow", 0.15, 10.0, 0.2, ("direct_rt", 80)),
-    ("exp", 0.3, 30.0, 0.2, ("unsupported", 480)), ("pow", 0.5, 10.0, 0.2, ("unsupported", 266))])
+    ("exp", 0.3, 30.0, 0.2, ("generic", 480)), ("pow", 0.5, 10.0, 0.2, ("generic", 266)),
+    ("gauss", 2.0, 5.0, 0.2, ("generic", 533)), ("gauss", 0.02, 5.0, 0.2, ("generic", 5))])
 def test_kernel_selection_over_window_lengths(kernel, s, kappa, pitch, want):
-    """R26: which kernels a window length runs (host-only plan): the Gaussian fast path for 21 <= L_min <= 256, the
+    """R26: which kernels a window length runs (host-only plan): the Gaussian fast path for 21 <= L_min <= 512, the
     compiled direct classes for L_min in {26, 53, 106}, runtime direct classes when spread <= L_min and
-    L_min + spread <= 128, PA_EUNSUPPORTED beyond."""
+    L_min + spread <= 128, the generic kernels K1g/K2g/K3g for every other window."""
     from paper_2604_09643_b200._pa import PAError, PA_EUNSUPPORTED
 
     grid = gen.make_grid((32, 32, 32), pitch)
@@ -105,10 +106,13 @@ def test_kernel_selection_over_window_lengths(kernel, s, kappa, pitch, want):
         return
     info = plan_info(grid, acq, 16)
     assert info["lmin"] == lmin, info
+    assert info["generic"] == (kind == "generic"), info
     if kind == "fast":
         assert info["fwd_deposit"] == 1 and info["adj_kernel"] in (1, 2), info
     elif kind == "direct":
         assert info["fwd_deposit"] == 0 and info["adj_kernel"] == 0 and info["direct_class"] == lmin, info
+    elif kind == "generic":
+        assert info["fwd_deposit"] == 0 and info["adj_kernel"] == 0 and info["direct_class"] == 0, info
     else:
         assert info["fwd_deposit"] == 0 and info["adj_kernel"] == 0 and info["direct_class"] < 0, info
         spread = int(np.floor(np.sqrt(3.0) * pitch / (C_MM_US * DT))) + 2
