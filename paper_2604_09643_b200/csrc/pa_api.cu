@@ -1075,7 +1075,7 @@ bool tgv_tensor_maps(const TgvArgs &t, const float *P, const float *w, CUtensorM
     const cuuint64_t nx = t.nx, ny = t.ny, nz = t.nz;
     const cuuint64_t dims[4] = {nx, ny, nz, 3};
     const cuuint64_t strides[3] = {nx * 4, nx * ny * 4, nx * ny * nz * 4};
-    const cuuint32_t box[4] = {(cuuint32_t)TGV_BOXX, (cuuint32_t)TGV_RY, 1, 3};
+    const cuuint32_t box[4] = {(cuuint32_t)TGV_BOXX, (cuuint32_t)TGV_TRY, 1, 3};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     if (enc(&mP, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(P), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1099,9 +1099,10 @@ pa_status launch_tgv(const TgvArgs &t, const float *P, const float *w, float *gP
     CUtensorMap mP, mW;
     ++g_nlaunch;
     if (PA_TGV_TMA && tgv_tensor_maps(t, P, w, mP, mW)) {
+        gd.y = (t.ny + TGV_TBY - 1) / TGV_TBY;  // <= the parts of the register-streamed grid (TGV_TBY >= TGV_BY)
         const size_t smem = tgv_tma_smem();
         CUDA_TRY(cudaFuncSetAttribute(k_tgv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_tgv_tma<<<gd, TGV_NT, smem, st>>>(t, mP, mW, gP, gw, part);
+        k_tgv_tma<<<gd, TGV2_NT, smem, st>>>(t, mP, mW, gP, gw, part);
     } else {
         k_tgv<<<gd, TGV_NT, 0, st>>>(t, P, w, gP, gw, part);
     }

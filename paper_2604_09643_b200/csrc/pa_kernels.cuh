@@ -2148,7 +2148,7 @@ constexpr int TGV_RX = TGV_BX + 2, TGV_RY = TGV_BY + 2;               // raw reg
 constexpr int TGV_NT = (TGV_RX * TGV_RY + 31) / 32 * 32;              // 352 threads
 constexpr int TGV_PX = TGV_BX + 1, TGV_PY = TGV_BY + 1;               // halo (field) points 33 x 9
 #ifndef TGV_MINB
-#define TGV_MINB 3
+#define TGV_MINB 2  // resident k_tgv_tma CTAs per SM (18 warps each at 16 rows)
 #endif
 
 // The dphi fields at a halo point of plane z (zero outside O): c = (P, w) at the point, rx / ry at its
@@ -2302,11 +2302,16 @@ __global__ void __launch_bounds__(TGV_NT, 2) k_tgv(TgvArgs t, const float *__res
 // TMA box: x0 - 4 .. x0 + 35 (the innermost start coordinate must be a multiple of 16 B, so not x0 - 1;
 // raw column i of the thread grid is box column i + 3), y0 - 1 .. y0 + 8
 constexpr int TGV_BOXX = 40, TGV_BOX0 = 3;
-constexpr int TGV_PLN = TGV_BOXX * TGV_RY;                      // floats of one channel plane (400)
+#ifndef TGV_TBYM
+#define TGV_TBYM 16  // 32 x 16 outputs per CTA (256^3: 0.151 ms; 8 rows 0.158, 12 rows 0.163, 24 rows 0.171)
+#endif
+constexpr int TGV_TBY = TGV_TBYM;                               // k_tgv_tma: outputs per CTA in y (>= TGV_BY)
+constexpr int TGV_TRY = TGV_TBY + 2, TGV_TPY = TGV_TBY + 1;     // box rows, halo (field) rows
+constexpr int TGV_PLN = TGV_BOXX * TGV_TRY;                     // floats of one channel plane (400 at 8 rows)
 constexpr int TGV_WOFF = (TGV_PLN + 31) / 32 * 32;              // w boxes after the P box (padded to 128 B)
 constexpr int TGV_STAGE_F = TGV_WOFF + (3 * TGV_PLN + 31) / 32 * 32;  // + the w boxes (padded): 6528 B per stage at BY = 8
 constexpr unsigned TGV_TX_BYTES = 4u * 4u * TGV_PLN;            // bytes a stage receives (6400)
-constexpr size_t tgv_tma_smem() { return (size_t)TGV_STAGES * TGV_STAGE_F * 4 + 2 * 2 * TGV_PY * TGV_PX * 16 + 128; }
+constexpr size_t tgv_tma_smem() { return (size_t)TGV_STAGES * TGV_STAGE_F * 4 + 2 * 2 * TGV_TPY * TGV_PX * 16 + 128; }
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *b, unsigned n)
@@ -2343,12 +2348,17 @@ __device__ __forceinline__ void tma_4d(float *dst, const void *tm, int x, int y,
 }
 
 // tmP: P as {nx, ny, nz} fp32, box {40, 10, 1};  tmW: w as {nx, ny, nz, 3}, box {40, 10, 1, 3}.
-// (Measured alternative: two raw rows per thread — the y + 1 neighbour of the first point is the second —
-// 192 threads per CTA: 0.19 vs 0.178 ms at 256^3.)
-__global__ void __launch_bounds__(TGV_NT, TGV_MINB) k_tgv_tma(TgvArgs t, const __grid_constant__ CUtensorMap tmP,
-                                                    const __grid_constant__ CUtensorMap tmW,
-                                                    float *__restrict__ gP, float *__restrict__ gw,
-                                                    double *__restrict__ part)
+// Threads only for the 33 x (TBY + 1) halo points (the raw planes arrive by TMA): warp w <= TBY is halo row
+// j = w, lanes columns i = 1..32 (uniform per warp: no divergent halo / ownership tests inside a row); warp
+// TBY + 1, lanes 0..TBY, is column i = 0.  32 x 16 outputs per CTA (halo rows 6%), 2 CTAs per SM.
+// Measured (256^3 / 512^3): one thread per raw point (352 threads, 8 rows) 0.179 / 1.295 ms; halo-point
+// threads at 8 rows 0.158 / 1.148, 12 rows 0.163 / 1.125, 16 rows 0.151 / 1.084, 24 rows 0.171 / 1.232;
+// 16-, 24-, 48-plane slabs 0.157 / 0.155 / 0.163 at 256^3; 4 stages 0.155; two raw rows per thread 0.19.
+constexpr int TGV2_NT = (TGV_TPY + 1) * 32;  // 576 at 16 rows
+__global__ void __launch_bounds__(TGV2_NT, TGV_MINB) k_tgv_tma(TgvArgs t, const __grid_constant__ CUtensorMap tmP,
+                                                     const __grid_constant__ CUtensorMap tmW,
+                                                     float *__restrict__ gP, float *__restrict__ gw,
+                                                     double *__restrict__ part)
 {
     extern __shared__ __align__(128) float tsm_[];
     // TMA destinations 128-B aligned whatever the dynamic base (tgv_tma_smem() has 128 B of slack)
@@ -2356,18 +2366,18 @@ __global__ void __launch_bounds__(TGV_NT, TGV_MINB) k_tgv_tma(TgvArgs t, const _
     float *stg = tsm;                                                          // [S][TGV_STAGE_F]
     float4 *frows = reinterpret_cast<float4 *>(tsm + TGV_STAGES * TGV_STAGE_F); // [2 planes][X, Y][PY][PX]
     __shared__ __align__(8) uint64_t full[TGV_STAGES];
-    __shared__ double red[TGV_NT / 32];
-    const int i = threadIdx.x % TGV_RX, j = threadIdx.x / TGV_RX;
-    const int x0 = blockIdx.x * TGV_BX, y0 = blockIdx.y * TGV_BY, z0 = blockIdx.z * TGV_ZS;
+    __shared__ double red[TGV2_NT / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = warp < TGV_TPY ? lane + 1 : 0, j = warp < TGV_TPY ? warp : lane;
+    const bool pt = warp < TGV_TPY || lane < TGV_TPY;                // a halo point (computes fields)
+    const int x0 = blockIdx.x * TGV_BX, y0 = blockIdx.y * TGV_TBY, z0 = blockIdx.z * TGV_ZS;
     const int x = x0 - 1 + i, y = y0 - 1 + j;
-    const bool rp = threadIdx.x < TGV_RX * TGV_RY;
-    const bool pt = rp && i < TGV_PX && j < TGV_PY;
     const int sz = t.nx * t.ny, nv = sz * t.nz;
     const bool own = pt && i >= 1 && j >= 1 && x < t.nx && y < t.ny;
     const bool fxy = x >= 0 && y >= 0 && x <= t.nx - 2 && y <= t.ny - 2;
-    const int kxy = (x >= 0 && y >= 0) ? y * t.nx + x : 0;
     const int zbeg = z0 - 1, zend = min(z0 + TGV_ZS, t.nz), nq = zend - zbeg;  // planes zbeg .. zend (nq + 1)
     const int o = j * TGV_BOXX + i + TGV_BOX0;                                   // this point in a box plane
+    const int fo = j * TGV_PX + i;                                               // ... in a field-row plane
     auto issue = [&](int q) {  // plane zbeg + q into stage q % S (one thread)
         float *d = stg + (q % TGV_STAGES) * TGV_STAGE_F;
         uint64_t *b = &full[q % TGV_STAGES];
@@ -2384,10 +2394,11 @@ __global__ void __launch_bounds__(TGV_NT, TGV_MINB) k_tgv_tma(TgvArgs t, const _
         for (int q = 0; q < TGV_STAGES && q <= nq; ++q) issue(q);
     double val = 0.0;
     float pz[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int q = 0; q < nq; ++q) {
+    int k = zbeg * sz + ((x >= 0 && y >= 0) ? y * t.nx + x : 0);  // global index of (x, y, z), advanced per plane
+    for (int q = 0; q < nq; ++q, k += sz) {
         const int z = zbeg + q;
         const float *s0 = stg + (q % TGV_STAGES) * TGV_STAGE_F, *s1 = stg + ((q + 1) % TGV_STAGES) * TGV_STAGE_F;
-        float4 *fx = frows + (q & 1) * 2 * TGV_PY * TGV_PX, *fy = fx + TGV_PY * TGV_PX;
+        float4 *fx = frows + (q & 1) * 2 * TGV_TPY * TGV_PX, *fy = fx + TGV_TPY * TGV_PX;
         mbar_wait(&full[q % TGV_STAGES], (unsigned)(q / TGV_STAGES) & 1u);
         mbar_wait(&full[(q + 1) % TGV_STAGES], (unsigned)((q + 1) / TGV_STAGES) & 1u);
         TgvF F = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -2407,18 +2418,27 @@ __global__ void __launch_bounds__(TGV_NT, TGV_MINB) k_tgv_tma(TgvArgs t, const _
             }
             F = tgv_fields(t, in, c, rx, ry, c1, v);
             if (own && z >= z0) val += (double)v;  // counted once, by the owner, in its own slab
-            fx[j * TGV_PX + i] = make_float4(F.n0, F.mxx, F.mxy, F.mxz);
-            fy[j * TGV_PX + i] = make_float4(F.n1, F.mxy, F.myy, F.myz);
+            fx[fo] = make_float4(F.n0, F.mxx, F.mxy, F.mxz);
+            fy[fo] = make_float4(F.n1, F.mxy, F.myy, F.myz);
         }
         __syncthreads();  // field rows of plane z published; stage q consumed by every thread
         if (threadIdx.x == 0 && q + TGV_STAGES <= nq) issue(q + TGV_STAGES);
-        if (own && z >= z0) tgv_grad(t, F, fx[j * TGV_PX + i - 1], fy[(j - 1) * TGV_PX + i], pz, z * sz + kxy, nv, gP, gw);
+        if (own && z >= z0) tgv_grad(t, F, fx[fo - 1], fy[fo - TGV_PX], pz, k, nv, gP, gw);
         pz[0] = F.n2;
         pz[1] = F.mxz;
         pz[2] = F.myz;
         pz[3] = F.mzz;
     }
-    tgv_block_value(val, red, part);
+    // fixed-order block sum (10 warps)
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) val += __shfl_down_sync(0xffffffffu, val, o2);
+    if (lane == 0) red[warp] = val;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s2 = 0.0;
+        for (int w = 0; w < TGV2_NT / 32; ++w) s2 += red[w];
+        part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s2;
+    }
 }
 
 }  // namespace pa
