@@ -63,7 +63,7 @@ md = f"""# {tag} launch list — `python bench.py --steps 1 --warmup 3 --no-cpu 
 Cold-cache, serialised per-launch device times: compare shares, not absolutes. Setup launches included (one trace-mode forward for the synthetic measurements, k_count), then 3 warm-up + 1 timed pa_step. Raw CSV: `{os.path.basename(src)}`; per-pass DRAM: `{tag}_traffic_c4.json`.
 
 {summ}
-Per step: k_fwd_dep {ft / 1e3:.2f} s (1 launch), K2a+K2c {at / 1e3:.2f} s ({chunks} chunks), everything else < 2 ms; bench step {step_ms / 1e3:.2f} s (`{tag}_bench_c4.json`).
+Per step: k_fwd_dep {ft / 1e3:.2f} s (1 launch), K2a+K2c {at / 1e3:.2f} s ({chunks} chunks), everything else < 2 ms (the step of the ncu-run bench command, serialised by the profiler: {step_ms / 1e3:.2f} s; the bench line is `{tag}_bench_c4.json`).
 
 {out['note']}.
 """
