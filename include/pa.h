@@ -189,7 +189,8 @@ typedef struct {
     float beta1, beta2, eps;        /* Adam                                     */
     int32_t step;                   /* Adam step t >= 1 (bias correction)                         */
     int32_t loss_kind;              /* 0 MSE (Eq. 2), 1 NC (Eq. 3/4)                              */
-    int32_t update_p0, update_pose; /* apply the p0 / pose updates                                */
+    int32_t update_p0, update_pose; /* apply the p0 / pose updates (update_pose = 0 with grad_euler
+                                       NULL skips the pose gradient: the adjoint runs without it)  */
     float tgv_lambda;               /* Eq. 2 weight of the TGV^2 term (0 = off; R20)        */
     float tgv_alpha1, tgv_alpha0;   /* TGV^2 first / second order weights (R20)        */
     float tgv_eps;                  /* smoothing of the norms, phi(v) = sqrt(|v|^2+eps^2) - eps   */

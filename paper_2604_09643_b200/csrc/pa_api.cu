@@ -1394,6 +1394,7 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
     float *tg_w = use_tgv ? tg_p + nvox : nullptr;
     double *tg_parts = use_tgv ? reinterpret_cast<double *>(ws + o_tp) : nullptr;
     const unsigned long long *ok = nullptr;  // the step's degenerate verdict (device; read by the Adam kernels)
+    const bool want_pose = cfg->update_pose || grad_euler != nullptr;  // else the pose gradient is skipped
 
     if (F > 0) {
         ++g_nlaunch;
@@ -1410,11 +1411,20 @@ pa_status pa_step(pa_ctx *ctx, const pa_grid *grid, const pa_acq *acq, const flo
         ++g_nlaunch;
         k_rowloss_sum<<<1, 256, 0, st>>>(rl, (long long)F * E, loss, row_loss);
         CUDA_TRY(cudaGetLastError());
-        // a4 + a5 + a6 (records ev[1], ev[2])
-        if ((s = adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, gpose, nullptr, true, st, off))) return s;
-        ++g_nlaunch;
-        k_euler_grad<<<(F + 127) / 128, 128, 0, st>>>(gpose, dR, F, geul);
-        CUDA_TRY(cudaGetLastError());
+        if (want_pose) {
+            // a4 + a5 + a6 (records ev[1], ev[2])
+            if ((s = adjoint_pose_core(ctx, pl, tmpl, poses, p0, cot, grad_p0, gpose, nullptr, true, st, off))) return s;
+            ++g_nlaunch;
+            k_euler_grad<<<(F + 127) / 128, 128, 0, st>>>(gpose, dR, F, geul);
+            CUDA_TRY(cudaGetLastError());
+        } else {
+            // a4 only: no pose update and no dL/dEuler requested -> the adjoint kernels without the pose moment
+            AdjLaunch La;
+            CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+            if ((s = launch_adjoint(ctx, pl, false, true, poses, tmpl, p0, cot, grad_p0, nullptr, La, false, st))) return s;
+            CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
+            ctx->ev_adj = true;
+        }
     } else {
         CUDA_TRY(cudaMemsetAsync(grad_p0, 0, sizeof(float) * nvox, st));
         CUDA_TRY(cudaMemsetAsync(loss, 0, 2 * sizeof(float), st));

@@ -275,3 +275,29 @@ def test_pa_step_does_not_synchronise_the_host(ctx):
     dev_s = a.elapsed_time(b) / 1e3
     assert dev_s > 0.05 and host_s < 0.25 * dev_s, (host_s, dev_s)
     ctx.step_status()
+
+
+@pytest.mark.parametrize("loss_kind", [0, 1])
+def test_p0_only_step_skips_pose_gradient(ctx, loss_kind):
+    """update_pose = 0 with no grad_euler requested runs the adjoint without the pose moment (pa.h): grad_p0,
+    the loss and the p0 update are bitwise those of the same step with the pose gradient computed, the poses
+    are untouched, and fewer libpa kernels run (no pose reduction / Euler chain)."""
+    grid, acq, tmpl, meas, p0, e0 = small_problem(seed=11, F=3)
+    nv, F = p0.size, e0.shape[0]
+    cfg = dict(lr_p0=1e-2, lr_rot=1e-3, lr_trans=1e-3, step=1, update_p0=1, update_pose=0, loss_kind=loss_kind)
+
+    def run(want_euler):
+        g, L = torch.empty(nv, device="cuda"), torch.empty(2, device="cuda")
+        p, e = T(p0), T(e0)
+        geul = torch.empty((F, 6), device="cuda") if want_euler else None
+        n0 = ctx.launch_count()
+        ctx.step(grid, acq, T(tmpl), T(meas), p, e, torch.zeros(2 * nv, device="cuda"),
+                 torch.zeros(12 * F, device="cuda"), g, L, cfg, grad_euler=geul)
+        torch.cuda.synchronize()
+        return g, L, p, e, ctx.launch_count() - n0
+
+    g1, L1, p1, e1, n1 = run(True)
+    g2, L2, p2, e2, n2 = run(False)
+    assert torch.equal(g1, g2) and torch.equal(L1, L2) and torch.equal(p1, p2)
+    assert torch.equal(e2, T(e0)) and torch.equal(e1, T(e0))
+    assert n2 < n1
