@@ -35,7 +35,8 @@ LANES = 128
 # (c dt) (in-window samples per pair).  The direct kernels (exp / power-law families, Gaussian fallback) walk the
 # window: the survey's per-update basis x W.
 OPS_PAIR = {
-    "k_fwd_dep": 72.5,            # K1d: geometry + window 31.5, Horner channels 30, 8 ATOMS (7 words + count) + 3 address
+    "k_fwd_dep": 72.5,            # K1d at rank R = 5 (47.5 + 5 R in general, dep_ops below): geometry + window 31.5,
+                                  # Horner channels 4 R + 10, R + 3 ATOMS (R + 2 words + count) + 3 address
     "k_adjoint_tay2_8": 76.25,    # K2c, 32-B records: geometry 25 + series & moments 36 + gradient 8.5 + reduction 6.75
     "k_adjoint_tay2_12": 88.25,   # K2c, 48-B records (short windows): synthetic division 27 instead of 15
     "k_adjoint_svd": 84.0,        # K2s: geometry 25 + rank-R basis evaluation 44 + gradient 8.5 + reduction 6.75
@@ -383,7 +384,8 @@ def main():
     W = 2.0 * w.acq["kappa"] * w.acq["sigma"] / (w.acq["c"] * w.acq["dt"])  # in-window samples per pair
     U_rank = float(n_local)  # updates per pass on this rank (rank 0 prints; LPT keeps ranks within a frame)
     if plan["fwd_deposit"]:
-        fwd_name, fwd_ops = "k_fwd_dep (K1d, deposit-form forward + fused loss/cotangent)", OPS_PAIR["k_fwd_dep"] / W
+        fwd_name = f"k_fwd_dep (K1d, deposit-form forward + fused loss/cotangent, rank {plan['dep_rank']})"
+        fwd_ops = (47.5 + 5.0 * plan["dep_rank"]) / W
     else:
         fwd_name, fwd_ops = "k_forward (K1, direct forward + fused loss/cotangent)", fam["fwd"]
     if plan["adj_kernel"] == 2:

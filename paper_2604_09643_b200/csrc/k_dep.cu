@@ -50,7 +50,8 @@ pa_status launch_forward_dep(pa_ctx *ctx, const Plan &pl, const float *poses, co
 {
     if (pl.dep_R == 7) return launch_dep_r<7>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
     if (pl.dep_R == 6) return launch_dep_r<6>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
-    return launch_dep_r<5>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    if (pl.dep_R == 5) return launch_dep_r<5>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
+    return launch_dep_r<4>(ctx, pl, poses, tmpl, p0, out, mode, meas, mask, rowloss, st);
 }
 
 }  // namespace pa

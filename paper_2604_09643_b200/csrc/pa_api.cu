@@ -117,11 +117,15 @@ void make_tay(Plan &pl, int lmin, double a, double sig)
 // ~= sum_{m<R} phi_m(t) psi_m(k).  Chebyshev interpolation of degree 9 in t on 64 nodes, SVD of the
 // (coefficient x tap) matrix by one-sided Jacobi (fp64), phi_m converted to monomials and reduced
 // to 4 coefficients of its parity; the optional last tap (k = LMIN - MA) as a cubic in t.  The
-// error of exactly what the kernel evaluates is measured on a fine grid; rank 5 (6 for L_min <= 32,
-// where the adjoint K2s needs the more accurate derivative), raised to 6 / 7 while it misses the
-// bound; > 2e-7 of max|G| at rank 7 keeps the direct kernels.
+// error of exactly what the kernel evaluates is measured on a fine grid; the smallest rank from 4 up that
+// meets PA_DEP_MAXERR (r2 final: 2e-6 of max|G| per term, R24 — rank 4 at C4, 5 at C5; measured forward parity
+// <= 1.6e-6 relative L2 away from the near field, C4 forward -7% against rank 5 at 2e-7); the K2s-grade bound
+// 2e-7 from rank 5 (6 for L_min <= 32) when the adjoint uses the basis too; beyond rank 7 the direct kernels.
 #ifndef PA_DEP_MAXERR
-#define PA_DEP_MAXERR 2e-7
+#define PA_DEP_MAXERR 2e-6
+#endif
+#ifndef PA_DEP_MAXERR_SVD
+#define PA_DEP_MAXERR_SVD 2e-7
 #endif
 void make_dep(Plan &pl, int lmin, double a, double sig)
 {
@@ -139,7 +143,12 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
     pl.dep_nw = 0;
     pl.dep_g = 1;
     pl.dep_tpr = 4;
-    pl.dep_R = lmin <= 32 ? 6 : 5;
+    // the forward's bound (PA_DEP_MAXERR) from rank 4 up; when the adjoint runs in this basis (K2s: by policy,
+    // or because K2c's Taylor bounds fail) the tighter PA_DEP_MAXERR_SVD from rank 5 / 6 up, as K2s's pose moment
+    // (the basis' t-derivative) needs it
+    const bool svd_grade = (pl.policy & PA_POLICY_ADJ_SVD) || !pl.tay_ok;
+    const double maxerr = svd_grade ? PA_DEP_MAXERR_SVD : PA_DEP_MAXERR;
+    pl.dep_R = svd_grade ? (lmin <= 32 ? 6 : 5) : 4;
     auto G = [&](double t, int q) {  // tap q in [0, K): k = q - MA
         const double D = Dc + Dw * t - (double)(q - MA) * a;
         return D * std::exp(-D * D / (2.0 * sig * sig));
@@ -266,11 +275,11 @@ void make_dep(Plan &pl, int lmin, double a, double sig)
             err = std::max(err, std::fabs(GX(t) - xv));
         }
         pl.dep_err = err / gmax;
-        if (pl.dep_err <= PA_DEP_MAXERR || R == DEP_MAXR) break;
+        if (pl.dep_err <= maxerr || R == DEP_MAXR) break;
         ++R;  // the rank missed the bound: one more term
     }
     pl.dep_R = R;
-    pl.dep_ok = pl.dep_err <= PA_DEP_MAXERR;
+    pl.dep_ok = pl.dep_err <= maxerr;
     // the adjoint K2s: the same basis, unscaled, and the error of the derivative d/dt (pose moment)
     SvdConst &svc = pl.sv;
     for (int m = 0; m <= R; ++m)
@@ -507,7 +516,7 @@ pa_status make_plan(const pa_grid *grid, const pa_acq *acq, int E, int F, int po
     // the kernels this geometry runs (policy bits force / prefer alternatives; pa.h PA_POLICY_*)
     // K1d: 32-bit in-plane offsets (nx ny < 2^30)
     const bool dep_avail = fast && pl.dep_ok && pl.dep_nw > 0 && (long long)g.nx * g.ny < (1ll << 30);
-    const bool svd_avail = fast && pl.dep_ok && pl.svd_derr <= 1e-5;
+    const bool svd_avail = fast && pl.dep_ok && pl.dep_R >= 5 && pl.svd_derr <= 1e-5;  // K2s: ranks 5-7
     const bool tay_avail = fast && pl.tay_ok;
     pl.fwd_dep = dep_avail && !(policy & PA_POLICY_FWD_DIRECT);
     if (policy & PA_POLICY_ADJ_DIRECT) pl.adj = ADJ_DIRECT;

@@ -1455,10 +1455,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
                     chan(std::integral_constant<int, 1>{});
                     chan(std::integral_constant<int, 2>{});
                     chan(std::integral_constant<int, 3>{});
-                    chan(std::integral_constant<int, 4>{});
+                    if constexpr (R > 4) chan(std::integral_constant<int, 4>{});
                     if constexpr (R > 5) chan(std::integral_constant<int, 5>{});
                     if constexpr (R > 6) chan(std::integral_constant<int, 6>{});
-                    static_assert(R >= 5 && R <= 7, "rank 5, 6 or 7");
+                    static_assert(R >= 4 && R <= 7, "rank 4 to 7");
                     {  // X: the optional last tap (L = LMIN + 1), a cubic in t by Horner
                         const float2 cx = make_float2(Lxx ? ct.x : 0.0f, Lxy ? ct.y : 0.0f);
                         const float2 px = __ffma2_rn(__ffma2_rn(__ffma2_rn(dc.cf2[R][3], t, dc.cf2[R][2]), t, dc.cf2[R][1]), t, dc.cf2[R][0]);

@@ -73,9 +73,9 @@ def test_power_of_two_scale_is_exact(ctx):
     assert torch.equal(4.0 * y1, y4)
 
 
-# the fp32 row accumulators (NJ x (R + 1) floats) bound the deposit form: 6000 samples fit one 16-warp
-# CTA next to the round-accumulator ring, 10000 do not (direct K1)
-@pytest.mark.parametrize("nt,want_dep,want_warps", [(4096, 1, 16), (6000, 1, 16), (10000, 0, 0)])
+# the fp32 row accumulators (NJ x (R + 1) floats) bound the deposit form: at rank 4, 4096 samples fit two 8-warp
+# CTAs per SM, 6000 one 16-warp CTA next to the round-accumulator ring, 10000 do not (direct K1)
+@pytest.mark.parametrize("nt,want_dep,want_warps", [(4096, 1, 8), (6000, 1, 16), (10000, 0, 0)])
 def test_long_traces(ctx, nt, want_dep, want_warps, record_parity):
     grid = gen.make_grid((12, 10, 8), 0.2)
     acq = gen.make_acq(nt, 0.2, t0=0.0)

@@ -4,7 +4,7 @@ moment-filter adjoint's Taylor order (K2a/K2c), through pa_get_plan_info (host o
 The factorisation G(D_m, k) = D_k exp(-D_k^2/2 s^2) ~ sum_m phi_m(t) psi_m(k) is computed by libpa's
 host code (Chebyshev fit + one-sided Jacobi SVD, C++).  Here it is pinned by an independent numpy
 SVD of the same pulse family on a fine grid: the library's measured error must be within a small
-factor of the optimal (Eckart-Young) rank-R error, and below the 2e-7 bound the plan requires."""
+factor of the optimal (Eckart-Young) rank-R error, and below the 2e-6 bound the plan requires (R24)."""
 import numpy as np
 import pytest
 
@@ -34,9 +34,9 @@ def test_plan_of_baseline_configs(name):
     w = gen.workload(name, frames=2)
     info = plan_info(w.grid, w.acq, w.E)
     assert info["fwd_deposit"] == 1 and info["adj_taylor"] == 1, info
-    assert info["dep_rank"] in (5, 6)
+    assert info["dep_rank"] in (4, 5, 6)
     assert info["dep_warps"] in (8, 16)
-    assert 0.0 < info["dep_err"] <= 2e-7, info
+    assert 0.0 < info["dep_err"] <= 2e-6, info
     assert info["tay_err"] <= 4e-7, info
 
 
@@ -73,8 +73,8 @@ def test_factorisation_error_matches_independent_svd(sigma):
     assert info["dep_err"] <= 20.0 * opt + 1e-12, (info["dep_err"], opt)
     # ... and its reported error is a real measurement of a rank-R approximation, not a placeholder
     assert info["dep_err"] >= 0.2 * opt, (info["dep_err"], opt)
-    # one rank less would not meet the bound (the rank is the smallest that does)
-    assert optimal_rank_error(sigma, 5.0, info["dep_rank"] - 1, lmin) > 2e-8
+    # one rank less would not meet the bound (the rank is the smallest from 4 up that does)
+    assert info["dep_rank"] == 4 or optimal_rank_error(sigma, 5.0, info["dep_rank"] - 1, lmin) > 2e-7
 
 
 def test_other_families_use_direct_forward():
