@@ -1123,6 +1123,9 @@ struct DepConst {
 // |sum n| < 2^30).  Measured 1% faster at C4 than subtracting per deposit (124.6 vs 125.8 ms per 16 frames).
 #define PA_DEP_CNT 1
 #endif
+#ifndef PA_DEP_FASTLOAD
+#define PA_DEP_FASTLOAD 1  // K1d: unpredicated 64-bit amplitude loads for tiles inside the grid (even nx): C4 forward 114.2 -> 105.3 ms per 16 frames
+#endif
 #ifndef PA_DEP_MAP
 #define PA_DEP_MAP 2  // lane -> voxel map: 2 = two z-adjacent tiles per warp slot (default); 1 = one tile, 2x4x1 per lane; 0 = 2x2x2 cluster
 #endif
@@ -1352,6 +1355,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? PA_DEP_MINB : 1) k_fwd_dep(
         const bool okx1 = ix0 + 1 < g.nx, okz1 = iz0 + 1 < g.nz;
         const int ny_left = g.ny - iy0;  // rows of the lane's y run inside the grid
         const float *pb = p0 + (ok0 ? ((size_t)iz0 * (size_t)sz + (size_t)(iy0 * sy + ix0)) : (size_t)0);
+#if PA_DEP_MAP == 2 && PA_DEP_FASTLOAD
+        // the common case: all 8 voxels inside and an even row pitch (the x-pair 8-B aligned: ix0 is even) ->
+        // four unpredicated 64-bit loads along the lane's 4 rows
+        if (ok0 && okx1 && ny_left >= 4 && (sy & 1) == 0) {
+            const float2 *q = reinterpret_cast<const float2 *>(pb);
+            const int s2 = sy >> 1;
+            const float2 v0 = __ldg(q), v1 = __ldg(q + s2), v2 = __ldg(q + 2 * s2), v3 = __ldg(q + 3 * s2);
+            P[0] = v0.x; P[1] = v0.y; P[2] = v1.x; P[3] = v1.y;
+            P[4] = v2.x; P[5] = v2.y; P[6] = v3.x; P[7] = v3.y;
+            return;
+        }
+#endif
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
             const int vx = v & 1, vy = dyv(v), vz = dzv(v);
