@@ -246,9 +246,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PA_BENCH_BACKEND=gloo: a functional check of the multi-rank path on a box with fewer GPUs than ranks (ranks
+    # share devices, gloo carries the all-reduce; the timing of such a run is not a measurement)
+    backend = os.environ.get("PA_BENCH_BACKEND", "nccl")
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -470,7 +477,8 @@ def main():
         "ms_per_step": ms, "s_per_iteration": ms / 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded vascular phantom, freehand sweep; meas = forward at true poses)",
         "config": {"workload": describe(w), "kernel": args.kernel, "frames_per_rank": Fl, "updates_per_pass": U,
-                   "parallelism": f"frame-sharded x{world} (LPT on exact per-frame counts), NCCL all-reduce of dL/dp0",
+                   "parallelism": f"frame-sharded x{world} (LPT on exact per-frame counts), "
+                                  f"{'NCCL' if backend == 'nccl' or world == 1 else backend + ' (functional check)'} all-reduce of dL/dp0",
                    "plan": {k: plan[k] for k in ("lmin", "fwd_deposit", "dep_rank", "adj_kernel", "tay_order")},
                    "libpa_hash": src_hash,
                    "l2": "inputs larger than L2 (meas + cotangent per step) and a 256 MiB L2 flush before every timed step"},
